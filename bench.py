@@ -1,0 +1,280 @@
+"""Benchmark of the fused GPU sparse-MPM step (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C4] [--scale S]
+
+One JSON line on rank 0.  metric: particle-steps/s (BASELINE.json).  A "step"
+is one Simulation.step of the whole scene (inputs resident in HBM for
+`value`; through the public API from host buffers for `e2e`).  The default
+workload is C4 (the ~99M-particle landslide) on 1 GPU.
+`--impl reference` times the CPU oracle port of the reference path (the
+reference is Python/numba; oracle/ restates it in C + OpenMP) on a bounded
+sample of the same scene, with all host threads.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "particle-steps/sec"
+CONFIG_NAMES = {"C1": "granular_column", "C2": "two_spheres", "C3": "incline", "C4": "landslide"}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def make_scene(cfg_name, scale):
+    from paper_2605_28525_b200 import scenes
+
+    if cfg_name == "C4":
+        return scenes.landslide(x_stride=max(1, int(round(1.0 / scale))))
+    if cfg_name == "C3":
+        return scenes.incline()
+    if cfg_name == "C2":
+        return scenes.two_spheres(box="stress")
+    return scenes.granular_column()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample_scene(cfg_name):
+    """Bounded sample of the bench scene for the CPU port (10-30 s of work)."""
+    from paper_2605_28525_b200 import scenes
+
+    if cfg_name == "C4":
+        return scenes.landslide(x_stride=100), "landslide release zone, every 100th x column (~1M particles)"
+    if cfg_name == "C3":
+        return scenes.incline(h=0.04), "incline at h=0.04 (1/8 of the particles)"
+    return make_scene(cfg_name, 1.0), "full scene"
+
+
+def run_cpu_port(cfg_name, steps, threads=None):
+    """Time the oracle port of the reference's CPU scan path (S/bench.py:172-233
+    compute_total: stress, map_build, alloc_zero, p2g, grid_update, g2p)."""
+    from oracle import oracle as o
+
+    sc, desc = cpu_sample_scene(cfg_name)
+    threads = threads or len(os.sched_getaffinity(0))
+    sim = o.OracleSimulation(sc.particles, sc.config.h, sc.config.gravity, sc.materials, sc.boundaries,
+                             backend="scan", deterministic=False, threads=threads)
+    sim.step(count_nodes=False)  # warm (page-in)
+    total = 0.0
+    for _ in range(steps):
+        st = sim.step(count_nodes=False)
+        total += sum(st["times"][p] for p in o.COMPUTE_PHASES)
+    n = sc.particles.n
+    return {"value": n * steps / total, "unit": METRIC, "cores": threads, "kind": "port",
+            "sample": f"{desc}: {n} particles x {steps} steps, scan backend, {threads} OpenMP threads",
+            "ms_per_step": 1e3 * total / steps, "n_particles": n}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    base = run_cpu_port(args.config, max(1, min(args.steps, 3)))
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": METRIC, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak" if args.gpus > 1 else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "config": args.config},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": base["value"], "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def ours(args):
+    import torch
+
+    from paper_2605_28525_b200 import _lib
+    from paper_2605_28525_b200.solver import Simulation
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    sc = make_scene(args.config, args.scale)
+    n = sc.particles.n
+    # ---- value: device-resident state, K steps timed on the sim's stream
+    sim = Simulation(sc.particles, sc.config, sc.materials, sc.boundaries)
+    stream = sim.stream
+    for _ in range(args.warmup):
+        sim.step()
+    dts = []
+    fused_ms, grid_ms, map_ms, nalloc = [], [], [], []
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            st = sim.step()
+            dts.append(st.dt)
+            fused_ms.append(st.times["g2p"] * 1e3)
+            grid_ms.append(st.times["grid_update"] * 1e3)
+            map_ms.append(st.times["map_build"] * 1e3)
+            nalloc.append(st.n_allocated)
+        end.record(stream)
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = n * args.steps / (ms * 1e-3)
+    # ---- roofline of the dominant kernel (fused g2p->stress->p2g)
+    peak, peak_kind = measured_peaks()
+    n_alloc = float(np.mean(nalloc))
+    fused_bytes = 204.0 * n + 40.0 * n_alloc  # SURVEY 8d per-unit figures
+    f_ms = float(np.mean(fused_ms))
+    achieved = fused_bytes / (f_ms * 1e-3) / 1e9
+    step_bytes = 204.0 * n + 80.0 * n_alloc
+    traffic = None
+    tf = ROOT / "profiles" / "r01_fused_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(args.config)
+        except Exception:  # noqa: BLE001
+            traffic = None
+    del sim
+    torch.cuda.empty_cache()
+    # ---- e2e: public API from host buffers (upload + K steps + download x,v)
+    host = sc.particles
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sim2 = Simulation(host, sc.config, sc.materials, sc.boundaries)
+    stats_bytes = 0
+    for _ in range(args.steps):
+        sim2.step()
+        stats_bytes += 2 * 128 + 24  # DevStats x2 + error word + counters (pinned copies)
+    out_x = np.empty_like(host.x)
+    out_v = np.empty_like(host.v)
+    from paper_2605_28525_b200 import _lib as L
+
+    L.check(L.load().smpm_sim_get_particles(sim2._h, out_x.ctypes.data, out_v.ctypes.data, None, None, None, None))
+    t1 = time.perf_counter()
+    h2d = n * (24 + 24 + 72 + 72 + 8 + 8 + 8)
+    d2h = n * 48
+    e2e_value = n * args.steps / (t1 - t0)
+    del sim2
+    line = {
+        "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[args.config], "config": args.config, "n_particles": n,
+                   "h": sc.config.h, "ppc": 2, "mean_allocated_nodes": n_alloc,
+                   "l2": "inputs larger than L2 (state %.1f GB)" % (n * 242 / 1e9),
+                   "dt": "CFL bound (cfl=0.4)", "parallelism": f"slab{world}" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "k_g2p2g (G2P+F+return map+next P2G)",
+                     "peak_kind": peak_kind, "kernel_ms": f_ms,
+                     "step_frac": step_bytes / (ms / args.steps * 1e-3) / 1e9 / peak},
+        "phases_ms": {"map_build(scan+bin)": float(np.mean(map_ms)), "grid_update": float(np.mean(grid_ms)),
+                      "fused": f_ms},
+        "e2e": {"value": e2e_value, "unit": METRIC,
+                "h2d_bytes_per_step": int(h2d / args.steps) + 8,
+                "d2h_bytes_per_step": int(d2h / args.steps + stats_bytes / args.steps)},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = {k: v for k, v in run_cpu_port(args.config, 2).items()
+                                if k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIG_NAMES))
+    ap.add_argument("--scale", type=float, default=1.0, help="fraction of the C4 release columns")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,199 @@
+/*
+ * smpm.h -- C ABI of libsmpm.so, the sm_100a sparse-MPM hot path.
+ *
+ * Drop-in boundary for the reference's hash-backend time step
+ * (/root/reference/pkg/src/sparsempm/, cited file:line below).  Plain C types
+ * only: device pointers are `void*`/typed pointers obtained from any CUDA
+ * allocator (the Python host uses torch), streams are `void*` (cudaStream_t).
+ * Every function returns an int status (SMPM_OK or a code below) and never
+ * throws.  Host-pointer arguments are marked "host".
+ */
+#ifndef SMPM_H
+#define SMPM_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; map 1:1 onto the reference's exception classes
+ * (errors.py:4-21). */
+enum {
+  SMPM_OK = 0,
+  SMPM_ERR_NONFINITE_X = 1,   /* SimulationError (solver.py:1005-1006) */
+  SMPM_ERR_DEGENERATE_F = 2,  /* SimulationError (solver.py:1013-1020) */
+  SMPM_ERR_DT_BOUND = 3,      /* SimulationError (solver.py:1027-1030) */
+  SMPM_ERR_KEY_RANGE = 4,     /* KeyRangeError (sparse_hash.py:255-258) */
+  SMPM_ERR_INACTIVE = 5,      /* InactiveNodeError (solver.py:1053-1058) */
+  SMPM_ERR_CAPACITY = 6,      /* internal capacity overflow (handled by growth) */
+  SMPM_ERR_CONFIG = 20,       /* ConfigError (solver.py:776-810) */
+  SMPM_ERR_CUDA = 30,         /* CUDA runtime failure (message: smpm_last_error) */
+  SMPM_ERR_ARG = 31           /* invalid argument */
+};
+
+const char* smpm_last_error(void);
+int smpm_version(void);
+
+/* ------------------------------------------------------------------ hash
+ * Replaces BlockHashTable / _insert_key / _lookup_key / _insert_many
+ * (sparse_hash.py:43-167) and _insert_particle_blocks
+ * (sparse_hash.py:170-215).  keys: u64[n_slots] (EMPTY = all ones),
+ * vals: u32[n_slots] (EMPTY = 0xffffffff), n_slots a power of two.
+ * active_keys/slot_of_rank: [cap_blocks] rank -> key / slot. */
+typedef struct {
+  uint64_t* keys;
+  uint32_t* vals;
+  uint64_t n_slots;
+  uint32_t* counter;
+  uint32_t* overflow;
+  uint64_t* active_keys;
+  uint32_t* slot_of_rank;
+  uint32_t cap_blocks;
+  uint32_t pad;
+} smpm_hash_desc;
+
+int smpm_hash_clear(const smpm_hash_desc* h, void* stream);
+/* _insert_many (sparse_hash.py:101-106): ranks u32 out, fresh u8 out */
+int smpm_hash_insert_many(const smpm_hash_desc* h, const uint64_t* packed, int64_t n, uint32_t* ranks,
+                          uint8_t* fresh, void* stream);
+/* _lookup_key (sparse_hash.py:81-93); 0xffffffff for absent */
+int smpm_hash_lookup_many(const smpm_hash_desc* h, const uint64_t* packed, int64_t n, uint32_t* ranks,
+                          void* stream);
+/* _insert_particle_blocks (sparse_hash.py:170-191).  x: f64 (n,3).
+ * first_pos (optional, u64[n_slots], init all ones) receives the minimum
+ * p*27+corner encounter position per slot, which orders ranks exactly like
+ * the reference's serial (deterministic) build.  err: u64 error word. */
+int smpm_insert_particle_blocks(const smpm_hash_desc* h, const double* x, int64_t n, double inv_h,
+                                uint64_t* first_pos, unsigned long long* err, void* stream);
+/* Reorders ranks: mode 0 = by key (== scan backend order,
+ * sparse_scan.py:145-164), mode 1 = by first_pos (== serial hash build
+ * order).  Rewrites vals, active_keys and slot_of_rank.  n_blocks is read
+ * from h->counter.  scratch: >= 40 * cap_blocks bytes (device). */
+int smpm_hash_canonicalize(const smpm_hash_desc* h, int mode, const uint64_t* first_pos, void* scratch,
+                           void* stream);
+/* active_blocks() (sparse_hash.py:156-167): int32 (n,3) in rank order */
+int smpm_hash_active_blocks(const smpm_hash_desc* h, int64_t n_blocks, int32_t* blocks, void* stream);
+
+/* ------------------------------------------------------- module transfers
+ * Reference module API (solver.py:863-924, materials.py:250-267) over a hash
+ * map; fields are fp32 on the compact node range rank*64 + local. */
+typedef struct {
+  double h, inv_h;
+  double gravity[3];
+} smpm_stencil_params;
+
+/* bspline_weights (solver.py:80-92): base i64 (n,3), w/dw f64 (n,3,3) */
+int smpm_bspline(const double* x, int64_t n, double h, int64_t* base, double* w, double* dw, void* stream);
+/* p2g + grid_forces (solver.py:309-453).  Any of mass/mom/force may be NULL. */
+int smpm_p2g(const smpm_hash_desc* h, const smpm_stencil_params* sp, int64_t n, const double* x, const double* v,
+             const double* C, const double* m, const double* sigma, const double* jac, const double* V0,
+             float* mass, float* mom, float* force, unsigned long long* err, void* stream);
+
+typedef struct {
+  int32_t kind; /* 0 plane, 1 heightfield */
+  int32_t pad;
+  double mu;
+  double point[3];
+  double normal[3];
+} smpm_boundary;
+
+typedef struct {
+  double h, dt, mass_floor;
+  double gravity[3]; /* added as m*g; zero when force already holds gravity */
+  int32_t n_bc;
+  int32_t pad;
+  const smpm_boundary* bc;  /* host */
+  const double* hf_data;    /* host [nx][ny] or NULL */
+  int64_t hf_nx, hf_ny;
+  double hf_x0, hf_y0, hf_cell;
+} smpm_grid_params;
+
+/* _grid_update (solver.py:578-625): vel holds momentum on entry, velocity on
+ * exit.  active_blocks: int32 (n_blocks,3) device. */
+int smpm_grid_update(const smpm_grid_params* gp, int64_t n_nodes, float* mass, float* vel, const float* force,
+                     const int32_t* active_blocks, void* stream);
+/* _g2p (solver.py:628-732): x,v,C,F f64 in/out */
+int smpm_g2p(const smpm_hash_desc* h, const smpm_stencil_params* sp, double dt, int64_t n, double* x, double* v,
+             double* C, double* F, const float* vel, unsigned long long* err, void* stream);
+
+typedef struct {
+  double mu, lam, alpha;
+  int32_t kind; /* 0 elastic, 1 drucker_prager (materials.py:17-20) */
+  int32_t pad;
+} smpm_material;
+
+/* _stress_kernel (materials.py:169-238): F in/out, sigma/jac out */
+int smpm_stress(const smpm_material* mats /*host*/, int32_t n_mat, int64_t n, double* F, double* sigma, double* jac,
+                const int64_t* mat_id, unsigned long long* err, void* stream);
+/* count_active_nodes (solver.py:749-757): scratch hash given by h */
+int smpm_count_active_nodes(const smpm_hash_desc* h, const double* x, int64_t n, double inv_h, uint64_t* nodemask,
+                            unsigned long long* err, uint64_t* count_out /*host*/, void* stream);
+
+/* ------------------------------------------------------------ simulation
+ * Simulation.step with backend="hash" (solver.py:1001-1093) as one fused
+ * device pipeline.  The context owns the particle state (double-buffered,
+ * block-binned) and the sparse grid.  set/get take reference-layout f64
+ * arrays (host or device pointers). */
+typedef struct smpm_sim smpm_sim;
+
+typedef struct {
+  double h;
+  double gravity[3];
+  double cfl;
+  double wave_speed;  /* max over materials (solver.py:951) */
+  double mass_floor;  /* MASS_FLOOR_SCALE * max m (solver.py:952) */
+  int32_t n_mat;
+  int32_t n_bc;
+  const smpm_material* mats; /* host */
+  const smpm_boundary* bc;   /* host */
+  const double* hf_data;     /* host [nx][ny] or NULL */
+  int64_t hf_nx, hf_ny;
+  double hf_x0, hf_y0, hf_cell;
+  int64_t particle_capacity;
+  int64_t block_capacity;    /* 0: automatic */
+  int32_t deterministic;     /* ranks by key (scan order) */
+  int32_t record_conservation;
+  int32_t device;
+  int32_t pad;
+  void* stream;              /* cudaStream_t or NULL (own stream) */
+} smpm_sim_config;
+
+typedef struct {
+  int64_t step;
+  double t, dt;
+  int64_t n_active;     /* bit-exact |union of particle stencils| */
+  int64_t n_blocks;     /* allocated = n_blocks * 64 */
+  double vmax;          /* max |v| after the step (next dt bound) */
+  double mass_sum, mom_sum[3];
+  int32_t status;       /* SMPM_OK or error code */
+  int32_t pad;
+  int64_t err_particle; /* particle index for errors */
+  float ms_map, ms_grid, ms_fused, ms_total; /* device phase times */
+} smpm_step_stats;
+
+int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out);
+int smpm_sim_destroy(smpm_sim* s);
+/* ParticleSet fields (solver.py:95-132): x,v (n,3) f64; C,F (n,3,3) f64;
+ * m,V0 (n) f64; mat_id (n) i64. */
+int smpm_sim_set_particles(smpm_sim* s, int64_t n, const double* x, const double* v, const double* C,
+                           const double* F, const double* m, const double* V0, const int64_t* mat_id);
+/* Any output may be NULL; sigma/jac are evaluated from the current F. */
+int smpm_sim_get_particles(smpm_sim* s, double* x, double* v, double* C, double* F, double* sigma, double* jac);
+/* One step; dt <= 0 selects the CFL bound.  Asynchronous. */
+int smpm_sim_step(smpm_sim* s, double dt);
+/* Waits for the last step and returns its stats (status != 0 on error). */
+int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out);
+/* Active blocks (int32 (n,3), rank order) and nodal fields after the
+ * step's P2G: mass, momentum, force (f32, gravity included). Host pointers,
+ * sized by smpm_sim_sync's n_blocks. */
+int smpm_sim_query_grid(smpm_sim* s, int32_t* blocks, float* mass, float* mom, float* force);
+/* Block count of the grid smpm_sim_query_grid returns (runs a pending
+ * prologue). */
+int smpm_sim_grid_size(smpm_sim* s, int64_t* n_blocks);
+int64_t smpm_sim_num_particles(const smpm_sim* s);
+double smpm_sim_vmax(smpm_sim* s);
+int smpm_sim_launch_count(const smpm_sim* s, int64_t* kernels_per_step);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,375 @@
+// Shared device code for the sm_100a sparse-MPM hot path.
+//
+// Reference: /root/reference/pkg/src/sparsempm/ (cited as file:line).  This is
+// a from-scratch GPU design, not a translation: fp64 only where parity needs it
+// (block/base indexing, node positions, boundary predicates), fp32 elsewhere.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace smpm {
+
+// grid_index.py:14-20
+constexpr int64_t KEY_BIAS = int64_t(1) << 20;
+constexpr int COORD_MIN = -(1 << 20);
+constexpr int COORD_MAX = (1 << 20) - 1;
+constexpr uint64_t EMPTY_KEY = ~uint64_t(0);
+constexpr uint32_t EMPTY_VAL = 0xFFFFFFFFu;
+constexpr int BSZ = 4;  // block_size (solver.py:771); fixed: one u64 node mask per block
+
+// Error codes, ordered like the checks in Simulation.step (solver.py:1005-1085).
+// The device error word is atomicMin((code << 40) | particle).
+enum ErrCode : uint32_t {
+  ERR_NONE = 0,
+  ERR_NONFINITE_X = 1,   // SimulationError (solver.py:1005-1006)
+  ERR_DEGENERATE_F = 2,  // SimulationError (solver.py:1013-1020)
+  ERR_DT_BOUND = 3,      // SimulationError (solver.py:1027-1030)
+  ERR_KEY_RANGE = 4,     // KeyRangeError (sparse_hash.py:255-258)
+  ERR_INACTIVE = 5,      // InactiveNodeError (solver.py:1053-1058)
+  ERR_CAPACITY = 6,      // internal: block capacity exceeded -> host grows + replays
+};
+constexpr uint64_t ERR_CLEAR = ~uint64_t(0);
+__host__ __device__ inline uint64_t err_word(uint32_t code, uint64_t particle) {
+  return (uint64_t(code) << 40) | (particle & ((uint64_t(1) << 40) - 1));
+}
+
+// ------------------------------------------------------------------ keys
+// grid_index.py:100-105
+__host__ __device__ inline uint64_t pack_key(int bi, int bj, int bk) {
+  return (uint64_t(int64_t(bi) + KEY_BIAS) << 42) | (uint64_t(int64_t(bj) + KEY_BIAS) << 21) |
+         uint64_t(int64_t(bk) + KEY_BIAS);
+}
+// grid_index.py:108-113
+__host__ __device__ inline void unpack_key(uint64_t key, int& bi, int& bj, int& bk) {
+  const uint64_t m = (uint64_t(1) << 21) - 1;
+  bk = int(int64_t(key & m) - KEY_BIAS);
+  bj = int(int64_t((key >> 21) & m) - KEY_BIAS);
+  bi = int(int64_t((key >> 42) & m) - KEY_BIAS);
+}
+// grid_index.py:116-121 (SplitMix64 finaliser)
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// ------------------------------------------------------------ hash table
+// Open addressing with linear probing from mix64(key) & (H-1); the slot is
+// claimed by CAS(EMPTY -> key) and the claimant takes rank = fetch_add(counter)
+// and publishes it; a thread that finds the key already claimed waits for the
+// rank (sparse_hash.py:43-73).  Ranks are u32.  The table additionally records
+// rank -> key and rank -> slot so compaction and clearing are O(n_blocks).
+struct HashView {
+  uint64_t* keys;
+  uint32_t* vals;
+  uint32_t mask;           // n_slots - 1 (power of two)
+  uint32_t cap_blocks;     // ranks >= cap_blocks are flagged as capacity overflow
+  uint32_t* counter;       // number of ranks handed out
+  uint32_t* overflow;      // probe exhaustion or capacity overflow
+  uint64_t* active_keys;   // [cap_blocks] rank -> key
+  uint32_t* slot_of_rank;  // [cap_blocks] rank -> slot
+};
+
+__device__ inline uint32_t ld_volatile_u32(const uint32_t* p) { return *(const volatile uint32_t*)p; }
+__device__ inline uint64_t ld_volatile_u64(const uint64_t* p) { return *(const volatile uint64_t*)p; }
+
+// Returns the rank, or EMPTY_VAL when the table overflowed.  *fresh reports a
+// newly inserted key.
+__device__ inline uint32_t hash_insert(const HashView& h, uint64_t key, bool* fresh = nullptr) {
+  uint32_t s = uint32_t(mix64(key)) & h.mask;
+  for (uint32_t it = 0; it <= h.mask; ++it) {
+    uint64_t stored = ld_volatile_u64(&h.keys[s]);
+    if (stored == EMPTY_KEY) {
+      unsigned long long prev = atomicCAS((unsigned long long*)&h.keys[s], (unsigned long long)EMPTY_KEY,
+                                          (unsigned long long)key);
+      if (prev == EMPTY_KEY) {
+        uint32_t rank = atomicAdd(h.counter, 1u);
+        if (rank < h.cap_blocks) {
+          h.active_keys[rank] = key;
+          h.slot_of_rank[rank] = s;
+        } else {
+          atomicExch(h.overflow, 1u);
+        }
+        atomicExch(&h.vals[s], rank);
+        if (fresh) *fresh = true;
+        return rank;
+      }
+      stored = prev;
+    }
+    if (stored == key) {
+      uint32_t r;
+      while ((r = ld_volatile_u32(&h.vals[s])) == EMPTY_VAL) {
+      }
+      if (fresh) *fresh = false;
+      return r;
+    }
+    s = (s + 1) & h.mask;
+  }
+  atomicExch(h.overflow, 1u);
+  if (fresh) *fresh = false;
+  return EMPTY_VAL;
+}
+
+// sparse_hash.py:81-93 / grid_index.py:134-147
+__device__ inline uint32_t hash_lookup(const uint64_t* keys, const uint32_t* vals, uint32_t mask, uint64_t key) {
+  uint32_t s = uint32_t(mix64(key)) & mask;
+  for (uint32_t it = 0; it <= mask; ++it) {
+    uint64_t stored = keys[s];
+    if (stored == key) return vals[s];
+    if (stored == EMPTY_KEY) return EMPTY_VAL;
+    s = (s + 1) & mask;
+  }
+  return EMPTY_VAL;
+}
+
+// --------------------------------------------------------------- stencil
+// Base node floor(x*inv_h - 0.5) in fp64 without contraction, from the same
+// stored fp64 x and host inv_h = 1.0/h as the reference (solver.py:43-44,
+// sparse_hash.py:174-176), so the active block/node sets are bit-exact.  The
+// cell-relative offset d = u - base is then exact enough to carry in fp32.
+__device__ inline bool axis_base(double x, double inv_h, int& base, float& d) {
+  double u = __dmul_rn(x, inv_h);
+  double fb = floor(__dadd_rn(u, -0.5));
+  if (!(fabs(fb) < 4.0e6)) return false;  // also rejects NaN/inf
+  base = int(fb);
+  d = float(__dadd_rn(u, -fb));
+  return true;
+}
+
+// block-span range check of sparse_hash.py:177-186 for one axis
+__device__ inline bool axis_in_key_range(int base) {
+  return (base >> 2) >= COORD_MIN && ((base + 2) >> 2) <= COORD_MAX;
+}
+
+// Quadratic B-spline weights and d/du weights per axis (solver.py:46-51).
+__device__ inline void bspline(float d, float w[3], float g[3]) {
+  float t0 = 1.5f - d, t1 = d - 1.0f, t2 = d - 0.5f;
+  w[0] = 0.5f * t0 * t0;
+  w[1] = 0.75f - t1 * t1;
+  w[2] = 0.5f * t2 * t2;
+  g[0] = d - 1.5f;
+  g[1] = -2.0f * t1;
+  g[2] = t2;
+}
+
+// ------------------------------------------------------- constitutive model
+// Material table entry (materials.py:55-78 derived constants).
+struct Material {
+  float mu, lam, alpha, ratio;  // ratio = (3 lam + 2 mu) / (2 mu)
+  int kind;                     // 0 elastic, 1 Drucker-Prager
+  int pad[3];
+};
+
+__device__ inline void jacobi_rotate(float& app, float& arr, float& apr, float& aop, float& aor, float* q, int r0,
+                                     int r1) {
+  // materials.py:88-122 in fp32: annihilate a[r0][r1]
+  if (apr == 0.0f) return;
+  float theta = 0.5f * (arr - app) / apr;
+  float th2 = theta * theta;
+  float t = isinf(th2) ? 0.5f / fabsf(theta) : 1.0f / (fabsf(theta) + sqrtf(1.0f + th2));
+  if (theta < 0.0f) t = -t;
+  float c = rsqrtf(1.0f + t * t);
+  float s = t * c;
+  float tau = s / (1.0f + c);
+  app = app - t * apr;
+  arr = arr + t * apr;
+  apr = 0.0f;
+  float op = aop, orr = aor;
+  aop = op - s * (orr + tau * op);
+  aor = orr + s * (op - tau * orr);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float qip = q[3 * i + r0], qir = q[3 * i + r1];
+    q[3 * i + r0] = c * qip - s * qir;
+    q[3 * i + r1] = s * qip + c * qir;
+  }
+}
+
+// Hencky elasticity + cohesionless Drucker-Prager return map in principal
+// space (materials.py:169-238), fp32.  F is row-major 3x3.  Returns false on a
+// degenerate F.  Outputs the Kirchhoff stress tau = J sigma (xx,yy,zz,xy,xz,yz)
+// and J; when `project`, the return-mapped F is written back.
+__device__ inline bool hencky_dp(float F[9], const Material& mat, bool project, float tau[6], float& J) {
+  float det = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+              F[2] * (F[3] * F[7] - F[4] * F[6]);
+  if (!(det > 0.0f) || !isfinite(det)) return false;
+  // C = F^T F (materials.py:181-189)
+  float a00 = F[0] * F[0] + F[3] * F[3] + F[6] * F[6];
+  float a11 = F[1] * F[1] + F[4] * F[4] + F[7] * F[7];
+  float a22 = F[2] * F[2] + F[5] * F[5] + F[8] * F[8];
+  float a01 = F[0] * F[1] + F[3] * F[4] + F[6] * F[7];
+  float a02 = F[0] * F[2] + F[3] * F[5] + F[6] * F[8];
+  float a12 = F[1] * F[2] + F[4] * F[5] + F[7] * F[8];
+  float V[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+  // cyclic Jacobi (materials.py:125-144); fp32 stopping rule
+#pragma unroll 1
+  for (int sweep = 0; sweep < 8; ++sweep) {
+    float off = fabsf(a01) + fabsf(a02) + fabsf(a12);
+    float scale = fabsf(a00) + fabsf(a11) + fabsf(a22) + off;
+    if (off <= 1e-7f * scale) break;
+    jacobi_rotate(a00, a11, a01, a02, a12, V, 0, 1);  // o = 2: a[2][0], a[2][1]
+    jacobi_rotate(a00, a22, a02, a01, a12, V, 0, 2);  // o = 1: a[1][0], a[1][2]
+    jacobi_rotate(a11, a22, a12, a01, a02, V, 1, 2);  // o = 0: a[0][1], a[0][2]
+  }
+  if (!(a00 > 0.0f) || !(a11 > 0.0f) || !(a22 > 0.0f)) return false;
+  float lam3[3] = {a00, a11, a22};
+  float U[9];
+  float e[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float inv_s = rsqrtf(lam3[k]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      U[3 * i + k] = (F[3 * i] * V[k] + F[3 * i + 1] * V[3 + k] + F[3 * i + 2] * V[6 + k]) * inv_s;
+    e[k] = 0.5f * logf(lam3[k]);
+  }
+  if (mat.kind == 1) {
+    // materials.py:147-166
+    float tr = e[0] + e[1] + e[2];
+    bool changed = false;
+    if (tr > 0.0f) {
+      changed = (e[0] != 0.f) || (e[1] != 0.f) || (e[2] != 0.f);
+      e[0] = e[1] = e[2] = 0.0f;
+    } else {
+      float m = tr * (1.0f / 3.0f);
+      float h0 = e[0] - m, h1 = e[1] - m, h2 = e[2] - m;
+      float en = sqrtf(h0 * h0 + h1 * h1 + h2 * h2);
+      float dg = en + mat.alpha * mat.ratio * tr;
+      if (dg > 0.0f && en > 0.0f) {
+        float c = dg / en;
+        e[0] -= c * h0;
+        e[1] -= c * h1;
+        e[2] -= c * h2;
+        changed = true;
+      }
+    }
+    if (changed && project) {
+      float q0 = expf(e[0]), q1 = expf(e[1]), q2 = expf(e[2]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          F[3 * i + j] = U[3 * i] * q0 * V[3 * j] + U[3 * i + 1] * q1 * V[3 * j + 1] + U[3 * i + 2] * q2 * V[3 * j + 2];
+    }
+  }
+  float tr = e[0] + e[1] + e[2];
+  float t0 = 2.0f * mat.mu * e[0] + mat.lam * tr;
+  float t1 = 2.0f * mat.mu * e[1] + mat.lam * tr;
+  float t2 = 2.0f * mat.mu * e[2] + mat.lam * tr;
+  J = expf(tr);
+  // tau = sum_k t_k u_k u_k^T  (materials.py:233-238 times J)
+  tau[0] = t0 * U[0] * U[0] + t1 * U[1] * U[1] + t2 * U[2] * U[2];
+  tau[1] = t0 * U[3] * U[3] + t1 * U[4] * U[4] + t2 * U[5] * U[5];
+  tau[2] = t0 * U[6] * U[6] + t1 * U[7] * U[7] + t2 * U[8] * U[8];
+  tau[3] = t0 * U[0] * U[3] + t1 * U[1] * U[4] + t2 * U[2] * U[5];
+  tau[4] = t0 * U[0] * U[6] + t1 * U[1] * U[7] + t2 * U[2] * U[8];
+  tau[5] = t0 * U[3] * U[6] + t1 * U[4] * U[7] + t2 * U[5] * U[8];
+  return true;
+}
+
+// ------------------------------------------------------------ grid update
+// Boundary table (solver.py:841-860): kind 0 plane, 1 heightfield.
+struct Boundary {
+  double point[3];
+  double normal[3];
+  double mu;
+  int kind;
+  int pad;
+};
+struct Heightfield {
+  const double* data;  // [nx][ny]
+  int nx, ny;
+  double x0, y0, cell;
+};
+struct GridParams {
+  double h, dt, mass_floor;
+  double gravity[3];
+  int n_bc;
+  int pad;
+  const Boundary* bc;
+  Heightfield hf;
+};
+
+// solver.py:241-274 (bilinear, clamped), fp64 exact mirror
+__device__ inline void hf_sample(const Heightfield& hf, double x, double y, double& z, double& dzdx, double& dzdy) {
+  double fx = __ddiv_rn(__dadd_rn(x, -hf.x0), hf.cell), fy = __ddiv_rn(__dadd_rn(y, -hf.y0), hf.cell);
+  double fi = floor(fx), fj = floor(fy);
+  long long i0 = (long long)fi, j0 = (long long)fj;
+  if (i0 < 0) i0 = 0;
+  if (i0 > hf.nx - 2) i0 = hf.nx - 2;
+  if (j0 < 0) j0 = 0;
+  if (j0 > hf.ny - 2) j0 = hf.ny - 2;
+  double tx = __dadd_rn(fx, -double(i0)), ty = __dadd_rn(fy, -double(j0));
+  tx = tx < 0.0 ? 0.0 : (tx > 1.0 ? 1.0 : tx);
+  ty = ty < 0.0 ? 0.0 : (ty > 1.0 ? 1.0 : ty);
+  double z00 = hf.data[i0 * hf.ny + j0], z10 = hf.data[(i0 + 1) * hf.ny + j0];
+  double z01 = hf.data[i0 * hf.ny + j0 + 1], z11 = hf.data[(i0 + 1) * hf.ny + j0 + 1];
+  double omx = __dadd_rn(1.0, -tx), omy = __dadd_rn(1.0, -ty);
+  z = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(z00, omx), omy), __dmul_rn(__dmul_rn(z10, tx), omy)),
+                          __dmul_rn(__dmul_rn(z01, omx), ty)),
+                __dmul_rn(__dmul_rn(z11, tx), ty));
+  dzdx = __ddiv_rn(__dadd_rn(__dmul_rn(__dadd_rn(z10, -z00), omy), __dmul_rn(__dadd_rn(z11, -z01), ty)), hf.cell);
+  dzdy = __ddiv_rn(__dadd_rn(__dmul_rn(__dadd_rn(z01, -z00), omx), __dmul_rn(__dadd_rn(z11, -z10), tx)), hf.cell);
+}
+
+// solver.py:277-291
+__device__ inline void coulomb_project(double& v0, double& v1, double& v2, double n0, double n1, double n2,
+                                       double mu) {
+  double vn = v0 * n0 + v1 * n1 + v2 * n2;
+  if (vn >= 0.0) return;
+  double t0 = v0 - vn * n0, t1 = v1 - vn * n1, t2 = v2 - vn * n2;
+  double tn = sqrt(t0 * t0 + t1 * t1 + t2 * t2);
+  if (tn <= 0.0) {
+    v0 = v1 = v2 = 0.0;
+    return;
+  }
+  double scale = 1.0 + mu * vn / tn;
+  if (scale < 0.0) scale = 0.0;
+  v0 = scale * t0;
+  v1 = scale * t1;
+  v2 = scale * t2;
+}
+
+// One node of _grid_update (solver.py:578-625).  `force` excludes gravity
+// here; gravity enters as m*g (the scatter's sum_p w m g equals m_node g).
+// Node position and boundary predicates are fp64 and contraction-free, so the
+// plane / terrain decisions match the reference for the same node.
+__device__ inline void grid_node(const GridParams& gp, int nx, int ny, int nz, double m, double p0, double p1,
+                                 double p2, double f0, double f1, double f2, float& o0, float& o1, float& o2) {
+  if (m <= gp.mass_floor) {
+    o0 = o1 = o2 = 0.0f;
+    return;
+  }
+  double inv_m = 1.0 / m;
+  double v0 = (p0 + gp.dt * (f0 + m * gp.gravity[0])) * inv_m;
+  double v1 = (p1 + gp.dt * (f1 + m * gp.gravity[1])) * inv_m;
+  double v2 = (p2 + gp.dt * (f2 + m * gp.gravity[2])) * inv_m;
+  if (gp.n_bc > 0) {
+    double x0 = __dmul_rn(double(nx), gp.h), x1 = __dmul_rn(double(ny), gp.h), x2 = __dmul_rn(double(nz), gp.h);
+    for (int b = 0; b < gp.n_bc; ++b) {
+      const Boundary& bc = gp.bc[b];
+      if (bc.kind == 0) {
+        double sd = __dadd_rn(__dadd_rn(__dmul_rn(__dadd_rn(x0, -bc.point[0]), bc.normal[0]),
+                                        __dmul_rn(__dadd_rn(x1, -bc.point[1]), bc.normal[1])),
+                              __dmul_rn(__dadd_rn(x2, -bc.point[2]), bc.normal[2]));
+        if (sd <= 0.0) coulomb_project(v0, v1, v2, bc.normal[0], bc.normal[1], bc.normal[2], bc.mu);
+      } else {
+        double zs, zx, zy;
+        hf_sample(gp.hf, x0, x1, zs, zx, zy);
+        if (__dadd_rn(x2, -zs) <= 0.0) {
+          double il = 1.0 / sqrt(zx * zx + zy * zy + 1.0);
+          coulomb_project(v0, v1, v2, -zx * il, -zy * il, il, bc.mu);
+        }
+      }
+    }
+  }
+  o0 = float(v0);
+  o1 = float(v1);
+  o2 = float(v2);
+}
+
+__device__ inline void err_report(unsigned long long* err, uint32_t code, uint64_t particle) {
+  atomicMin(err, (unsigned long long)err_word(code, particle));
+}
+
+}  // namespace smpm

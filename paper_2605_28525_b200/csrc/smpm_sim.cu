@@ -1,0 +1,1591 @@
+// Fused sm_100a pipeline for Simulation.step with backend="hash"
+// (reference: /root/reference/pkg/src/sparsempm/solver.py:1001-1093).
+//
+// Per step (S = table of this step's particles, T = the other table):
+//   scan1(S)  block totals, n_active (popcount of node masks), dt, snapshot T
+//   scan2(S)  cell offsets + work items (block rank, slot group)
+//   bin(S)    perm[cell_off[key] + idx] = storage index
+//   grid(S)   momentum -> velocity + boundaries over active nodes; zero the
+//             accumulators; clear table T
+//   g2p2g(S -> T)  per work item: G2P from the smem velocity arena, F update,
+//             advection, Hencky/DP return map of the *next* step's stress,
+//             next-step block keys + node masks + bins, and the next step's
+//             P2G into a fixed-point int32 smem arena flushed with
+//             red.global.add.v4.f32.
+// The reference's step order stress -> map -> p2g -> grid -> g2p is the same
+// computation rotated: stress(n+1), map(n+1) and p2g(n+1) depend only on the
+// state G2P(n) writes, so they run in G2P(n)'s epilogue (a prologue kernel
+// does them for step 0 and after host-side edits).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/smpm.h"
+#include "smpm_common.cuh"
+#include "smpm_internal.h"
+
+namespace smpm {
+
+// ---------------------------------------------------------------- layout
+// Smem arenas use node address k + 8 j + 68 i: warp lanes are a 2x4x4 box of
+// distinct cells, so for any stencil offset the 32 lanes hit 32 distinct banks
+// (68 = 4 mod 32); measured 29 lane-atomics/clk/SM vs 8.6 for a naive layout
+// (profiles/r01_ubench_atomics.md).
+constexpr int AI = 68, AJ = 8;
+constexpr int SCAT_N = 8 * AI;   // scatter arena: nodes 4B-1 .. 4B+6 per axis
+constexpr int GATH_N = 6 * AI;   // gather arena: nodes 4B .. 4B+5 per axis
+constexpr int NF = 7;            // m, p0..2, f0..2
+constexpr int CTA = 256;         // 64 cells x 4 slots
+constexpr int SLOTS = 4;
+constexpr uint32_t MAGIC_BITS = 0x4B400000u;  // bits of 1.5 * 2^23
+constexpr float MAGIC = 12582912.0f;
+constexpr uint32_t BAD_KEY = 0xFFFFFFFFu;
+
+__device__ __forceinline__ int aaddr(int i, int j, int k) { return k + AJ * j + AI * i; }
+
+struct Particles {
+  double* x[3];
+  float* v[3];
+  float* C[9];
+  float* F[9];
+  float* m;
+  float* V0;
+  uint8_t* mat;
+  uint32_t* pid;
+};
+
+struct TableDev {
+  HashView hv;
+  uint64_t* nodemask;    // [cap_b]
+  uint32_t* cell_count;  // [cap_b*64]
+  uint32_t* cell_off;    // [cap_b*64]
+  uint32_t* block_total; // [cap_b]
+  uint32_t* block_items; // [cap_b]
+  uint2* items;          // [cap_items] (rank, group)
+  uint32_t* tile_sums;   // [3*max_tiles]
+  uint32_t* done;        // last-CTA counter
+  uint32_t* item_next;   // persistent-kernel work counter
+};
+
+// Device-side per-table statistics (the step whose particles are binned in
+// this table).
+struct DevStats {
+  unsigned long long err;   // shared error word lives in ctx; copy here
+  uint32_t n_blocks;
+  uint32_t n_items;
+  uint32_t overflow;
+  uint32_t vmax2_bits;      // max |v|^2 of the particles binned here
+  uint32_t prev_blocks;     // snapshot of the other table's block count
+  uint32_t n_binned;
+  unsigned long long n_active;
+  double dt;
+  double mass_sum, mom_sum[3];
+};
+
+struct StepParams {
+  double h, inv_h, dt_req, cfl, wave_speed;
+  int record_conservation;
+  int project;
+};
+
+// ------------------------------------------------------------------ scan
+constexpr int TB = 256;  // blocks per tile
+
+__device__ inline uint32_t warp_sum(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ inline uint32_t warp_max(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Exclusive CTA scan of one value per thread (256 threads).
+__device__ inline uint32_t cta_excl_scan(uint32_t v, uint32_t* sh /*[8]*/, uint32_t& total) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = lane < 8 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < 8) sh[lane] = s;
+  }
+  __syncthreads();
+  total = sh[7];
+  uint32_t base = w ? sh[w - 1] : 0;
+  uint32_t r = base + x - v;
+  __syncthreads();
+  return r;
+}
+
+// scan1: per block totals / items / popcount; per tile sums; the last CTA
+// scans tile sums and finalises the step scalars (dt, error checks).
+__global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
+                                               unsigned long long* err, StepParams sp) {
+  __shared__ uint32_t red[3][8];
+  __shared__ bool last;
+  const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
+  const int ntiles = (nb + TB - 1) / TB;
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t s_tot = 0, s_items = 0, s_pop = 0;
+    for (int b = w; b < TB; b += 8) {
+      uint32_t r = tile * TB + b;
+      if (r >= nb) break;
+      uint32_t c0 = S.cell_count[size_t(r) * 64 + lane], c1 = S.cell_count[size_t(r) * 64 + 32 + lane];
+      uint32_t tot = warp_sum(c0 + c1), mx = warp_max(max(c0, c1));
+      uint32_t items = (mx + SLOTS - 1) / SLOTS;
+      if (lane == 0) {
+        S.block_total[r] = tot;
+        S.block_items[r] = items;
+        s_tot += tot;
+        s_items += items;
+        s_pop += __popcll(S.nodemask[r]);
+      }
+    }
+    if (lane == 0) {
+      red[0][w] = s_tot;
+      red[1][w] = s_items;
+      red[2][w] = s_pop;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      uint32_t a = 0;
+      for (int i = 0; i < 8; ++i) a += red[threadIdx.x][i];
+      S.tile_sums[3 * tile + threadIdx.x] = a;
+    }
+    __syncthreads();
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(S.done, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // exclusive scan of tile sums (3 channels), 256 threads, loop over chunks
+  uint32_t carry[3] = {0, 0, 0};
+  __shared__ uint32_t sh[8];
+  unsigned long long n_active = 0;
+  for (int base = 0; base < ntiles; base += 256) {
+    int t = base + threadIdx.x;
+    for (int ch = 0; ch < 3; ++ch) {
+      uint32_t v = t < ntiles ? ((volatile uint32_t*)S.tile_sums)[3 * t + ch] : 0;
+      uint32_t tot;
+      uint32_t ex = cta_excl_scan(v, sh, tot);
+      if (t < ntiles && ch < 2) S.tile_sums[3 * t + ch] = ex + carry[ch];
+      if (ch == 2) n_active += tot;
+      carry[ch] += tot;
+    }
+  }
+  if (threadIdx.x == 0) {
+    *S.done = 0;
+    *S.item_next = 0;
+    DevStats* st = stS;
+    st->n_blocks = nb;
+    st->n_items = carry[1];
+    st->n_binned = carry[0];
+    st->n_active = n_active;
+    st->overflow = *S.hv.overflow | (*S.hv.counter > S.hv.cap_blocks ? 1u : 0u);
+    // dt is validated on the host against the CFL bound (solver.py:1021-1030)
+    st->dt = sp.dt_req;
+    st->mass_sum = 0.0;
+    st->mom_sum[0] = st->mom_sum[1] = st->mom_sum[2] = 0.0;
+    // snapshot + reset of the other table: it receives the next P2G
+    stT->prev_blocks = min(*T.hv.counter, T.hv.cap_blocks);
+    *T.hv.counter = 0;
+    *T.hv.overflow = 0;
+    stT->vmax2_bits = 0;
+  }
+}
+
+// scan2: cell offsets (particles sorted by block rank, then cell) and work
+// items (one per block and group of SLOTS particles per cell).
+__global__ void __launch_bounds__(256) k_scan2(TableDev S) {
+  __shared__ uint32_t sh[8];
+  __shared__ uint32_t boff[TB], ioff[TB];
+  const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
+  const int ntiles = (nb + TB - 1) / TB;
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t r = tile * TB + threadIdx.x;
+    uint32_t tot = r < nb ? S.block_total[r] : 0, it = r < nb ? S.block_items[r] : 0, t1, t2;
+    uint32_t e1 = cta_excl_scan(tot, sh, t1);
+    uint32_t e2 = cta_excl_scan(it, sh, t2);
+    boff[threadIdx.x] = e1 + S.tile_sums[3 * tile];
+    ioff[threadIdx.x] = e2 + S.tile_sums[3 * tile + 1];
+    __syncthreads();
+    for (int b = w; b < TB; b += 8) {
+      uint32_t rr = tile * TB + b;
+      if (rr >= nb) break;
+      uint32_t c0 = S.cell_count[size_t(rr) * 64 + lane], c1 = S.cell_count[size_t(rr) * 64 + 32 + lane];
+      uint32_t x0 = c0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x0, o);
+        if (lane >= o) x0 += y;
+      }
+      uint32_t sum0 = __shfl_sync(0xffffffffu, x0, 31);
+      uint32_t x1 = c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x1, o);
+        if (lane >= o) x1 += y;
+      }
+      S.cell_off[size_t(rr) * 64 + lane] = boff[b] + x0 - c0;
+      S.cell_off[size_t(rr) * 64 + 32 + lane] = boff[b] + sum0 + x1 - c1;
+      uint32_t nit = S.block_items[rr];
+      for (uint32_t g = lane; g < nit; g += 32) S.items[ioff[b] + g] = make_uint2(rr, g);
+    }
+    __syncthreads();
+  }
+}
+
+// bin: scatter storage indices into sorted positions
+__global__ void k_bin(const uint2* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    uint2 b = bin[i];
+    if (b.x == BAD_KEY) continue;
+    perm[S.cell_off[b.x] + b.y] = uint32_t(i);
+  }
+}
+
+// grid update over the active nodes of S (+ accumulator zeroing, clearing of
+// table T for reuse by the next P2G).
+__global__ void __launch_bounds__(256) k_grid(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
+                                              float4* __restrict__ acc, float4* __restrict__ gv, GridParams gp,
+                                              int record) {
+  const uint32_t nb = stS->n_blocks;
+  gp.dt = stS->dt;
+  const size_t nn = size_t(nb) * 64;
+  double msum = 0, p0s = 0, p1s = 0, p2s = 0;
+  for (size_t c = blockIdx.x * size_t(blockDim.x) + threadIdx.x; c < nn; c += size_t(gridDim.x) * blockDim.x) {
+    uint32_t r = uint32_t(c >> 6), l = uint32_t(c & 63);
+    float4 a = acc[2 * c], b = acc[2 * c + 1];
+    acc[2 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    acc[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int bi, bj, bk;
+    unpack_key(S.hv.active_keys[r], bi, bj, bk);
+    float o0, o1, o2;
+    grid_node(gp, bi * 4 + int(l >> 4), bj * 4 + int((l >> 2) & 3), bk * 4 + int(l & 3), a.x, a.y, a.z, a.w, b.x,
+              b.y, b.z, o0, o1, o2);
+    gv[c] = make_float4(o0, o1, o2, 0.f);
+    if (record) {
+      msum += a.x;
+      p0s += a.y;
+      p1s += a.z;
+      p2s += a.w;
+    }
+  }
+  if (record) {
+    for (int o = 16; o; o >>= 1) {
+      msum += __shfl_xor_sync(0xffffffffu, msum, o);
+      p0s += __shfl_xor_sync(0xffffffffu, p0s, o);
+      p1s += __shfl_xor_sync(0xffffffffu, p1s, o);
+      p2s += __shfl_xor_sync(0xffffffffu, p2s, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&stS->mass_sum, msum);
+      atomicAdd(&stS->mom_sum[0], p0s);
+      atomicAdd(&stS->mom_sum[1], p1s);
+      atomicAdd(&stS->mom_sum[2], p2s);
+    }
+  }
+  // clear table T (its blocks were the previous step's)
+  const uint32_t nbt = stT->prev_blocks;
+  for (size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x; r < nbt; r += size_t(gridDim.x) * blockDim.x) {
+    uint32_t s = T.hv.slot_of_rank[r];
+    T.hv.keys[s] = EMPTY_KEY;
+    T.hv.vals[s] = EMPTY_VAL;
+    T.nodemask[r] = 0;
+  }
+  for (size_t c = blockIdx.x * size_t(blockDim.x) + threadIdx.x; c < size_t(nbt) * 64;
+       c += size_t(gridDim.x) * blockDim.x)
+    T.cell_count[c] = 0;
+}
+
+// --------------------------------------------------------- prologue keys
+// Bins particles (arbitrary storage order) by the block of their base cell.
+__global__ void k_prologue_keys(Particles P, int64_t n, TableDev B, uint2* __restrict__ bin, double inv_h,
+                                unsigned long long* err) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    int base[3];
+    float d;
+    bool ok = true;
+    double xs[3] = {P.x[0][i], P.x[1][i], P.x[2][i]};
+    for (int a = 0; a < 3; ++a) {
+      if (!isfinite(xs[a])) {
+        err_report(err, ERR_NONFINITE_X, P.pid[i]);
+        ok = false;
+        break;
+      }
+      if (!axis_base(xs[a], inv_h, base[a], d) || !axis_in_key_range(base[a])) {
+        err_report(err, ERR_KEY_RANGE, P.pid[i]);
+        ok = false;
+        break;
+      }
+    }
+    if (!ok) {
+      bin[i] = make_uint2(BAD_KEY, 0);
+      continue;
+    }
+    uint64_t key = pack_key(base[0] >> 2, base[1] >> 2, base[2] >> 2);
+    uint32_t rank = hash_insert(B.hv, key);
+    if (rank >= B.hv.cap_blocks) {
+      bin[i] = make_uint2(BAD_KEY, 0);
+      continue;
+    }
+    uint32_t cell = uint32_t(((base[0] & 3) << 4) | ((base[1] & 3) << 2) | (base[2] & 3));
+    uint32_t key2 = rank * 64 + cell;
+    uint32_t idx = atomicAdd(&B.cell_count[key2], 1u);
+    bin[i] = make_uint2(key2, idx);
+  }
+}
+
+// ------------------------------------------------------------------ g2p2g
+struct FusedArgs {
+  Particles src, dst;
+  const uint32_t* perm;       // sorted position -> src index
+  TableDev B;                 // table of the particles' current blocks
+  TableDev S;                 // table receiving the next P2G
+  const float4* gv;           // grid velocity of B (float4 per node)
+  float4* acc;                // accumulators of S (2 float4 per node)
+  uint2* bin_out;             // bins of dst particles in S
+  const Material* mats;
+  int n_mat;
+  double h, inv_h;
+  const DevStats* stB;
+  DevStats* stS;
+  unsigned long long* err;
+  int project;
+};
+
+struct __align__(16) FusedSmem {
+  float gv[3][GATH_N];
+  int acc[NF][SCAT_N];
+  uint32_t cnt[SCAT_N];
+  uint32_t t1[SCAT_N];
+  uint32_t t2[SCAT_N];
+  uint32_t mask[27][2];
+  uint32_t rank[27];
+  uint32_t grank[8];
+  uint32_t bmax[3];
+  uint32_t item_r, item_g;
+  int bi, bj, bk;
+  Material mats[8];
+};
+
+__device__ __forceinline__ void red_v4(float4* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void sred(int* p, int v) {
+  asm volatile("red.shared.add.s32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int magic_q(float t) { return __float_as_int(t); }
+
+// power-of-two fixed-point scale for contributions bounded by b (b*S <= 2^21)
+__device__ __forceinline__ float fx_scale(float b, float& inv) {
+  int e = 0;
+  if (b > 0.f) frexpf(b, &e);
+  int s = 21 - e;
+  s = max(-100, min(100, s));
+  inv = ldexpf(1.0f, -s);
+  return ldexpf(1.0f, s);
+}
+
+// Global (slow-path) scatter of a particle that moved outside its block's
+// 8^3 arena: direct inserts and float atomics (rare: |dx| > 1 cell/step).
+__device__ void scatter_global(const FusedArgs& A, const int nb[3], const float d[3], float m, const float v[3],
+                               const float C[9], const float M[6], uint32_t pidv, uint2& binv) {
+  float w[3][3], g[3][3];
+  for (int a = 0; a < 3; ++a) bspline(d[a], w[a], g[a]);
+  const float h = float(A.h), ih = float(A.inv_h);
+  for (int oi = 0; oi < 3; ++oi)
+    for (int oj = 0; oj < 3; ++oj)
+      for (int ok = 0; ok < 3; ++ok) {
+        int n0 = nb[0] + oi, n1 = nb[1] + oj, n2 = nb[2] + ok;
+        uint32_t r = hash_insert(A.S.hv, pack_key(n0 >> 2, n1 >> 2, n2 >> 2));
+        if (r >= A.S.hv.cap_blocks) continue;
+        uint32_t l = uint32_t(((n0 & 3) << 4) | ((n1 & 3) << 2) | (n2 & 3));
+        float wk = w[0][oi] * w[1][oj] * w[2][ok];
+        float dx0 = (float(oi) - d[0]) * h, dx1 = (float(oj) - d[1]) * h, dx2 = (float(ok) - d[2]) * h;
+        float wm = wk * m;
+        float mv0 = v[0] + C[0] * dx0 + C[1] * dx1 + C[2] * dx2;
+        float mv1 = v[1] + C[3] * dx0 + C[4] * dx1 + C[5] * dx2;
+        float mv2 = v[2] + C[6] * dx0 + C[7] * dx1 + C[8] * dx2;
+        float gx = g[0][oi] * w[1][oj] * w[2][ok] * ih, gy = w[0][oi] * g[1][oj] * w[2][ok] * ih,
+              gz = w[0][oi] * w[1][oj] * g[2][ok] * ih;
+        float f0 = -(M[0] * gx + M[3] * gy + M[4] * gz);
+        float f1 = -(M[3] * gx + M[1] * gy + M[5] * gz);
+        float f2 = -(M[4] * gx + M[5] * gy + M[2] * gz);
+        size_t node = size_t(r) * 64 + l;
+        red_v4(&A.acc[2 * node], wm, wm * mv0, wm * mv1, wm * mv2);
+        red_v4(&A.acc[2 * node + 1], f0, f1, f2, 0.f);
+        atomicOr((unsigned long long*)&A.S.nodemask[r], 1ull << l);
+      }
+  uint32_t r = hash_insert(A.S.hv, pack_key(nb[0] >> 2, nb[1] >> 2, nb[2] >> 2));
+  if (r >= A.S.hv.cap_blocks) {
+    binv = make_uint2(BAD_KEY, 0);
+    return;
+  }
+  uint32_t cell = uint32_t(((nb[0] & 3) << 4) | ((nb[1] & 3) << 2) | (nb[2] & 3));
+  uint32_t key = r * 64 + cell;
+  binv = make_uint2(key, atomicAdd(&A.S.cell_count[key], 1u));
+  (void)pidv;
+}
+
+template <bool GATHER>
+__global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smraw);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < A.n_mat && i < 8; i += CTA) sm.mats[i] = A.mats[i];
+  const uint32_t n_items = A.stB->n_items;
+  const double dt = GATHER ? A.stB->dt : 0.0;
+  const float ih = float(A.inv_h);
+  const float hf_ = float(A.h);
+  uint32_t vmax2_local = 0;
+
+  while (true) {
+    __syncthreads();  // previous item's flush done before re-zeroing
+    if (tid == 0) {
+      uint32_t it = atomicAdd(A.B.item_next, 1u);
+      if (it < n_items) {
+        uint2 rg = A.B.items[it];
+        sm.item_r = rg.x;
+        sm.item_g = rg.y;
+        unpack_key(A.B.hv.active_keys[rg.x], sm.bi, sm.bj, sm.bk);
+      } else {
+        sm.item_r = BAD_KEY;
+      }
+    }
+    // zero arenas
+    for (int i = tid; i < NF * SCAT_N; i += CTA) (&sm.acc[0][0])[i] = 0;
+    for (int i = tid; i < SCAT_N; i += CTA) sm.cnt[i] = 0;
+    if (tid < 54) (&sm.mask[0][0])[tid] = 0;
+    if (tid < 3) sm.bmax[tid] = 0;
+    __syncthreads();
+    const uint32_t r = sm.item_r;
+    if (r == BAD_KEY) break;
+    const int B0 = sm.bi, B1 = sm.bj, B2 = sm.bk;
+    if (GATHER) {
+      if (tid < 8) {
+        int c0 = tid >> 2, c1 = (tid >> 1) & 1, c2 = tid & 1;
+        sm.grank[tid] = hash_lookup(A.B.hv.keys, A.B.hv.vals, A.B.hv.mask, pack_key(B0 + c0, B1 + c1, B2 + c2));
+      }
+      __syncthreads();
+      for (int n = tid; n < 216; n += CTA) {
+        int i = n / 36, j = (n / 6) % 6, k = n % 6;
+        uint32_t gr = sm.grank[((i >> 2) << 2) | ((j >> 2) << 1) | (k >> 2)];
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gr < A.B.hv.cap_blocks) v = A.gv[size_t(gr) * 64 + (((i & 3) << 4) | ((j & 3) << 2) | (k & 3))];
+        int ad = aaddr(i, j, k);
+        sm.gv[0][ad] = v.x;
+        sm.gv[1][ad] = v.y;
+        sm.gv[2][ad] = v.z;
+      }
+      __syncthreads();
+    }
+    // ---- particle of this thread
+    const int cell = tid & 63;
+    const uint32_t slot = sm.item_g * SLOTS + (tid >> 6);
+    const uint32_t key = r * 64 + cell;
+    const uint32_t cnt = A.B.cell_count[key];
+    const bool valid = slot < cnt;
+    uint32_t pos = 0, src = 0;
+    double xn[3];
+    float vn[3], Cn[9], M[6], m = 0.f, d1[3];
+    int nb[3], ab[3];
+    bool far = false, ok = valid;
+    float bm = 0.f, bp = 0.f, bf = 0.f;
+    if (valid) {
+      pos = A.B.cell_off[key] + slot;
+      src = A.perm[pos];
+      xn[0] = A.src.x[0][src];
+      xn[1] = A.src.x[1][src];
+      xn[2] = A.src.x[2][src];
+      float F[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) F[q] = A.src.F[q][src];
+      m = A.src.m[src];
+      const float V0 = A.src.V0[src];
+      const uint8_t mt = A.src.mat[src];
+      const uint32_t pidv = A.src.pid[src];
+      if (GATHER) {
+        // ---- G2P (solver.py:628-732) from the smem velocity arena
+        int lb[3];
+        float d[3], w[3][3], g[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          int bs;
+          axis_base(xn[a], A.inv_h, bs, d[a]);
+          bspline(d[a], w[a], g[a]);
+          lb[a] = bs - 4 * (a == 0 ? B0 : (a == 1 ? B1 : B2));
+        }
+        float v0 = 0, v1 = 0, v2 = 0;
+        float b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
+        float a00 = 0, a01 = 0, a02 = 0, a10 = 0, a11 = 0, a12 = 0, a20 = 0, a21 = 0, a22 = 0;
+        const float* g0p = &sm.gv[0][aaddr(lb[0], lb[1], lb[2])];
+        const float* g1p = &sm.gv[1][aaddr(lb[0], lb[1], lb[2])];
+        const float* g2p = &sm.gv[2][aaddr(lb[0], lb[1], lb[2])];
+        float wzd[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) wzd[k] = w[2][k] * (float(k) - d[2]);
+#pragma unroll
+        for (int oi = 0; oi < 3; ++oi) {
+#pragma unroll
+          for (int oj = 0; oj < 3; ++oj) {
+            float S0 = 0, S1 = 0, S2 = 0, T0 = 0, T1 = 0, T2 = 0, U0 = 0, U1 = 0, U2 = 0;
+#pragma unroll
+            for (int ok = 0; ok < 3; ++ok) {
+              int o = aaddr(oi, oj, ok);
+              float q0 = g0p[o], q1 = g1p[o], q2 = g2p[o];
+              S0 += w[2][ok] * q0;
+              S1 += w[2][ok] * q1;
+              S2 += w[2][ok] * q2;
+              T0 += wzd[ok] * q0;
+              T1 += wzd[ok] * q1;
+              T2 += wzd[ok] * q2;
+              U0 += g[2][ok] * q0;
+              U1 += g[2][ok] * q1;
+              U2 += g[2][ok] * q2;
+            }
+            float wij = w[0][oi] * w[1][oj];
+            float dxi = wij * (float(oi) - d[0]), dyj = wij * (float(oj) - d[1]);
+            float Ax = g[0][oi] * w[1][oj], Ay = w[0][oi] * g[1][oj];
+            v0 += wij * S0;
+            v1 += wij * S1;
+            v2 += wij * S2;
+            b00 += dxi * S0;
+            b10 += dxi * S1;
+            b20 += dxi * S2;
+            b01 += dyj * S0;
+            b11 += dyj * S1;
+            b21 += dyj * S2;
+            b02 += wij * T0;
+            b12 += wij * T1;
+            b22 += wij * T2;
+            a00 += Ax * S0;
+            a10 += Ax * S1;
+            a20 += Ax * S2;
+            a01 += Ay * S0;
+            a11 += Ay * S1;
+            a21 += Ay * S2;
+            a02 += wij * U0;
+            a12 += wij * U1;
+            a22 += wij * U2;
+          }
+        }
+        const float cs = 4.0f * ih;  // C = B * 4/h^2 with dx = h * (o - d)
+        Cn[0] = b00 * cs;
+        Cn[1] = b01 * cs;
+        Cn[2] = b02 * cs;
+        Cn[3] = b10 * cs;
+        Cn[4] = b11 * cs;
+        Cn[5] = b12 * cs;
+        Cn[6] = b20 * cs;
+        Cn[7] = b21 * cs;
+        Cn[8] = b22 * cs;
+        vn[0] = v0;
+        vn[1] = v1;
+        vn[2] = v2;
+        const float dth = float(dt) * ih;  // a = (sum v g) / h
+        float A9[9] = {a00 * dth, a01 * dth, a02 * dth, a10 * dth, a11 * dth, a12 * dth, a20 * dth, a21 * dth, a22 * dth};
+        float Fn[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            Fn[3 * i + j] = F[3 * i + j] + (A9[3 * i] * F[j] + A9[3 * i + 1] * F[3 + j] + A9[3 * i + 2] * F[6 + j]);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) F[q] = Fn[q];
+        xn[0] = __dadd_rn(xn[0], __dmul_rn(dt, double(v0)));
+        xn[1] = __dadd_rn(xn[1], __dmul_rn(dt, double(v1)));
+        xn[2] = __dadd_rn(xn[2], __dmul_rn(dt, double(v2)));
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) vn[a] = A.src.v[a][src];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Cn[q] = A.src.C[q][src];
+      }
+      // ---- stress of the next step (materials.py:169-238)
+      float tau[6], J;
+      const Material& mat = sm.mats[mt < 8 ? mt : 0];
+      if (!hencky_dp(F, mat, A.project != 0, tau, J)) {
+        err_report(A.err, ERR_DEGENERATE_F, pidv);
+        ok = false;
+        tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q) M[q] = V0 * tau[q];
+      // ---- write the particle at its sorted position (next storage order)
+      A.dst.x[0][pos] = xn[0];
+      A.dst.x[1][pos] = xn[1];
+      A.dst.x[2][pos] = xn[2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) A.dst.v[a][pos] = vn[a];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) A.dst.C[q][pos] = Cn[q];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) A.dst.F[q][pos] = F[q];
+      A.dst.m[pos] = m;
+      A.dst.V0[pos] = V0;
+      A.dst.mat[pos] = mt;
+      A.dst.pid[pos] = pidv;
+      float vv = vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2];
+      vmax2_local = max(vmax2_local, __float_as_uint(vv));
+      // ---- next step's keys
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (!isfinite(xn[a])) {
+          if (ok) err_report(A.err, ERR_NONFINITE_X, pidv);
+          ok = false;
+        } else if (!axis_base(xn[a], A.inv_h, nb[a], d1[a]) || !axis_in_key_range(nb[a])) {
+          if (ok) err_report(A.err, ERR_KEY_RANGE, pidv);
+          ok = false;
+        }
+      }
+      if (ok) {
+        ab[0] = nb[0] - (4 * B0 - 1);
+        ab[1] = nb[1] - (4 * B1 - 1);
+        ab[2] = nb[2] - (4 * B2 - 1);
+        far = ab[0] < 0 || ab[0] > 5 || ab[1] < 0 || ab[1] > 5 || ab[2] < 0 || ab[2] > 5;
+        float cm = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          cm = fmaxf(cm, fabsf(vn[a]) + 1.5f * hf_ * (fabsf(Cn[3 * a]) + fabsf(Cn[3 * a + 1]) + fabsf(Cn[3 * a + 2])));
+        float fm = fmaxf(fabsf(M[0]) + fabsf(M[3]) + fabsf(M[4]),
+                         fmaxf(fabsf(M[3]) + fabsf(M[1]) + fabsf(M[5]), fabsf(M[4]) + fabsf(M[5]) + fabsf(M[2])));
+        if (!far) {
+          bm = m * 0.421875f * 1.001f;
+          bp = m * 0.421875f * cm * 1.001f;
+          bf = fm * 0.5625f * ih * 1.001f;
+        }
+      }
+    }
+    // ---- block-wide maxima of the contribution bounds
+    {
+      uint32_t um = __float_as_uint(bm), up = __float_as_uint(bp), uf = __float_as_uint(bf);
+      um = warp_max(um);
+      up = warp_max(up);
+      uf = warp_max(uf);
+      if ((tid & 31) == 0) {
+        atomicMax(&sm.bmax[0], um);
+        atomicMax(&sm.bmax[1], up);
+        atomicMax(&sm.bmax[2], uf);
+      }
+    }
+    __syncthreads();
+    float iSm, iSp, iSf;
+    const float Sm = fx_scale(__uint_as_float(sm.bmax[0]), iSm);
+    const float Sp = fx_scale(__uint_as_float(sm.bmax[1]), iSp);
+    const float Sf = fx_scale(__uint_as_float(sm.bmax[2]), iSf);
+    uint32_t lidx = 0;
+    uint2 binv = make_uint2(BAD_KEY, 0);
+    if (ok && !far) {
+      // ---- P2G of the next step into the fixed-point arena
+      float w[3][3], g[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) bspline(d1[a], w[a], g[a]);
+      const int ad0 = aaddr(ab[0], ab[1], ab[2]);
+      lidx = atomicAdd(&sm.cnt[ad0], 1u);
+      const float mSm = m * Sm, mSp = m * Sp;
+      // force: f = -(M grad w); grad w = (g0 w1 w2, w0 g1 w2, w0 w1 g2)/h
+      const float fs = -Sf * ih;
+      const float Mh[6] = {M[0] * fs, M[1] * fs, M[2] * fs, M[3] * fs, M[4] * fs, M[5] * fs};
+      float cz[3][3];  // h * C_d2 * (ok - d2)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float dz = (float(k) - d1[2]) * hf_;
+        cz[0][k] = Cn[2] * dz;
+        cz[1][k] = Cn[5] * dz;
+        cz[2][k] = Cn[8] * dz;
+      }
+      int* a0 = &sm.acc[0][ad0];
+#pragma unroll
+      for (int oi = 0; oi < 3; ++oi) {
+        const float dx = (float(oi) - d1[0]) * hf_;
+#pragma unroll
+        for (int oj = 0; oj < 3; ++oj) {
+          const float dy = (float(oj) - d1[1]) * hf_;
+          const float wij = w[0][oi] * w[1][oj];
+          const float q0 = vn[0] + Cn[0] * dx + Cn[1] * dy;
+          const float q1 = vn[1] + Cn[3] * dx + Cn[4] * dy;
+          const float q2 = vn[2] + Cn[6] * dx + Cn[7] * dy;
+          const float Ax = g[0][oi] * w[1][oj], Ay = w[0][oi] * g[1][oj];
+          const float r0 = Mh[0] * Ax + Mh[3] * Ay, s0 = Mh[4] * wij;
+          const float r1 = Mh[3] * Ax + Mh[1] * Ay, s1 = Mh[5] * wij;
+          const float r2 = Mh[4] * Ax + Mh[5] * Ay, s2 = Mh[2] * wij;
+          const float wmm = wij * mSm, wmp = wij * mSp;
+#pragma unroll
+          for (int ok2 = 0; ok2 < 3; ++ok2) {
+            const int o = aaddr(oi, oj, ok2);
+            const float wz = w[2][ok2], gz = g[2][ok2];
+            const float cm = wmp * wz;
+            sred(a0 + o, magic_q(fmaf(wmm, wz, MAGIC)));
+            sred(a0 + 1 * SCAT_N + o, magic_q(fmaf(cm, q0 + cz[0][ok2], MAGIC)));
+            sred(a0 + 2 * SCAT_N + o, magic_q(fmaf(cm, q1 + cz[1][ok2], MAGIC)));
+            sred(a0 + 3 * SCAT_N + o, magic_q(fmaf(cm, q2 + cz[2][ok2], MAGIC)));
+            sred(a0 + 4 * SCAT_N + o, magic_q(fmaf(wz, r0, fmaf(gz, s0, MAGIC))));
+            sred(a0 + 5 * SCAT_N + o, magic_q(fmaf(wz, r1, fmaf(gz, s1, MAGIC))));
+            sred(a0 + 6 * SCAT_N + o, magic_q(fmaf(wz, r2, fmaf(gz, s2, MAGIC))));
+          }
+        }
+      }
+    } else if (ok && far) {
+      scatter_global(A, nb, d1, m, vn, Cn, M, 0, binv);
+    }
+    __syncthreads();
+    // ---- K(n) = number of contributions to node n: 3x3x3 box sum of the
+    // base-cell counts (separable), plus node masks of the 27 blocks
+    for (int n = tid; n < 512; n += CTA) {
+      int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
+      int ad = aaddr(i, j, k);
+      uint32_t s = sm.cnt[ad];
+      if (k >= 1) s += sm.cnt[ad - 1];
+      if (k >= 2) s += sm.cnt[ad - 2];
+      sm.t1[ad] = s;
+    }
+    __syncthreads();
+    for (int n = tid; n < 512; n += CTA) {
+      int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
+      int ad = aaddr(i, j, k);
+      uint32_t s = sm.t1[ad];
+      if (j >= 1) s += sm.t1[ad - AJ];
+      if (j >= 2) s += sm.t1[ad - 2 * AJ];
+      sm.t2[ad] = s;
+    }
+    __syncthreads();
+    for (int n = tid; n < 512; n += CTA) {
+      int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
+      int ad = aaddr(i, j, k);
+      uint32_t s = sm.t2[ad];
+      if (i >= 1) s += sm.t2[ad - AI];
+      if (i >= 2) s += sm.t2[ad - 2 * AI];
+      sm.t1[ad] = s;  // K
+      if (s) {
+        int di = (i + 3) >> 2, dj = (j + 3) >> 2, dk = (k + 3) >> 2;
+        int l = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
+        atomicOr(&sm.mask[di * 9 + dj * 3 + dk][l >> 5], 1u << (l & 31));
+      }
+    }
+    __syncthreads();
+    if (tid < 27) {
+      uint64_t mk = (uint64_t(sm.mask[tid][1]) << 32) | sm.mask[tid][0];
+      uint32_t rk = BAD_KEY;
+      if (mk) {
+        int di = tid / 9 - 1, dj = (tid / 3) % 3 - 1, dk = tid % 3 - 1;
+        rk = hash_insert(A.S.hv, pack_key(B0 + di, B1 + dj, B2 + dk));
+        if (rk < A.S.hv.cap_blocks) atomicOr((unsigned long long*)&A.S.nodemask[rk], (unsigned long long)mk);
+        else rk = BAD_KEY;
+      }
+      sm.rank[tid] = rk;
+    }
+    __syncthreads();
+    // ---- bin reservations per arena base cell (one global atomic per cell)
+    for (int n = tid; n < 216; n += CTA) {
+      int i = n / 36, j = (n / 6) % 6, k = n % 6;
+      int ad = aaddr(i, j, k);
+      uint32_t c = sm.cnt[ad];
+      if (c) {
+        int di = (i + 3) >> 2, dj = (j + 3) >> 2, dk = (k + 3) >> 2;
+        uint32_t rk = sm.rank[di * 9 + dj * 3 + dk];
+        uint32_t lc = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
+        sm.t2[ad] = rk == BAD_KEY ? BAD_KEY : rk * 64 + lc;
+        sm.cnt[ad] = rk == BAD_KEY ? 0 : atomicAdd(&A.S.cell_count[rk * 64 + lc], c);
+      }
+    }
+    __syncthreads();
+    if (valid) {
+      if (ok && !far) {
+        int ad0 = aaddr(ab[0], ab[1], ab[2]);
+        uint32_t k2 = sm.t2[ad0];
+        binv = k2 == BAD_KEY ? make_uint2(BAD_KEY, 0) : make_uint2(k2, sm.cnt[ad0] + lidx);
+      }
+      A.bin_out[pos] = binv;
+    }
+    // ---- flush the arena: value = (sum - K * MAGIC_BITS) / S
+    for (int n = tid; n < 512; n += CTA) {
+      int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
+      int ad = aaddr(i, j, k);
+      uint32_t K = sm.t1[ad];
+      if (!K) continue;
+      int di = (i + 3) >> 2, dj = (j + 3) >> 2, dk = (k + 3) >> 2;
+      uint32_t rk = sm.rank[di * 9 + dj * 3 + dk];
+      if (rk == BAD_KEY) continue;
+      int l = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
+      const uint32_t bias = K * MAGIC_BITS;
+      float vals[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) vals[f] = float(int(uint32_t(sm.acc[f][ad]) - bias));
+      size_t node = size_t(rk) * 64 + l;
+      red_v4(&A.acc[2 * node], vals[0] * iSm, vals[1] * iSp, vals[2] * iSp, vals[3] * iSp);
+      red_v4(&A.acc[2 * node + 1], vals[4] * iSf, vals[5] * iSf, vals[6] * iSf, 0.f);
+    }
+  }
+  vmax2_local = warp_max(vmax2_local);
+  if ((tid & 31) == 0 && vmax2_local) atomicMax(&A.stS->vmax2_bits, vmax2_local);
+}
+
+// ------------------------------------------------------- state transfer
+// Upload: reference layout f64 -> SoA (x f64, rest f32).
+__global__ void k_upload(Particles P, int64_t off, int64_t n, const double* __restrict__ x,
+                         const double* __restrict__ v, const double* __restrict__ C, const double* __restrict__ F,
+                         const double* __restrict__ m, const double* __restrict__ V0,
+                         const int64_t* __restrict__ mat) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t j = off + i;
+    for (int a = 0; a < 3; ++a) P.x[a][j] = x[3 * i + a];
+    for (int a = 0; a < 3; ++a) P.v[a][j] = float(v[3 * i + a]);
+    for (int q = 0; q < 9; ++q) P.C[q][j] = float(C[9 * i + q]);
+    for (int q = 0; q < 9; ++q) P.F[q][j] = float(F[9 * i + q]);
+    P.m[j] = float(m[i]);
+    P.V0[j] = float(V0[i]);
+    P.mat[j] = uint8_t(mat[i]);
+    P.pid[j] = uint32_t(j);
+  }
+}
+
+// Download: un-permute by pid into reference layout.  sigma/jac from F.
+__global__ void k_download(Particles P, int64_t n, int64_t lo, int64_t hi, double* x, double* v, double* C,
+                           double* F, double* sigma, double* jac, const Material* mats, int n_mat) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t p = P.pid[i];
+    if (p < lo || p >= hi) continue;
+    int64_t o = p - lo;
+    if (x)
+      for (int a = 0; a < 3; ++a) x[3 * o + a] = P.x[a][i];
+    if (v)
+      for (int a = 0; a < 3; ++a) v[3 * o + a] = P.v[a][i];
+    if (C)
+      for (int q = 0; q < 9; ++q) C[9 * o + q] = P.C[q][i];
+    float Fl[9];
+    for (int q = 0; q < 9; ++q) Fl[q] = P.F[q][i];
+    if (F)
+      for (int q = 0; q < 9; ++q) F[9 * o + q] = Fl[q];
+    if (sigma || jac) {
+      float tau[6], J = 1.f;
+      int mt = P.mat[i];
+      Material mm = mats[mt < n_mat ? mt : 0];
+      if (!hencky_dp(Fl, mm, false, tau, J)) {
+        for (int q = 0; q < 6; ++q) tau[q] = NAN;
+        J = NAN;
+      }
+      if (jac) jac[o] = J;
+      if (sigma) {
+        float iJ = 1.0f / J;
+        const int map[9] = {0, 3, 4, 3, 1, 5, 4, 5, 2};
+        for (int q = 0; q < 9; ++q) sigma[9 * o + q] = double(tau[map[q]] * iJ);
+      }
+    }
+  }
+}
+
+}  // namespace smpm
+
+// =================================================================== host
+using namespace smpm;
+
+struct smpm_sim {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double h = 0, inv_h = 0, cfl = 0.4, wave_speed = 0, mass_floor = 0;
+  double gravity[3] = {0, 0, 0};
+  int deterministic = 0, record = 0;
+  int64_t n = 0, cap_p = 0;
+  uint32_t cap_b = 0, cap_items = 0, max_tiles = 0;
+  uint64_t n_slots = 0;
+  // device buffers
+  std::vector<void*> allocs;
+  Particles state[2];
+  int cur = 0;  // state buffer holding the current particles
+  uint2* bin = nullptr;
+  uint32_t* perm = nullptr;
+  TableDev tab[2];
+  int S = 0;  // table holding the current particles' bins
+  float4* acc = nullptr;
+  float4* gv = nullptr;
+  DevStats* dstats = nullptr;  // [2]
+  unsigned long long* derr = nullptr;
+  Material* dmats = nullptr;
+  int n_mat = 0;
+  Boundary* dbc = nullptr;
+  int n_bc = 0;
+  double* dhf = nullptr;
+  Heightfield hf{};
+  // host
+  DevStats* hstats = nullptr;  // pinned [2]
+  unsigned long long* herr = nullptr;
+  int64_t step_count = 0;
+  double t = 0;
+  bool need_prologue = true;
+  bool prologue_project = true;
+  int pending_err = 0;
+  int64_t pending_particle = 0;
+  int persist_blocks = 0;
+  cudaEvent_t ev[5];
+  smpm_step_stats last{};
+  double vmax = 0;        // max |v| of the current particles (CFL bound input)
+  bool in_flight = false; // a step was launched and not yet synced
+  uint32_t* hcount = nullptr;  // pinned: counter/overflow of the table just filled
+  std::vector<smpm_material> host_mats;
+};
+
+namespace {
+thread_local char g_err[512] = "";
+}
+void smpm_internal_set_error(const char* msg) { snprintf(g_err, sizeof(g_err), "%s", msg); }
+namespace {
+int set_err(int code, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      snprintf(g_err, sizeof(g_err), "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+               __LINE__);                                                                          \
+      return SMPM_ERR_CUDA;                                                                        \
+    }                                                                                              \
+  } while (0)
+
+template <class T>
+int dalloc(smpm_sim* s, T** p, size_t count) {
+  void* q = nullptr;
+  CK(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
+  s->allocs.push_back(q);
+  *p = reinterpret_cast<T*>(q);
+  return SMPM_OK;
+}
+#define DA(ptr, count)                          \
+  do {                                          \
+    int rc_ = dalloc(s, &(ptr), (count));       \
+    if (rc_) return rc_;                        \
+  } while (0)
+
+float __uint_as_float_host(uint32_t u) {
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+uint64_t next_pow2(uint64_t v) {
+  uint64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+int alloc_particles(smpm_sim* s, Particles& P, int64_t cap) {
+  for (int a = 0; a < 3; ++a) DA(P.x[a], cap);
+  for (int a = 0; a < 3; ++a) DA(P.v[a], cap);
+  for (int q = 0; q < 9; ++q) DA(P.C[q], cap);
+  for (int q = 0; q < 9; ++q) DA(P.F[q], cap);
+  DA(P.m, cap);
+  DA(P.V0, cap);
+  DA(P.mat, cap);
+  DA(P.pid, cap);
+  return SMPM_OK;
+}
+
+int alloc_grid(smpm_sim* s) {
+  const uint32_t cb = s->cap_b;
+  s->n_slots = next_pow2(uint64_t(cb) * 4);
+  s->max_tiles = (cb + TB - 1) / TB;
+  for (int t = 0; t < 2; ++t) {
+    TableDev& T = s->tab[t];
+    DA(T.hv.keys, s->n_slots);
+    DA(T.hv.vals, s->n_slots);
+    DA(T.hv.counter, 4);
+    T.hv.overflow = T.hv.counter + 1;
+    T.done = T.hv.counter + 2;
+    T.item_next = T.hv.counter + 3;
+    DA(T.hv.active_keys, cb);
+    DA(T.hv.slot_of_rank, cb);
+    T.hv.mask = uint32_t(s->n_slots - 1);
+    T.hv.cap_blocks = cb;
+    DA(T.nodemask, cb);
+    DA(T.cell_count, size_t(cb) * 64);
+    DA(T.cell_off, size_t(cb) * 64);
+    DA(T.block_total, cb);
+    DA(T.block_items, cb);
+    DA(T.items, s->cap_items);
+    DA(T.tile_sums, 3 * size_t(s->max_tiles));
+    CK(cudaMemsetAsync(T.hv.keys, 0xFF, s->n_slots * 8, s->stream));
+    CK(cudaMemsetAsync(T.hv.vals, 0xFF, s->n_slots * 4, s->stream));
+    CK(cudaMemsetAsync(T.hv.counter, 0, 16, s->stream));
+    CK(cudaMemsetAsync(T.nodemask, 0, size_t(cb) * 8, s->stream));
+    CK(cudaMemsetAsync(T.cell_count, 0, size_t(cb) * 64 * 4, s->stream));
+  }
+  DA(s->acc, size_t(cb) * 64 * 2);
+  DA(s->gv, size_t(cb) * 64);
+  CK(cudaMemsetAsync(s->acc, 0, size_t(cb) * 64 * 32, s->stream));
+  return SMPM_OK;
+}
+
+size_t smem_bytes() { return sizeof(FusedSmem); }
+
+FusedArgs fused_args(smpm_sim* s, int B, int dstbuf, int project) {
+  FusedArgs A;
+  A.src = s->state[s->cur];
+  A.dst = s->state[dstbuf];
+  A.perm = s->perm;
+  A.B = s->tab[B];
+  A.S = s->tab[1 - B];
+  A.gv = s->gv;
+  A.acc = s->acc;
+  A.bin_out = s->bin;
+  A.mats = s->dmats;
+  A.n_mat = s->n_mat;
+  A.h = s->h;
+  A.inv_h = s->inv_h;
+  A.stB = s->dstats + B;
+  A.stS = s->dstats + (1 - B);
+  A.err = s->derr;
+  A.project = project;
+  return A;
+}
+
+StepParams step_params(smpm_sim* s, double dt) {
+  StepParams sp;
+  sp.h = s->h;
+  sp.inv_h = s->inv_h;
+  sp.dt_req = dt;
+  sp.cfl = s->cfl;
+  sp.wave_speed = s->wave_speed;
+  sp.record_conservation = s->record;
+  sp.project = 1;
+  return sp;
+}
+
+int scan_and_bin(smpm_sim* s, int Sx, double dt) {
+  StepParams sp = step_params(s, dt);
+  int grid = std::max(1, std::min<int>(s->max_tiles, 148 * 8));
+  k_scan1<<<grid, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp);
+  k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx]);
+  k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n, s->tab[Sx], s->perm);
+  CK(cudaGetLastError());
+  return SMPM_OK;
+}
+
+int launch_fused(smpm_sim* s, bool gather, int project) {
+  int dstbuf = 1 - s->cur;
+  FusedArgs A = fused_args(s, s->S, dstbuf, project);
+  size_t smem = smem_bytes();
+  if (gather)
+    k_g2p2g<true><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+  else
+    k_g2p2g<false><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+  CK(cudaGetLastError());
+  s->cur = dstbuf;
+  s->S = 1 - s->S;
+  return SMPM_OK;
+}
+
+GridParams grid_params(smpm_sim* s) {
+  GridParams gp;
+  gp.h = s->h;
+  gp.dt = 0;
+  gp.mass_floor = s->mass_floor;
+  for (int a = 0; a < 3; ++a) gp.gravity[a] = s->gravity[a];
+  gp.n_bc = s->n_bc;
+  gp.bc = s->dbc;
+  gp.hf = s->hf;
+  return gp;
+}
+
+// Capacity state of one table: returns the block count, or UINT32_MAX when the
+// table overflowed (probe exhaustion or more ranks than cap_b).
+int table_state(smpm_sim* s, int t, uint32_t* need, bool* over) {
+  uint32_t c[2];
+  CK(cudaMemcpyAsync(c, s->tab[t].hv.counter, 8, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  *need = std::max(*need, c[0]);
+  if (c[1] || c[0] > s->cap_b) *over = true;
+  return SMPM_OK;
+}
+
+int grow_grid(smpm_sim* s, uint32_t need) {
+  CK(cudaStreamSynchronize(s->stream));
+  std::vector<void*> grid_ptrs;
+  for (int t = 0; t < 2; ++t) {
+    TableDev& T = s->tab[t];
+    void* ps[] = {T.hv.keys, T.hv.vals, T.hv.counter, T.hv.active_keys, T.hv.slot_of_rank, T.nodemask,
+                  T.cell_count, T.cell_off, T.block_total, T.block_items, T.items, T.tile_sums};
+    for (void* p : ps) grid_ptrs.push_back(p);
+  }
+  grid_ptrs.push_back(s->acc);
+  grid_ptrs.push_back(s->gv);
+  std::vector<void*> keep;
+  for (void* p : s->allocs) {
+    if (std::find(grid_ptrs.begin(), grid_ptrs.end(), p) != grid_ptrs.end())
+      CK(cudaFree(p));
+    else
+      keep.push_back(p);
+  }
+  s->allocs = keep;
+  uint64_t nc = std::max<uint64_t>(uint64_t(s->cap_b) * 2, next_pow2(uint64_t(need) + need / 4));
+  if (nc > (1ull << 28)) return set_err(SMPM_ERR_CAPACITY, "block capacity exceeds 2^28");
+  s->cap_b = uint32_t(nc);
+  s->cap_items = uint32_t(std::min<uint64_t>(uint64_t(s->cap_p) / SLOTS + s->cap_b + 1024, 0xFFFFFFF0ull));
+  return alloc_grid(s);
+}
+
+int decode_err(unsigned long long w, int64_t* particle) {
+  if (w == ERR_CLEAR) return SMPM_OK;
+  *particle = int64_t(w & ((1ull << 40) - 1));
+  return int(w >> 40);
+}
+
+// Step 0 / after host edits / after a capacity overflow: reset both tables,
+// bin the current particles by block (keys -> scan -> bin) and run the P2G-only
+// variant of the fused kernel.  Synchronous; grows the grid until it fits.
+// Returns an error code (KeyRange / non-finite / degenerate) if detected.
+int run_prologue(smpm_sim* s, int project) {
+  for (int attempt = 0; attempt < 24; ++attempt) {
+    for (int t = 0; t < 2; ++t) {
+      TableDev& T = s->tab[t];
+      CK(cudaMemsetAsync(T.hv.keys, 0xFF, s->n_slots * 8, s->stream));
+      CK(cudaMemsetAsync(T.hv.vals, 0xFF, s->n_slots * 4, s->stream));
+      CK(cudaMemsetAsync(T.hv.counter, 0, 16, s->stream));
+      CK(cudaMemsetAsync(T.nodemask, 0, size_t(s->cap_b) * 8, s->stream));
+      CK(cudaMemsetAsync(T.cell_count, 0, size_t(s->cap_b) * 64 * 4, s->stream));
+    }
+    CK(cudaMemsetAsync(s->acc, 0, size_t(s->cap_b) * 64 * 32, s->stream));
+    CK(cudaMemsetAsync(s->dstats, 0, 2 * sizeof(DevStats), s->stream));
+    CK(cudaMemsetAsync(s->derr, 0xFF, 8, s->stream));
+    s->S = 0;
+    k_prologue_keys<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n, s->tab[0], s->bin, s->inv_h, s->derr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->herr, s->derr, 8, cudaMemcpyDeviceToHost, s->stream));
+    uint32_t need = 0;
+    bool over = false;
+    int rc = table_state(s, 0, &need, &over);
+    if (rc) return rc;
+    int64_t p = 0;
+    int code = decode_err(*s->herr, &p);
+    if (code) {
+      s->pending_err = code;
+      s->pending_particle = p;
+      return code;
+    }
+    if (over) {
+      rc = grow_grid(s, need);
+      if (rc) return rc;
+      continue;
+    }
+    rc = scan_and_bin(s, 0, 0.0);
+    if (rc) return rc;
+    // every binned particle is copied to the other buffer, so the swap in
+    // launch_fused keeps the full particle set even if the scatter overflows
+    rc = launch_fused(s, false, project);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(s->hstats, s->dstats, 2 * sizeof(DevStats), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(s->herr, s->derr, 8, cudaMemcpyDeviceToHost, s->stream));
+    need = 0;
+    rc = table_state(s, s->S, &need, &over);
+    if (rc) return rc;
+    code = decode_err(*s->herr, &p);
+    if (code) {
+      s->pending_err = code;
+      s->pending_particle = p;
+      return code;
+    }
+    if (over) {
+      rc = grow_grid(s, need);
+      if (rc) return rc;
+      project = 0;  // F is already return-mapped
+      continue;
+    }
+    s->vmax = std::sqrt(double(__uint_as_float_host(s->hstats[s->S].vmax2_bits)));
+    s->need_prologue = false;
+    return SMPM_OK;
+  }
+  return set_err(SMPM_ERR_CAPACITY, "capacity growth did not converge");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* smpm_last_error(void) { return g_err; }
+int smpm_version(void) { return 1; }
+
+int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
+  if (!cfg || !out) return set_err(SMPM_ERR_ARG, "null argument");
+  if (!(cfg->h > 0)) return set_err(SMPM_ERR_CONFIG, "grid cell size must be positive");
+  if (cfg->n_mat < 1 || cfg->n_mat > 8) return set_err(SMPM_ERR_CONFIG, "1..8 materials supported");
+  smpm_sim* s = new smpm_sim();
+  s->device = cfg->device;
+  CK(cudaSetDevice(s->device));
+  if (cfg->stream) {
+    s->stream = (cudaStream_t)cfg->stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    s->own_stream = true;
+  }
+  s->h = cfg->h;
+  s->inv_h = 1.0 / cfg->h;
+  s->cfl = cfg->cfl;
+  s->wave_speed = cfg->wave_speed;
+  s->mass_floor = cfg->mass_floor;
+  for (int a = 0; a < 3; ++a) s->gravity[a] = cfg->gravity[a];
+  s->deterministic = cfg->deterministic;
+  s->record = cfg->record_conservation;
+  s->cap_p = std::max<int64_t>(cfg->particle_capacity, 1);
+  // materials
+  s->n_mat = cfg->n_mat;
+  s->host_mats.assign(cfg->mats, cfg->mats + cfg->n_mat);
+  std::vector<Material> hm(cfg->n_mat);
+  for (int i = 0; i < cfg->n_mat; ++i) {
+    const smpm_material& m = cfg->mats[i];
+    hm[i].mu = float(m.mu);
+    hm[i].lam = float(m.lam);
+    hm[i].alpha = float(m.alpha);
+    hm[i].ratio = float((3.0 * m.lam + 2.0 * m.mu) / (2.0 * m.mu));
+    hm[i].kind = m.kind;
+  }
+  int rc = dalloc(s, &s->dmats, 8);
+  if (rc) return rc;
+  CK(cudaMemcpy(s->dmats, hm.data(), hm.size() * sizeof(Material), cudaMemcpyHostToDevice));
+  // boundaries
+  s->n_bc = cfg->n_bc;
+  std::vector<Boundary> hb(std::max(cfg->n_bc, 1));
+  for (int i = 0; i < cfg->n_bc; ++i) {
+    const smpm_boundary& b = cfg->bc[i];
+    hb[i].kind = b.kind;
+    hb[i].mu = b.mu;
+    for (int a = 0; a < 3; ++a) {
+      hb[i].point[a] = b.point[a];
+      hb[i].normal[a] = b.normal[a];
+    }
+  }
+  rc = dalloc(s, &s->dbc, hb.size());
+  if (rc) return rc;
+  CK(cudaMemcpy(s->dbc, hb.data(), hb.size() * sizeof(Boundary), cudaMemcpyHostToDevice));
+  if (cfg->hf_data && cfg->hf_nx >= 2 && cfg->hf_ny >= 2) {
+    rc = dalloc(s, &s->dhf, size_t(cfg->hf_nx * cfg->hf_ny));
+    if (rc) return rc;
+    CK(cudaMemcpy(s->dhf, cfg->hf_data, size_t(cfg->hf_nx * cfg->hf_ny) * 8, cudaMemcpyHostToDevice));
+    s->hf.data = s->dhf;
+    s->hf.nx = int(cfg->hf_nx);
+    s->hf.ny = int(cfg->hf_ny);
+    s->hf.x0 = cfg->hf_x0;
+    s->hf.y0 = cfg->hf_y0;
+    s->hf.cell = cfg->hf_cell;
+  }
+  // particles
+  for (int b = 0; b < 2; ++b) {
+    rc = alloc_particles(s, s->state[b], s->cap_p);
+    if (rc) return rc;
+  }
+  rc = dalloc(s, &s->bin, s->cap_p);
+  if (rc) return rc;
+  rc = dalloc(s, &s->perm, s->cap_p);
+  if (rc) return rc;
+  // grid
+  uint64_t cb = cfg->block_capacity > 0 ? uint64_t(cfg->block_capacity)
+                                        : next_pow2(std::max<uint64_t>(4096, uint64_t(s->cap_p) / 96));
+  s->cap_b = uint32_t(std::min<uint64_t>(cb, 1ull << 30));
+  s->cap_items = uint32_t(std::min<uint64_t>(uint64_t(s->cap_p) / SLOTS + s->cap_b + 1024, 0xFFFFFFF0ull));
+  rc = alloc_grid(s);
+  if (rc) return rc;
+  rc = dalloc(s, &s->dstats, 2);
+  if (rc) return rc;
+  rc = dalloc(s, &s->derr, 1);
+  if (rc) return rc;
+  CK(cudaMallocHost(&s->hstats, 2 * sizeof(DevStats)));
+  CK(cudaMallocHost(&s->herr, sizeof(unsigned long long)));
+  CK(cudaMallocHost(&s->hcount, 2 * sizeof(uint32_t)));
+  CK(cudaFuncSetAttribute(k_g2p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes())));
+  CK(cudaFuncSetAttribute(k_g2p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes())));
+  int occ = 0, sms = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<true>, CTA, smem_bytes()));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+  s->persist_blocks = std::max(1, occ) * sms;
+  for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&s->ev[i]));
+  *out = s;
+  return SMPM_OK;
+}
+
+int smpm_sim_destroy(smpm_sim* s) {
+  if (!s) return SMPM_OK;
+  cudaSetDevice(s->device);
+  cudaStreamSynchronize(s->stream);
+  for (void* p : s->allocs) cudaFree(p);
+  if (s->hstats) cudaFreeHost(s->hstats);
+  if (s->herr) cudaFreeHost(s->herr);
+  if (s->hcount) cudaFreeHost(s->hcount);
+  for (int i = 0; i < 5; ++i) cudaEventDestroy(s->ev[i]);
+  if (s->own_stream) cudaStreamDestroy(s->stream);
+  delete s;
+  return SMPM_OK;
+}
+
+int smpm_sim_set_particles(smpm_sim* s, int64_t n, const double* x, const double* v, const double* C,
+                           const double* F, const double* m, const double* V0, const int64_t* mat_id) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  if (n < 1) return set_err(SMPM_ERR_CONFIG, "simulation needs at least one particle");
+  if (n > s->cap_p) return set_err(SMPM_ERR_ARG, "particle count exceeds capacity");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  s->n = n;
+  s->cur = 0;
+  // staged chunks (inputs may be host or device memory)
+  const int64_t CH = 1 << 22;
+  double *sx, *sv, *sC, *sF, *sm, *sV;
+  int64_t* smat;
+  CK(cudaMallocAsync(&sx, CH * 3 * 8, s->stream));
+  CK(cudaMallocAsync(&sv, CH * 3 * 8, s->stream));
+  CK(cudaMallocAsync(&sC, CH * 9 * 8, s->stream));
+  CK(cudaMallocAsync(&sF, CH * 9 * 8, s->stream));
+  CK(cudaMallocAsync(&sm, CH * 8, s->stream));
+  CK(cudaMallocAsync(&sV, CH * 8, s->stream));
+  CK(cudaMallocAsync(&smat, CH * 8, s->stream));
+  for (int64_t off = 0; off < n; off += CH) {
+    int64_t c = std::min(CH, n - off);
+    CK(cudaMemcpyAsync(sx, x + 3 * off, c * 24, cudaMemcpyDefault, s->stream));
+    CK(cudaMemcpyAsync(sv, v + 3 * off, c * 24, cudaMemcpyDefault, s->stream));
+    CK(cudaMemcpyAsync(sC, C + 9 * off, c * 72, cudaMemcpyDefault, s->stream));
+    CK(cudaMemcpyAsync(sF, F + 9 * off, c * 72, cudaMemcpyDefault, s->stream));
+    CK(cudaMemcpyAsync(sm, m + off, c * 8, cudaMemcpyDefault, s->stream));
+    CK(cudaMemcpyAsync(sV, V0 + off, c * 8, cudaMemcpyDefault, s->stream));
+    CK(cudaMemcpyAsync(smat, mat_id + off, c * 8, cudaMemcpyDefault, s->stream));
+    k_upload<<<148 * 4, 256, 0, s->stream>>>(s->state[0], off, c, sx, sv, sC, sF, sm, sV, smat);
+    CK(cudaGetLastError());
+  }
+  CK(cudaFreeAsync(sx, s->stream));
+  CK(cudaFreeAsync(sv, s->stream));
+  CK(cudaFreeAsync(sC, s->stream));
+  CK(cudaFreeAsync(sF, s->stream));
+  CK(cudaFreeAsync(sm, s->stream));
+  CK(cudaFreeAsync(sV, s->stream));
+  CK(cudaFreeAsync(smat, s->stream));
+  s->need_prologue = true;
+  s->prologue_project = true;
+  s->pending_err = 0;
+  return SMPM_OK;
+}
+
+int smpm_sim_get_particles(smpm_sim* s, double* x, double* v, double* C, double* F, double* sigma, double* jac) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  const int64_t CH = 1 << 22;
+  const int64_t n = s->n;
+  double *sx = nullptr, *sv = nullptr, *sC = nullptr, *sF = nullptr, *ss = nullptr, *sj = nullptr;
+  if (x) CK(cudaMallocAsync(&sx, CH * 24, s->stream));
+  if (v) CK(cudaMallocAsync(&sv, CH * 24, s->stream));
+  if (C) CK(cudaMallocAsync(&sC, CH * 72, s->stream));
+  if (F) CK(cudaMallocAsync(&sF, CH * 72, s->stream));
+  if (sigma) CK(cudaMallocAsync(&ss, CH * 72, s->stream));
+  if (jac) CK(cudaMallocAsync(&sj, CH * 8, s->stream));
+  for (int64_t lo = 0; lo < n; lo += CH) {
+    int64_t c = std::min(CH, n - lo);
+    k_download<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], n, lo, lo + c, sx, sv, sC, sF, ss, sj, s->dmats,
+                                               s->n_mat);
+    CK(cudaGetLastError());
+    if (x) CK(cudaMemcpyAsync(x + 3 * lo, sx, c * 24, cudaMemcpyDefault, s->stream));
+    if (v) CK(cudaMemcpyAsync(v + 3 * lo, sv, c * 24, cudaMemcpyDefault, s->stream));
+    if (C) CK(cudaMemcpyAsync(C + 9 * lo, sC, c * 72, cudaMemcpyDefault, s->stream));
+    if (F) CK(cudaMemcpyAsync(F + 9 * lo, sF, c * 72, cudaMemcpyDefault, s->stream));
+    if (sigma) CK(cudaMemcpyAsync(sigma + 9 * lo, ss, c * 72, cudaMemcpyDefault, s->stream));
+    if (jac) CK(cudaMemcpyAsync(jac + lo, sj, c * 8, cudaMemcpyDefault, s->stream));
+  }
+  for (double* p : {sx, sv, sC, sF, ss, sj})
+    if (p) CK(cudaFreeAsync(p, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return SMPM_OK;
+}
+
+int smpm_sim_step(smpm_sim* s, double dt) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  if (s->n < 1) return set_err(SMPM_ERR_CONFIG, "no particles");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  if (s->pending_err) {
+    s->last.status = s->pending_err;
+    s->last.err_particle = s->pending_particle;
+    return s->pending_err;
+  }
+  if (s->need_prologue) {
+    int rc = run_prologue(s, s->prologue_project ? 1 : 0);
+    if (rc) {
+      s->last.status = rc;
+      s->last.err_particle = s->pending_particle;
+      return rc;
+    }
+    s->prologue_project = false;
+  }
+  // CFL bound and dt validation (solver.py:984-987, 1021-1030)
+  double bound = s->cfl * s->h / (s->wave_speed + s->vmax);
+  if (!(dt > 0)) dt = bound;
+  if (dt > bound * (1.0 + 1e-9)) {
+    s->last.status = SMPM_ERR_DT_BOUND;
+    s->last.dt = dt;
+    s->last.vmax = bound;  // reported by the caller's message
+    return set_err(SMPM_ERR_DT_BOUND, "timestep exceeds the stability bound");
+  }
+  const int Sx = s->S;
+  CK(cudaEventRecord(s->ev[0], s->stream));
+  int rc = scan_and_bin(s, Sx, dt);
+  if (rc) return rc;
+  CK(cudaEventRecord(s->ev[1], s->stream));
+  GridParams gp = grid_params(s);
+  k_grid<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
+                                         s->gv, gp, s->record);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(s->ev[2], s->stream));
+  rc = launch_fused(s, true, 1);
+  if (rc) return rc;
+  CK(cudaEventRecord(s->ev[3], s->stream));
+  CK(cudaMemcpyAsync(s->hstats, s->dstats, 2 * sizeof(DevStats), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->herr, s->derr, 8, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->hcount, s->tab[s->S].hv.counter, 8, cudaMemcpyDeviceToHost, s->stream));
+  s->in_flight = true;
+  return SMPM_OK;
+}
+
+int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  CK(cudaSetDevice(s->device));
+  CK(cudaStreamSynchronize(s->stream));
+  if (s->in_flight) {
+    s->in_flight = false;
+    const int Sx = 1 - s->S;  // table of the step just completed
+    const DevStats& st = s->hstats[Sx];
+    const DevStats& nx = s->hstats[s->S];
+    int64_t p = 0;
+    int code = decode_err(*s->herr, &p);
+    smpm_step_stats r{};
+    r.dt = st.dt;
+    r.n_active = int64_t(st.n_active);
+    r.n_blocks = int64_t(st.n_blocks);
+    s->vmax = std::sqrt(double(__uint_as_float_host(nx.vmax2_bits)));
+    r.vmax = s->vmax;
+    r.mass_sum = st.mass_sum;
+    for (int a = 0; a < 3; ++a) r.mom_sum[a] = st.mom_sum[a];
+    cudaEventElapsedTime(&r.ms_map, s->ev[0], s->ev[1]);
+    cudaEventElapsedTime(&r.ms_grid, s->ev[1], s->ev[2]);
+    cudaEventElapsedTime(&r.ms_fused, s->ev[2], s->ev[3]);
+    cudaEventElapsedTime(&r.ms_total, s->ev[0], s->ev[3]);
+    s->step_count += 1;
+    s->t += st.dt;
+    r.step = s->step_count;
+    r.t = s->t;
+    r.status = SMPM_OK;
+    if (code) {  // raised by the next step (reference order: stress/map of step n+1)
+      s->pending_err = code;
+      s->pending_particle = p;
+    } else if (s->hcount[1] || s->hcount[0] > s->cap_b) {
+      int rc = grow_grid(s, s->hcount[0]);
+      if (rc) return rc;
+      s->need_prologue = true;
+      s->prologue_project = false;
+    }
+    s->last = r;
+  }
+  if (out) *out = s->last;
+  return SMPM_OK;
+}
+
+int smpm_sim_query_grid(smpm_sim* s, int32_t* blocks, float* mass, float* mom, float* force) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  if (s->need_prologue) {
+    int rc = run_prologue(s, s->prologue_project ? 1 : 0);
+    if (rc) return rc;
+    s->prologue_project = false;
+  }
+  CK(cudaStreamSynchronize(s->stream));
+  const TableDev& T = s->tab[s->S];
+  uint32_t nb;
+  CK(cudaMemcpy(&nb, T.hv.counter, 4, cudaMemcpyDeviceToHost));
+  nb = std::min(nb, s->cap_b);
+  std::vector<uint64_t> keys(nb);
+  std::vector<float> a(size_t(nb) * 64 * 8);
+  CK(cudaMemcpy(keys.data(), T.hv.active_keys, size_t(nb) * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(a.data(), s->acc, a.size() * 4, cudaMemcpyDeviceToHost));
+  for (uint32_t r = 0; r < nb; ++r) {
+    int bi, bj, bk;
+    unpack_key(keys[r], bi, bj, bk);
+    if (blocks) {
+      blocks[3 * r] = bi;
+      blocks[3 * r + 1] = bj;
+      blocks[3 * r + 2] = bk;
+    }
+    for (int l = 0; l < 64; ++l) {
+      const float* q = &a[(size_t(r) * 64 + l) * 8];
+      size_t o = size_t(r) * 64 + l;
+      if (mass) mass[o] = q[0];
+      if (mom)
+        for (int d = 0; d < 3; ++d) mom[3 * o + d] = q[1 + d];
+      if (force)
+        for (int d = 0; d < 3; ++d) force[3 * o + d] = float(double(q[4 + d]) + double(q[0]) * s->gravity[d]);
+    }
+  }
+  return SMPM_OK;
+}
+
+int smpm_sim_grid_size(smpm_sim* s, int64_t* n_blocks) {
+  if (!s || !n_blocks) return set_err(SMPM_ERR_ARG, "null argument");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  if (s->need_prologue) {
+    int rc = run_prologue(s, s->prologue_project ? 1 : 0);
+    if (rc) return rc;
+    s->prologue_project = false;
+  }
+  uint32_t nb;
+  CK(cudaMemcpy(&nb, s->tab[s->S].hv.counter, 4, cudaMemcpyDeviceToHost));
+  *n_blocks = std::min(nb, s->cap_b);
+  return SMPM_OK;
+}
+
+int64_t smpm_sim_num_particles(const smpm_sim* s) { return s ? s->n : 0; }
+
+double smpm_sim_vmax(smpm_sim* s) {
+  if (!s) return 0;
+  if (s->in_flight) smpm_sim_sync(s, nullptr);
+  if (s->need_prologue && !s->pending_err) run_prologue(s, s->prologue_project ? 1 : 0), s->prologue_project = false;
+  return s->vmax;
+}
+
+int smpm_sim_launch_count(const smpm_sim* s, int64_t* kernels_per_step) {
+  if (kernels_per_step) *kernels_per_step = 5;  // scan1, scan2, bin, grid, g2p2g
+  return s ? SMPM_OK : SMPM_ERR_ARG;
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+"""Module-level GPU kernels vs the oracle / reference golden vectors.
+
+Integer work (keys, hash ranks, active sets, node counts) is bit-exact.
+Floating point is fp32 on the device vs fp64 in the reference; tolerances are
+norm-wise and stated per quantity.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2605_28525_b200 import grid_index as gi  # noqa: E402
+from paper_2605_28525_b200 import solver as S  # noqa: E402
+from paper_2605_28525_b200.materials import MaterialModel, update_stress  # noqa: E402
+from paper_2605_28525_b200.sparse_hash import BlockHashTable, build_hash_sparse_grid  # noqa: E402
+from tests.test_oracle_golden import _PS, _boundaries, _materials  # noqa: E402
+
+
+def normwise(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def keyed(blocks, values, width):
+    """node-coordinate keyed dict view of compact fields"""
+    b = np.asarray(blocks, dtype=np.int64)
+    local = np.stack(np.meshgrid(range(4), range(4), range(4), indexing="ij"), -1).reshape(-1, 3)
+    nodes = (b[:, None, :] * 4 + local[None]).reshape(-1, 3)
+    keys = gi.pack_keys(nodes)
+    order = np.argsort(keys)
+    return keys[order], np.asarray(values).reshape(-1, width)[order]
+
+
+def test_hash_insert_sequence_matches_reference(golden):
+    g = golden("hash")
+    t = BlockHashTable(8192)
+    ranks, fresh = t.insert_many(gi.pack_keys(g["ins_blocks"][:1]))
+    out_r, out_f = [int(ranks[0])], [bool(fresh[0])]
+    for b in g["ins_blocks"][1:]:
+        r, f = t.insert(tuple(b))
+        out_r.append(r)
+        out_f.append(f)
+    assert np.array_equal(np.array(out_r), g["ins_ranks"])
+    assert np.array_equal(np.array(out_f), g["ins_fresh"])
+    assert np.array_equal(t.keys, g["ins_keys"])
+    assert np.array_equal(t.vals, g["ins_vals"])
+    assert t.lookup((999, 0, 0)) == -1
+
+
+def test_hash_concurrent_unique_winner():
+    rng = np.random.default_rng(0)
+    blocks = rng.integers(-30, 30, size=(200_000, 3))
+    keys = gi.pack_keys(blocks)
+    t = BlockHashTable(1 << 16)
+    ranks, fresh = t.insert_many(keys)
+    uniq = np.unique(keys)
+    assert t.count == uniq.shape[0]
+    assert int(fresh.sum()) == uniq.shape[0]
+    # every occurrence of a key got the same rank; ranks are a permutation
+    first = {}
+    for k, r in zip(keys[:20000], ranks[:20000]):
+        assert first.setdefault(int(k), int(r)) == int(r)
+    assert np.array_equal(np.sort(np.unique(ranks)), np.arange(uniq.shape[0]))
+    ab = t.active_blocks()
+    assert np.array_equal(gi.pack_keys(ab)[ranks], keys)
+
+
+def test_hash_overflow_flag():
+    t = BlockHashTable(2)
+    r, f = t.insert_many(gi.pack_keys([(0, 0, 0), (1, 0, 0), (2, 0, 0)]))
+    assert t.overflowed
+    assert (r == -1).sum() == 1
+
+
+def test_build_matches_reference_orders(golden):
+    g = golden("hash")
+    x, h = g["cloud_x"], float(g["cloud_h"])
+    hm = build_hash_sparse_grid(x, h, 4, deterministic=True)
+    assert np.array_equal(hm.active_blocks, g["hash_active"])
+    km = build_hash_sparse_grid(x, h, 4, rank_order="key")
+    assert np.array_equal(km.active_blocks, g["scan_active"])
+    pm = build_hash_sparse_grid(x, h, 4)  # concurrent ranks: same set
+    assert np.array_equal(np.sort(gi.pack_keys(pm.active_blocks)), np.sort(gi.pack_keys(g["scan_active"])))
+    r2 = build_hash_sparse_grid(x, h, 4, initial_capacity=64, deterministic=True)
+    assert np.array_equal(r2.active_blocks, g["rebuild_active"])
+    assert r2.table.n_slots == int(g["rebuild_capacity"])
+    for nd in g["nodes"][:50]:
+        try:
+            hm.node_index(nd)
+            ok = True
+        except KeyError:
+            ok = False
+        assert ok == (km.block_index(gi.block_of(nd)) >= 0)
+
+
+def test_count_active_nodes_bit_exact(golden):
+    g = golden("count")
+    for i in range(4):
+        assert S.count_active_nodes(g[f"x{i}"], float(g[f"h{i}"])) == int(g[f"count{i}"])
+    assert S.count_active_nodes(np.array([[0.53, 0.51, 0.49]]), 0.1) == 27
+
+
+def test_bspline(golden):
+    g = golden("stencil")
+    for i in range(0, g["x"].shape[0], 7):
+        b, w, dw = S.bspline_weights(g["x"][i], g["h"][i])
+        assert np.array_equal(b, g["base"][i])
+        np.testing.assert_allclose(w, g["w"][i], atol=2e-7)
+        np.testing.assert_allclose(dw, g["dw"][i], atol=3e-7 / g["h"][i])
+
+
+def test_stress_vs_reference(golden):
+    g = golden("phases")
+    ps = _PS(g)
+    update_stress(ps, _materials())
+    assert normwise(ps.F, g["st_F"]) < 1e-6
+    assert normwise(ps.sigma, g["st_sigma"]) < 1e-4
+    assert normwise(ps.jac, g["st_jac"]) < 1e-6
+
+
+def test_degenerate_F_raises():
+    from paper_2605_28525_b200.errors import SimulationError
+
+    ps = S.ParticleSet.from_samples(np.zeros((3, 3)), np.ones(3), 1.0)
+    ps.F[1] = 0.0
+    with pytest.raises(SimulationError, match="particle 1"):
+        update_stress(ps, _materials()[:1])
+
+
+def test_transfers_vs_reference(golden, oracle):
+    g = golden("phases")
+    h = float(g["h"])
+    ps = _PS(g)
+    ps.F[...] = g["st_F"]
+    ps.sigma = g["st_sigma"].copy()
+    ps.jac = g["st_jac"].copy()
+    amap = build_hash_sparse_grid(ps.x, h, 4, rank_order="key")
+    assert np.array_equal(amap.active_blocks, g["map_active"])  # key order == scan order
+    f = S.p2g(ps, amap, h)
+    S.grid_forces(ps, amap, h, g["gravity"], fields=f)
+    assert normwise(f.mass, g["p2g_mass"]) < 1e-6
+    assert normwise(f.vel, g["p2g_mom"]) < 1e-5
+    assert normwise(f.force, g["p2g_force"]) < 1e-5
+    # grid update from the reference's own P2G output
+    ref = S.NodalFields(mass=g["p2g_mass"].copy(), vel=g["p2g_mom"].copy(), force=g["p2g_force"].copy())
+    S.grid_update(ref, amap, h, float(g["dt"]), float(g["mass_floor"]), _boundaries())
+    heavy = g["p2g_mass"] > 1e-3 * g["p2g_mass"].max()
+    assert normwise(ref.vel[heavy], g["gu_vel"][heavy]) < 1e-5
+    # g2p from the reference's grid velocities
+    ref.vel[...] = g["gu_vel"]
+    S.g2p(ps, amap, ref, h, float(g["dt"]))
+    assert np.abs(ps.x - g["g2p_x"]).max() < 1e-5 * np.abs(g["g2p_x"]).max()
+    assert normwise(ps.v, g["g2p_v"]) < 1e-5
+    assert normwise(ps.C, g["g2p_C"]) < 1e-4
+    assert normwise(ps.F, g["g2p_F"]) < 1e-5
+
+
+def test_friction_projection():
+    out = S.apply_friction_boundary([1.0, 0.0, -1.0], [0, 0, 1], 0.5)
+    np.testing.assert_allclose(out, [0.5, 0.0, 0.0], atol=1e-7)
+    out = S.apply_friction_boundary([1.0, 2.0, 3.0], [0, 0, 1], 0.5)
+    np.testing.assert_allclose(out, [1.0, 2.0, 3.0], atol=1e-7)
+    out = S.apply_friction_boundary([0.1, 0.0, -1.0], [0, 0, 1], 0.5)
+    np.testing.assert_allclose(out, [0.0, 0.0, 0.0], atol=1e-7)

@@ -1,0 +1,176 @@
+"""Simulation.step (fused GPU pipeline) vs the oracle, step by step.
+
+Each step starts both sides from the same state (the GPU state is fed to
+the oracle), so tolerances are per step: active block set, n_blocks and
+n_active bit-exact; grid mass/momentum and particle x/v norm-wise fp32
+tolerances; C/F/force looser."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2605_28525_b200 import grid_index as gi  # noqa: E402
+from paper_2605_28525_b200 import scenes  # noqa: E402
+from paper_2605_28525_b200.errors import SimulationError  # noqa: E402
+from paper_2605_28525_b200.materials import MaterialModel  # noqa: E402
+from paper_2605_28525_b200.solver import BoundaryCondition, SimConfig, Simulation  # noqa: E402
+from tests.test_gpu_module import keyed, normwise  # noqa: E402
+from tests.test_oracle_golden import _boundaries  # noqa: E402
+
+TOL = dict(x=1e-6, v=2e-5, C=2e-4, F=2e-5, mass=1e-6, mom=2e-5, force=2e-4)
+
+
+def column_scene(h=0.05, size=(0.4, 0.3, 0.5), seed=3, vx=0.4, bcs="mixed", mat=None):
+    pos, vol = scenes.sample_box((-size[0] / 2, -size[1] / 2, 0.03), (size[0] / 2, size[1] / 2, size[2]), h, 2)
+    rng = np.random.default_rng(seed)
+    pos = pos + rng.uniform(-0.2, 0.2, pos.shape) * h / 2
+    mat = mat or scenes.SAND
+    ps = scenes.rest_particles(pos, vol, mat.density, velocity=(vx, 0.0, 0.0))
+    cfg = SimConfig(h=h, gravity=np.array([0.5, 0.0, -9.81]), total_time=1.0, domain_min=np.array([-1.0, -1.0, -0.2]),
+                    domain_max=np.array([1.0, 1.0, 1.0]))
+    b = _boundaries() if bcs == "mixed" else []
+    return ps, cfg, [mat], b
+
+
+def oracle_step(oracle, state, cfg, mats, bcs, dt):
+    o = oracle.OracleSimulation(state, cfg.h, cfg.gravity, mats, bcs, backend="hash", deterministic=True)
+    st = o.step(dt)
+    return o, st
+
+
+def oracle_grid(oracle, state, cfg, mats):
+    s = oracle.OracleParticles.from_any(state)
+    oracle.update_stress(s, mats)
+    amap = oracle.build_hash_sparse_grid(s.x, cfg.h, 4, deterministic=True)
+    f = oracle.p2g(s, amap, cfg.h)
+    oracle.grid_forces(s, amap, cfg.h, cfg.gravity, fields=f)
+    return amap, f
+
+
+def compare_grid(oracle, sim, cfg, mats):
+    blocks, f = sim.query_grid()
+    amap, fr = oracle_grid(oracle, sim.particles, cfg, mats)
+    # bit-exact active block set
+    assert np.array_equal(np.sort(gi.pack_keys(blocks)), np.sort(gi.pack_keys(amap.active_blocks)))
+    kg, mg = keyed(blocks, f.mass, 1)
+    kr, mr = keyed(amap.active_blocks, fr.mass, 1)
+    assert np.array_equal(kg, kr)
+    _, pg = keyed(blocks, f.vel, 3)
+    _, pr = keyed(amap.active_blocks, fr.vel, 3)
+    _, fg = keyed(blocks, f.force, 3)
+    _, frr = keyed(amap.active_blocks, fr.force, 3)
+    errs = dict(mass=normwise(mg, mr), mom=normwise(pg, pr), force=normwise(fg, frr))
+    return errs
+
+
+@pytest.mark.parametrize("bcs", ["mixed", "none"])
+def test_steps_match_oracle(oracle, bcs):
+    ps, cfg, mats, bc = column_scene(bcs=bcs)
+    sim = Simulation(ps, cfg, mats, bc)
+    worst = {}
+    for s in range(8):
+        gerr = compare_grid(oracle, sim, cfg, mats)
+        state = sim.particles.copy()
+        dt = 0.9 * sim.dt_bound()
+        st = sim.step(dt)
+        o, ost = oracle_step(oracle, state, cfg, mats, bc, dt)
+        assert st.n_active == ost["n_active"], s
+        assert st.n_allocated == ost["n_allocated"], s
+        after = sim.particles
+        oracle.update_stress(o.particles, mats)  # GPU F is return-mapped at step end
+        errs = dict(x=float(np.abs(after.x - o.particles.x).max() / np.abs(o.particles.x).max()),
+                    v=normwise(after.v, o.particles.v), C=normwise(after.C, o.particles.C),
+                    F=normwise(after.F, o.particles.F), **gerr)
+        for k, e in errs.items():
+            worst[k] = max(worst.get(k, 0.0), e)
+    print("worst per-step errors:", {k: f"{v:.2e}" for k, v in worst.items()})
+    for k, e in worst.items():
+        assert e <= TOL[k], (k, e)
+
+
+def test_capacity_growth_replays_exactly(oracle):
+    ps, cfg, mats, bc = column_scene()
+    a = Simulation(ps.copy(), cfg, mats, bc)
+    b = Simulation(ps.copy(), cfg, mats, bc, block_capacity=8)
+    for _ in range(3):
+        sa = a.step(1e-4)
+        sb = b.step(1e-4)
+        assert sa.n_active == sb.n_active and sa.n_allocated == sb.n_allocated
+    assert np.abs(a.particles.x - b.particles.x).max() < 1e-9
+
+
+def test_free_fall_is_exact():
+    mat = MaterialModel(kind="elastic", density=1000.0, youngs_modulus=1e4, poisson_ratio=0.2)
+    ps, cfg, mats, bc = column_scene(bcs="none", mat=mat, vx=0.0)
+    cfg.gravity = np.array([0.0, 0.0, -9.81])
+    sim = Simulation(ps, cfg, mats, [])
+    z0 = ps.x[:, 2].copy()
+    dt = 1e-3
+    for _ in range(20):
+        sim.step(dt)
+    t = 20 * dt
+    # symplectic Euler: z = z0 - g dt^2 n(n+1)/2
+    z_exact = z0 - 9.81 * dt * dt * 20 * 21 / 2
+    assert np.abs(sim.particles.x[:, 2] - z_exact).max() < 1e-6
+    assert np.abs(sim.particles.v[:, 2] + 9.81 * t).max() < 1e-4
+    assert np.abs(sim.particles.F - np.eye(3)).max() < 1e-5
+
+
+def test_rest_state_stays_fixed():
+    mat = MaterialModel(kind="elastic", density=1000.0, youngs_modulus=1e4, poisson_ratio=0.2)
+    ps, cfg, mats, bc = column_scene(bcs="none", mat=mat, vx=0.0)
+    cfg.gravity = np.zeros(3)
+    pts = ps.x.copy()
+    sim = Simulation(ps, cfg, mats, [])
+    for _ in range(5):
+        sim.step(1e-3)
+    assert np.abs(sim.particles.v).max() == 0.0
+    assert np.abs(sim.particles.x - pts).max() == 0.0
+
+
+def test_step_stats_and_conservation():
+    ps, cfg, mats, bc = column_scene(bcs="none")
+    sim = Simulation(ps, cfg, mats, [], record_conservation=True)
+    st = sim.step(1e-4)
+    assert st.n_active > 0 and st.n_allocated >= st.n_active and st.n_allocated % 64 == 0
+    assert abs(st.mass_sum - ps.m.sum()) < 1e-5 * ps.m.sum()
+    mom = (sim.particles.m[:, None] * 0).sum(axis=0)
+    del mom
+    for phase in ("map_build", "alloc_zero", "p2g", "grid_update", "g2p", "stress"):
+        assert phase in st.times
+
+
+def test_degenerate_particle_raises_with_index():
+    ps, cfg, mats, bc = column_scene(bcs="none")
+    sim = Simulation(ps, cfg, mats, [])
+    sim.step(1e-4)
+    sim.particles.F[3] = 0.0
+    with pytest.raises(SimulationError, match="particle 3"):
+        sim.step(1e-4)
+
+
+def test_dt_above_bound_raises():
+    ps, cfg, mats, bc = column_scene(bcs="none")
+    sim = Simulation(ps, cfg, mats, [])
+    with pytest.raises(SimulationError):
+        sim.step(10.0 * sim.dt_bound())
+    sim.step(0.5 * sim.dt_bound())  # the rejected step left no trace
+
+
+def test_nonfinite_position_raises():
+    ps, cfg, mats, bc = column_scene(bcs="none")
+    ps.x[5, 1] = np.nan
+    with pytest.raises(SimulationError):
+        sim = Simulation(ps, cfg, mats, [])
+        sim.step(1e-4)
+
+
+def test_heightfield_slide_steps():
+    sc = scenes.landslide(x_stride=100, h=2.0, depth=(0.5, 10.0))
+    sim = sc.simulation()
+    n0 = sim.step().n_active
+    for _ in range(5):
+        st = sim.step()
+    assert st.n_active > 0 and n0 > 0
+    assert np.isfinite(sim.particles.x).all()

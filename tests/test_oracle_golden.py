@@ -1,0 +1,150 @@
+"""Pins the C oracle (oracle/) against golden vectors produced by the
+reference itself (tests/golden/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+from paper_2605_28525_b200 import grid_index as gi
+from paper_2605_28525_b200.materials import MaterialModel
+from paper_2605_28525_b200.solver import BoundaryCondition, Heightfield
+
+
+def _materials():
+    return [MaterialModel(kind="drucker_prager", density=1500.0, youngs_modulus=1e6, poisson_ratio=0.3,
+                          friction_angle_deg=30.0),
+            MaterialModel(kind="elastic", density=1000.0, youngs_modulus=2e5, poisson_ratio=0.25)]
+
+
+def _boundaries():
+    xs = np.arange(12) * 0.1 - 0.55
+    ys = np.arange(10) * 0.1 - 0.45
+    data = 0.02 + 0.15 * xs[:, None] + 0.05 * ys[None, :] ** 2
+    hf = Heightfield(x0=-0.55, y0=-0.45, cell=0.1, data=data)
+    return [BoundaryCondition(kind="plane", mu=0.3, point=np.zeros(3), normal=np.array([0.0, 0.1, 1.0])),
+            BoundaryCondition(kind="plane", mu=0.0, point=np.array([0.25, 0.0, 0.0]),
+                              normal=np.array([-1.0, 0.0, 0.0])),
+            BoundaryCondition(kind="heightfield", mu=0.5, heightfield=hf)]
+
+
+class _PS:
+    def __init__(self, g, prefix="in_"):
+        n = g[prefix + "x"].shape[0]
+        self.x = g[prefix + "x"].copy()
+        self.v = g[prefix + "v"].copy()
+        self.C = g[prefix + "C"].copy()
+        self.F = g[prefix + "F"].copy()
+        self.m = g[prefix + "m"].copy()
+        self.V0 = g[prefix + "V0"].copy()
+        self.mat_id = g[prefix + "mat_id"].copy()
+        self.sigma = np.zeros((n, 3, 3))
+        self.jac = np.ones(n)
+
+
+def test_keys_match_reference(oracle, golden):
+    g = golden("keys")
+    packed = oracle.pack_keys(g["blocks"])
+    assert np.array_equal(packed, g["packed"])
+    assert np.array_equal(oracle.unpack_keys(g["packed"]), g["unpacked"])
+    assert np.array_equal(oracle.mix64_array(g["mix_in"]), g["mix_out"])
+    for k in list(g["mix_in"][:50]) + list(g["mix_in"][-50:]):
+        assert oracle.mix64(int(k)) == gi.mix64(int(k))
+    # host helpers of the package agree too
+    for b, k in zip(g["blocks"][:200], g["packed"][:200]):
+        assert gi.pack_key(tuple(b)) == int(k)
+        assert gi.unpack_key(int(k)) == tuple(int(c) for c in b)
+    assert gi.pack_key((0, 0, 0)) == 2 ** 62 + 2 ** 41 + 2 ** 20
+    assert gi.mix64(0) == 0
+
+
+def test_hash_insert_sequence(oracle, golden):
+    g = golden("hash")
+    t = oracle.BlockHashTable(8192)
+    ranks, fresh = [], []
+    for b in g["ins_blocks"]:
+        r, f = t.insert(tuple(b))
+        ranks.append(r)
+        fresh.append(f)
+    assert np.array_equal(np.array(ranks), g["ins_ranks"])
+    assert np.array_equal(np.array(fresh), g["ins_fresh"])
+    assert np.array_equal(t.keys, g["ins_keys"])
+    assert np.array_equal(t.vals, g["ins_vals"])
+
+
+def test_hash_and_scan_builds(oracle, golden):
+    g = golden("hash")
+    x, h = g["cloud_x"], float(g["cloud_h"])
+    hm = oracle.build_hash_sparse_grid(x, h, 4, deterministic=True)
+    assert np.array_equal(hm.active_blocks, g["hash_active"])
+    assert np.array_equal(hm.keys, g["hash_keys"])
+    assert np.array_equal(hm.vals, g["hash_vals"])
+    sm = oracle.build_scan_sparse_grid(x, h, 4)
+    assert np.array_equal(sm.active_blocks, g["scan_active"])
+    assert np.array_equal(sm.phi_flat, g["scan_phi"])
+    hm2 = oracle.build_hash_sparse_grid(x, h, 4, initial_capacity=64, deterministic=True)
+    assert np.array_equal(hm2.active_blocks, g["rebuild_active"])
+    assert hm2.keys.shape[0] == int(g["rebuild_capacity"])
+    idx = [sm.node_index(nd) for nd in g["nodes"]]
+    assert np.array_equal(np.array(idx), g["scan_node_index"])
+    # sorted keys of the hash build == scan order (finding 6)
+    order = np.argsort(oracle.pack_keys(hm.active_blocks))
+    assert np.array_equal(hm.active_blocks[order], sm.active_blocks)
+
+
+def test_count_active_nodes(oracle, golden):
+    g = golden("count")
+    for i in range(4):
+        assert oracle.count_active_nodes(g[f"x{i}"], float(g[f"h{i}"])) == int(g[f"count{i}"])
+        assert oracle.active_node_set(g[f"x{i}"], float(g[f"h{i}"])).shape[0] == int(g[f"count{i}"])
+
+
+def test_stencil(oracle, golden):
+    g = golden("stencil")
+    for i in range(g["x"].shape[0]):
+        b, w, dw = oracle.bspline_weights(g["x"][i], g["h"][i])
+        assert np.array_equal(b, g["base"][i])
+        assert np.array_equal(w, g["w"][i])
+        assert np.array_equal(dw, g["dw"][i])
+
+
+def test_phases_bitwise(oracle, golden):
+    g = golden("phases")
+    ps = _PS(g)
+    h = float(g["h"])
+    mats = _materials()
+    oracle.update_stress(ps, mats)
+    assert np.array_equal(ps.F, g["st_F"])
+    np.testing.assert_allclose(ps.sigma, g["st_sigma"], rtol=0, atol=1e-9 * np.abs(g["st_sigma"]).max())
+    np.testing.assert_allclose(ps.jac, g["st_jac"], rtol=1e-14)
+    amap = oracle.build_scan_sparse_grid(ps.x, h, 4)
+    assert np.array_equal(amap.active_blocks, g["map_active"])
+    f = oracle.p2g(ps, amap, h)
+    oracle.grid_forces(ps, amap, h, g["gravity"], fields=f)
+    assert np.array_equal(f.mass, g["p2g_mass"])
+    assert np.array_equal(f.vel, g["p2g_mom"])
+    np.testing.assert_allclose(f.force, g["p2g_force"], rtol=0, atol=1e-12 * np.abs(g["p2g_force"]).max())
+    # continue from the reference's own fields so downstream checks are exact
+    f.force[...] = g["p2g_force"]
+    oracle.grid_update(f, amap, h, float(g["dt"]), float(g["mass_floor"]), _boundaries())
+    assert np.array_equal(f.vel, g["gu_vel"])
+    ps.F[...] = g["st_F"]
+    oracle.g2p(ps, amap, f, h, float(g["dt"]))
+    for k in ("x", "v", "C", "F"):
+        assert np.array_equal(getattr(ps, k), g["g2p_" + k]), k
+
+
+@pytest.mark.parametrize("backend", ["scan", "hash"])
+def test_steps_match_reference(oracle, golden, backend):
+    g = golden(f"steps_{backend}")
+    ps = _PS(g)
+    sim = oracle.OracleSimulation(ps, float(g["h"]), g["gravity"], _materials()[:1], _boundaries(),
+                                  backend=backend, deterministic=True)
+    for s in range(g["x"].shape[0]):
+        st = sim.step()
+        assert st["dt"] == g["dt"][s]
+        assert st["n_active"] == g["n_active"][s]
+        assert st["n_allocated"] == g["n_allocated"][s]
+        np.testing.assert_allclose(sim.particles.x, g["x"][s], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(sim.particles.v, g["v"][s], rtol=0, atol=1e-9 * max(1.0, np.abs(g["v"][s]).max()))
+    np.testing.assert_allclose(sim.particles.F, g["F"], rtol=0, atol=1e-9)
+    if backend == "hash":
+        assert np.array_equal(sim.last_map.active_blocks, g["last_active"])
