@@ -42,7 +42,7 @@ def make_scene(cfg_name, scale):
     from paper_2605_28525_b200 import scenes
 
     if cfg_name == "C4":
-        return scenes.landslide(x_stride=max(1, int(round(1.0 / scale))))
+        return scenes.landslide(fraction=scale)
     if cfg_name == "C3":
         return scenes.incline()
     if cfg_name == "C2":
@@ -110,7 +110,7 @@ def cpu_sample_scene(cfg_name):
     from paper_2605_28525_b200 import scenes
 
     if cfg_name == "C4":
-        return scenes.landslide(x_stride=100), "landslide release zone, every 100th x column (~1M particles)"
+        return scenes.landslide(fraction=0.05), "first 5% (12.5 m) of the landslide release zone (4.95M particles)"
     if cfg_name == "C3":
         return scenes.incline(h=0.04), "incline at h=0.04 (1/8 of the particles)"
     return make_scene(cfg_name, 1.0), "full scene"

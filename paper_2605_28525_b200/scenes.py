@@ -119,20 +119,22 @@ def landslide_terrain(cell=5.0):
     return Heightfield(x0=0.0, y0=-250.0, cell=cell, data=data)
 
 
-def landslide(h=0.5, ppc=2, release=((100.0, 350.0), (-62.5, 62.5)), depth=(0.5, 50.0), mu=0.35, x_stride=1):
+def landslide(h=0.5, ppc=2, release=((100.0, 350.0), (-62.5, 62.5)), depth=(0.5, 50.0), mu=0.35, x_stride=1,
+              fraction=1.0):
     """C4: terrain-conforming release zone over the analytic DEM.
 
     Particles sit on a lattice of spacing h/ppc in x and y; each (x,y) column
     is filled from z_s + depth[0] to z_s + depth[1] (z_s the bilinear DEM
     height, i.e. what the grid boundary sees).  ``x_stride`` > 1 keeps every
-    k-th x column (a bounded sample of the same scene for the CPU baseline).
+    k-th x column; ``fraction`` < 1 keeps the leading fraction of the release
+    zone in x (contiguous: same block occupancy as the full scene).
     """
     hf = landslide_terrain()
     sp = h / ppc
     (x0, x1), (y0, y1) = release
     xs = x0 + (np.arange(int(round((x1 - x0) / sp))) + 0.5) * sp
     ys = y0 + (np.arange(int(round((y1 - y0) / sp))) + 0.5) * sp
-    xs = xs[::x_stride]
+    xs = xs[: max(1, int(round(xs.shape[0] * fraction)))][::x_stride]
     nz = int(round((depth[1] - depth[0]) / sp))
     zoff = depth[0] + (np.arange(nz) + 0.5) * sp
     gx, gy = np.meshgrid(xs, ys, indexing="ij")

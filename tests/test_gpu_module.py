@@ -53,7 +53,7 @@ def test_hash_concurrent_unique_winner():
     rng = np.random.default_rng(0)
     blocks = rng.integers(-30, 30, size=(200_000, 3))
     keys = gi.pack_keys(blocks)
-    t = BlockHashTable(1 << 16)
+    t = BlockHashTable(1 << 18)
     ranks, fresh = t.insert_many(keys)
     uniq = np.unique(keys)
     assert t.count == uniq.shape[0]

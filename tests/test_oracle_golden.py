@@ -39,6 +39,10 @@ class _PS:
         self.sigma = np.zeros((n, 3, 3))
         self.jac = np.ones(n)
 
+    @property
+    def n(self):
+        return int(self.x.shape[0])
+
 
 def test_keys_match_reference(oracle, golden):
     g = golden("keys")
