@@ -31,31 +31,38 @@
 namespace smpm {
 
 // ---------------------------------------------------------------- layout
-// Smem arenas use node address k + 8 j + 68 i: warp lanes are a 2x4x4 box of
-// distinct cells, so for any stencil offset the 32 lanes hit 32 distinct banks
-// (68 = 4 mod 32); measured 29 lane-atomics/clk/SM vs 8.6 for a naive layout
+// Scatter arena (int32 fixed point, one array per field) uses node address
+// k + 8 j + 68 i: warp lanes are a 2x4x4 box of distinct cells, so for any
+// stencil offset the 32 lanes hit 32 distinct banks (68 = 4 mod 32); measured
+// 29 lane-atomics/clk/SM vs 8.6 for a naive layout
 // (profiles/r01_ubench_atomics.md).
 constexpr int AI = 68, AJ = 8;
 constexpr int SCAT_N = 8 * AI;   // scatter arena: nodes 4B-1 .. 4B+6 per axis
-constexpr int GATH_N = 6 * AI;   // gather arena: nodes 4B .. 4B+5 per axis
 constexpr int NF = 7;            // m, p0..2, f0..2
+constexpr int NA = NF + 1;       // + contribution count K
 constexpr int CTA = 256;         // 64 cells x 4 slots
 constexpr int SLOTS = 4;
 constexpr uint32_t MAGIC_BITS = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float MAGIC = 12582912.0f;
 constexpr uint32_t BAD_KEY = 0xFFFFFFFFu;
+// Gather arena: float4 velocity per node, nodes 4B .. 4B+5 per axis, address
+// (k ^ 4*(j&1)) + 8 j + 48 i in float4 units: each quarter-warp (2x4 cells)
+// reads 8 distinct 16-byte bank groups, so the 27 LDS.128 per particle are
+// conflict-free.
+constexpr int GATH_N = 6 * 48;
 
 __device__ __forceinline__ int aaddr(int i, int j, int k) { return k + AJ * j + AI * i; }
+__device__ __forceinline__ int gaddr(int i, int j, int k) { return (k ^ ((j & 1) << 2)) + 8 * j + 48 * i; }
+
+// Particle record: one 128-byte line per particle (float word offsets).
+//   x f64[3] @0 | m @6 | V0 @7 | F[9] @8 | pid|mat<<29 @17 | v[3] @18 | C[9] @21 | pad @30
+// G2P reads chunks 0..4 (80 B: x, m, V0, F, pid/mat); the kernel writes all 8.
+constexpr int REC_W = 32;
+constexpr int W_M = 6, W_V0 = 7, W_F = 8, W_PM = 17, W_V = 18, W_C = 21;
+constexpr uint32_t PID_MASK = (1u << 29) - 1;
 
 struct Particles {
-  double* x[3];
-  float* v[3];
-  float* C[9];
-  float* F[9];
-  float* m;
-  float* V0;
-  uint8_t* mat;
-  uint32_t* pid;
+  float4* rec;  // [n] records
 };
 
 struct TableDev {
@@ -65,6 +72,7 @@ struct TableDev {
   uint32_t* cell_off;    // [cap_b*64]
   uint32_t* block_total; // [cap_b]
   uint32_t* block_items; // [cap_b]
+  uint32_t* nbr8;        // [cap_b*8] ranks of blocks B + {0,1}^3 (gather arena)
   uint2* items;          // [cap_items] (rank, group)
   uint32_t* tile_sums;   // [3*max_tiles]
   uint32_t* done;        // last-CTA counter
@@ -74,7 +82,7 @@ struct TableDev {
 // Device-side per-table statistics (the step whose particles are binned in
 // this table).
 struct DevStats {
-  unsigned long long err;   // shared error word lives in ctx; copy here
+  unsigned long long err;
   uint32_t n_blocks;
   uint32_t n_items;
   uint32_t overflow;
@@ -135,7 +143,7 @@ __device__ inline uint32_t cta_excl_scan(uint32_t v, uint32_t* sh /*[8]*/, uint3
 }
 
 // scan1: per block totals / items / popcount; per tile sums; the last CTA
-// scans tile sums and finalises the step scalars (dt, error checks).
+// scans tile sums and finalises the step scalars.
 __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
                                                unsigned long long* err, StepParams sp) {
   __shared__ uint32_t red[3][8];
@@ -151,6 +159,13 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
       uint32_t c0 = S.cell_count[size_t(r) * 64 + lane], c1 = S.cell_count[size_t(r) * 64 + 32 + lane];
       uint32_t tot = warp_sum(c0 + c1), mx = warp_max(max(c0, c1));
       uint32_t items = (mx + SLOTS - 1) / SLOTS;
+      // neighbour ranks for the gather arena of this block's work items
+      if (lane < 8 && items) {
+        int bi, bj, bk;
+        unpack_key(S.hv.active_keys[r], bi, bj, bk);
+        S.nbr8[size_t(r) * 8 + lane] = hash_lookup(S.hv.keys, S.hv.vals, S.hv.mask,
+                                                   pack_key(bi + (lane >> 2), bj + ((lane >> 1) & 1), bk + (lane & 1)));
+      }
       if (lane == 0) {
         S.block_total[r] = tot;
         S.block_items[r] = items;
@@ -178,7 +193,6 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // exclusive scan of tile sums (3 channels), 256 threads, loop over chunks
   uint32_t carry[3] = {0, 0, 0};
   __shared__ uint32_t sh[8];
   unsigned long long n_active = 0;
@@ -256,12 +270,13 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S) {
   }
 }
 
-// bin: scatter storage indices into sorted positions
-__global__ void k_bin(const uint2* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm) {
+// bin: every particle takes the next position of its cell (atomic cursor that
+// starts at the scanned cell offset and ends at offset + count).
+__global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    uint2 b = bin[i];
-    if (b.x == BAD_KEY) continue;
-    perm[S.cell_off[b.x] + b.y] = uint32_t(i);
+    uint32_t key = bin[i];
+    if (key == BAD_KEY) continue;
+    perm[atomicAdd(&S.cell_off[key], 1u)] = uint32_t(i);
   }
 }
 
@@ -321,39 +336,40 @@ __global__ void __launch_bounds__(256) k_grid(TableDev S, TableDev T, DevStats* 
 
 // --------------------------------------------------------- prologue keys
 // Bins particles (arbitrary storage order) by the block of their base cell.
-__global__ void k_prologue_keys(Particles P, int64_t n, TableDev B, uint2* __restrict__ bin, double inv_h,
+__global__ void k_prologue_keys(Particles P, int64_t n, TableDev B, uint32_t* __restrict__ bin, double inv_h,
                                 unsigned long long* err) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double* xr = reinterpret_cast<const double*>(&P.rec[i * 8]);
+    const uint32_t pid = __float_as_uint(reinterpret_cast<const float*>(&P.rec[i * 8])[W_PM]) & PID_MASK;
     int base[3];
     float d;
     bool ok = true;
-    double xs[3] = {P.x[0][i], P.x[1][i], P.x[2][i]};
     for (int a = 0; a < 3; ++a) {
-      if (!isfinite(xs[a])) {
-        err_report(err, ERR_NONFINITE_X, P.pid[i]);
+      double xa = xr[a];
+      if (!isfinite(xa)) {
+        err_report(err, ERR_NONFINITE_X, pid);
         ok = false;
         break;
       }
-      if (!axis_base(xs[a], inv_h, base[a], d) || !axis_in_key_range(base[a])) {
-        err_report(err, ERR_KEY_RANGE, P.pid[i]);
+      if (!axis_base(xa, inv_h, base[a], d) || !axis_in_key_range(base[a])) {
+        err_report(err, ERR_KEY_RANGE, pid);
         ok = false;
         break;
       }
     }
     if (!ok) {
-      bin[i] = make_uint2(BAD_KEY, 0);
+      bin[i] = BAD_KEY;
       continue;
     }
     uint64_t key = pack_key(base[0] >> 2, base[1] >> 2, base[2] >> 2);
     uint32_t rank = hash_insert(B.hv, key);
     if (rank >= B.hv.cap_blocks) {
-      bin[i] = make_uint2(BAD_KEY, 0);
+      bin[i] = BAD_KEY;
       continue;
     }
     uint32_t cell = uint32_t(((base[0] & 3) << 4) | ((base[1] & 3) << 2) | (base[2] & 3));
-    uint32_t key2 = rank * 64 + cell;
-    uint32_t idx = atomicAdd(&B.cell_count[key2], 1u);
-    bin[i] = make_uint2(key2, idx);
+    bin[i] = rank * 64 + cell;
+    atomicAdd(&B.cell_count[rank * 64 + cell], 1u);
   }
 }
 
@@ -365,7 +381,7 @@ struct FusedArgs {
   TableDev S;                 // table receiving the next P2G
   const float4* gv;           // grid velocity of B (float4 per node)
   float4* acc;                // accumulators of S (2 float4 per node)
-  uint2* bin_out;             // bins of dst particles in S
+  uint32_t* bin_out;          // cell keys (rank*64+cell) of dst particles in S
   const Material* mats;
   int n_mat;
   double h, inv_h;
@@ -375,18 +391,21 @@ struct FusedArgs {
   int project;
 };
 
+struct ItemInfo {
+  uint32_t r, g;
+  int b[3];
+  uint32_t nbr[8];
+};
+
 struct __align__(16) FusedSmem {
-  float gv[3][GATH_N];
-  int acc[NF][SCAT_N];
-  uint32_t cnt[SCAT_N];
-  uint32_t t1[SCAT_N];
-  uint32_t t2[SCAT_N];
-  uint32_t mask[27][2];
+  float4 stage[CTA * 8];     // prefetched particle records (chunk c of thread t at t*8 + ((c+t)&7))
+  float4 garena[2][GATH_N];  // double-buffered velocity arena
+  int acc[NA][SCAT_N];       // fixed-point arena (+ contribution count)
+  uint32_t cnt[SCAT_N];      // particles per arena base cell; later: bin base
+  uint32_t occ[16];          // base-cell occupancy bitmap: 8x8 rows (i,j) of 8 k-bits
   uint32_t rank[27];
-  uint32_t grank[8];
   uint32_t bmax[3];
-  uint32_t item_r, item_g;
-  int bi, bj, bk;
+  ItemInfo info[3];          // ring: items i, i+1, i+2
   Material mats[8];
 };
 
@@ -396,13 +415,21 @@ __device__ __forceinline__ void red_v4(float4* p, float a, float b, float c, flo
 __device__ __forceinline__ void sred(int* p, int v) {
   asm volatile("red.shared.add.s32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ int magic_q(float t) { return __float_as_int(t); }
 
-// power-of-two fixed-point scale for contributions bounded by b (b*S <= 2^21)
+// power-of-two fixed-point scale for contributions bounded by b: b*S <= 2^22
+// (exact magic-add conversion) and 256 contributions fit in int32
 __device__ __forceinline__ float fx_scale(float b, float& inv) {
   int e = 0;
   if (b > 0.f) frexpf(b, &e);
-  int s = 21 - e;
+  int s = 22 - e;
   s = max(-100, min(100, s));
   inv = ldexpf(1.0f, -s);
   return ldexpf(1.0f, s);
@@ -411,7 +438,7 @@ __device__ __forceinline__ float fx_scale(float b, float& inv) {
 // Global (slow-path) scatter of a particle that moved outside its block's
 // 8^3 arena: direct inserts and float atomics (rare: |dx| > 1 cell/step).
 __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float d[3], float m, const float v[3],
-                               const float C[9], const float M[6], uint32_t pidv, uint2& binv) {
+                               const float C[9], const float M[6], uint32_t& binv) {
   float w[3][3], g[3][3];
   for (int a = 0; a < 3; ++a) bspline(d[a], w[a], g[a]);
   const float h = float(A.h), ih = float(A.inv_h);
@@ -440,13 +467,57 @@ __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float 
       }
   uint32_t r = hash_insert(A.S.hv, pack_key(nb[0] >> 2, nb[1] >> 2, nb[2] >> 2));
   if (r >= A.S.hv.cap_blocks) {
-    binv = make_uint2(BAD_KEY, 0);
+    binv = BAD_KEY;
     return;
   }
   uint32_t cell = uint32_t(((nb[0] & 3) << 4) | ((nb[1] & 3) << 2) | (nb[2] & 3));
-  uint32_t key = r * 64 + cell;
-  binv = make_uint2(key, atomicAdd(&A.S.cell_count[key], 1u));
-  (void)pidv;
+  binv = r * 64 + cell;
+  atomicAdd(&A.S.cell_count[binv], 1u);
+}
+
+__device__ __forceinline__ void fetch_item(const FusedArgs& A, uint32_t n_items, ItemInfo& inf) {
+  uint32_t it = atomicAdd(A.B.item_next, 1u);
+  if (it < n_items) {
+    uint2 rg = A.B.items[it];
+    inf.r = rg.x;
+    inf.g = rg.y;
+    unpack_key(A.B.hv.active_keys[rg.x], inf.b[0], inf.b[1], inf.b[2]);
+  } else {
+    inf.r = BAD_KEY;
+  }
+}
+
+// sorted position of this thread's particle in item (r, g); returns validity
+__device__ __forceinline__ bool item_slot(const FusedArgs& A, uint32_t r, uint32_t g, int tid, uint32_t& pos) {
+  if (r == BAD_KEY) return false;
+  const uint32_t key = r * 64 + (tid & 63);
+  const uint32_t slot = g * SLOTS + (tid >> 6);
+  const uint32_t cnt = A.B.cell_count[key];
+  if (slot >= cnt) return false;
+  pos = A.B.cell_off[key] - cnt + slot;  // k_bin advanced cell_off to the cell's end
+  return true;
+}
+
+template <bool GATHER>
+__device__ __forceinline__ void prefetch_record(FusedSmem& sm, const FusedArgs& A, int tid, uint32_t src) {
+  const float4* g = A.src.rec + size_t(src) * 8;
+  float4* st = &sm.stage[tid * 8];
+  constexpr int NC = GATHER ? 5 : 8;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) cp_async16(&st[(c + tid) & 7], &g[c]);
+}
+
+__device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A, const ItemInfo& inf, int buf,
+                                               int tid) {
+  for (int n = tid; n < 216; n += CTA) {
+    int i = n / 36, j = (n / 6) % 6, k = n % 6;
+    uint32_t gr = inf.nbr[((i >> 2) << 2) | ((j >> 2) << 1) | (k >> 2)];
+    float4* dst = &sm.garena[buf][gaddr(i, j, k)];
+    if (gr < A.B.hv.cap_blocks)
+      cp_async16(dst, &A.gv[size_t(gr) * 64 + (((i & 3) << 4) | ((j & 3) << 2) | (k & 3))]);
+    else
+      *dst = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 }
 
 template <bool GATHER>
@@ -461,71 +532,88 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
   const float hf_ = float(A.h);
   uint32_t vmax2_local = 0;
 
+  // ---- prime the pipeline: records of item 0, indices of item 1, metadata
+  // of item 2.  In steady state item i computes while item i+1's records and
+  // velocity arena are in flight and item i+2's indices are being loaded.
+  if (tid < 3) sm.bmax[tid] = 0;  // re-zeroed after [B3] each item (read after [B2])
+  if (tid == 0) fetch_item(A, n_items, sm.info[0]);
+  __syncthreads();
+  uint32_t pos = 0, pos1 = 0, src1 = 0;
+  bool valid = false, valid1 = false;
+  {
+    const ItemInfo& i0 = sm.info[0];
+    if (GATHER && tid < 8 && i0.r != BAD_KEY) sm.info[0].nbr[tid] = A.B.nbr8[size_t(i0.r) * 8 + tid];
+    valid = item_slot(A, i0.r, i0.g, tid, pos);
+    if (valid) prefetch_record<GATHER>(sm, A, tid, A.perm[pos]);
+    if (tid == 0) fetch_item(A, n_items, sm.info[1]);
+  }
+  __syncthreads();
+  {
+    const ItemInfo& i1 = sm.info[1];
+    valid1 = item_slot(A, i1.r, i1.g, tid, pos1);
+    if (valid1) src1 = A.perm[pos1];
+    if (tid == 0) fetch_item(A, n_items, sm.info[2]);
+  }
+  if (GATHER && sm.info[0].r != BAD_KEY) prefetch_arena(sm, A, sm.info[0], 0, tid);
+  cp_async_commit();
+  int buf = 0, c = 0;
+
   while (true) {
-    __syncthreads();  // previous item's flush done before re-zeroing
-    if (tid == 0) {
-      uint32_t it = atomicAdd(A.B.item_next, 1u);
-      if (it < n_items) {
-        uint2 rg = A.B.items[it];
-        sm.item_r = rg.x;
-        sm.item_g = rg.y;
-        unpack_key(A.B.hv.active_keys[rg.x], sm.bi, sm.bj, sm.bk);
-      } else {
-        sm.item_r = BAD_KEY;
-      }
-    }
-    // zero arenas
-    for (int i = tid; i < NF * SCAT_N; i += CTA) (&sm.acc[0][0])[i] = 0;
-    for (int i = tid; i < SCAT_N; i += CTA) sm.cnt[i] = 0;
-    if (tid < 54) (&sm.mask[0][0])[tid] = 0;
-    if (tid < 3) sm.bmax[tid] = 0;
-    __syncthreads();
-    const uint32_t r = sm.item_r;
+    cp_async_wait_all();
+    __syncthreads();  // [B1] records + arena of this item landed; previous flush done
+    const ItemInfo& cur = sm.info[c];
+    const ItemInfo& nxt = sm.info[c == 2 ? 0 : c + 1];
+    const ItemInfo& nn = sm.info[c == 0 ? 2 : c - 1];
+    const uint32_t r = cur.r;
     if (r == BAD_KEY) break;
-    const int B0 = sm.bi, B1 = sm.bj, B2 = sm.bk;
-    if (GATHER) {
-      if (tid < 8) {
-        int c0 = tid >> 2, c1 = (tid >> 1) & 1, c2 = tid & 1;
-        sm.grank[tid] = hash_lookup(A.B.hv.keys, A.B.hv.vals, A.B.hv.mask, pack_key(B0 + c0, B1 + c1, B2 + c2));
-      }
-      __syncthreads();
-      for (int n = tid; n < 216; n += CTA) {
-        int i = n / 36, j = (n / 6) % 6, k = n % 6;
-        uint32_t gr = sm.grank[((i >> 2) << 2) | ((j >> 2) << 1) | (k >> 2)];
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gr < A.B.hv.cap_blocks) v = A.gv[size_t(gr) * 64 + (((i & 3) << 4) | ((j & 3) << 2) | (k & 3))];
-        int ad = aaddr(i, j, k);
-        sm.gv[0][ad] = v.x;
-        sm.gv[1][ad] = v.y;
-        sm.gv[2][ad] = v.z;
-      }
-      __syncthreads();
+    const int B0 = cur.b[0], B1 = cur.b[1], B2 = cur.b[2];
+    // zero the scatter arena (previous item's flush is complete)
+    {
+      int4* z = reinterpret_cast<int4*>(&sm.acc[0][0]);
+      for (int i = tid; i < NA * SCAT_N / 4; i += CTA) z[i] = make_int4(0, 0, 0, 0);
+      int4* zc = reinterpret_cast<int4*>(&sm.cnt[0]);
+      for (int i = tid; i < SCAT_N / 4; i += CTA) zc[i] = make_int4(0, 0, 0, 0);
+      if (tid < 16) sm.occ[tid] = 0;
     }
-    // ---- particle of this thread
-    const int cell = tid & 63;
-    const uint32_t slot = sm.item_g * SLOTS + (tid >> 6);
-    const uint32_t key = r * 64 + cell;
-    const uint32_t cnt = A.B.cell_count[key];
-    const bool valid = slot < cnt;
-    uint32_t pos = 0, src = 0;
+    if (GATHER && tid < 8 && nxt.r != BAD_KEY)
+      sm.info[c == 2 ? 0 : c + 1].nbr[tid] = A.B.nbr8[size_t(nxt.r) * 8 + tid];
+    // this item's record -> registers, then the stage slot takes item i+1's
+    float4 c0, c1, c2, c3, c4, c5, c6, c7;
+    if (valid) {
+      const float4* st = &sm.stage[tid * 8];
+      c0 = st[(0 + tid) & 7];
+      c1 = st[(1 + tid) & 7];
+      c2 = st[(2 + tid) & 7];
+      c3 = st[(3 + tid) & 7];
+      c4 = st[(4 + tid) & 7];
+      if (!GATHER) {
+        c5 = st[(5 + tid) & 7];
+        c6 = st[(6 + tid) & 7];
+        c7 = st[(7 + tid) & 7];
+      }
+    }
+    if (valid1) prefetch_record<GATHER>(sm, A, tid, src1);
+    // item i+2: sorted position and source index (consumed one item later)
+    uint32_t pos2 = 0, src2 = 0;
+    const bool valid2 = item_slot(A, nn.r, nn.g, tid, pos2);
+    if (valid2) src2 = A.perm[pos2];
+
     double xn[3];
     float vn[3], Cn[9], M[6], m = 0.f, d1[3];
     int nb[3], ab[3];
     bool far = false, ok = valid;
     float bm = 0.f, bp = 0.f, bf = 0.f;
+    uint32_t pidv = 0;
     if (valid) {
-      pos = A.B.cell_off[key] + slot;
-      src = A.perm[pos];
-      xn[0] = A.src.x[0][src];
-      xn[1] = A.src.x[1][src];
-      xn[2] = A.src.x[2][src];
-      float F[9];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) F[q] = A.src.F[q][src];
-      m = A.src.m[src];
-      const float V0 = A.src.V0[src];
-      const uint8_t mt = A.src.mat[src];
-      const uint32_t pidv = A.src.pid[src];
+      xn[0] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
+      xn[1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
+      xn[2] = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
+      m = c1.z;
+      const float V0 = c1.w;
+      float F[9] = {c2.x, c2.y, c2.z, c2.w, c3.x, c3.y, c3.z, c3.w, c4.x};
+      const uint32_t pm = __float_as_uint(c4.y);
+      pidv = pm & PID_MASK;
+      const int mt = int(pm >> 29);
       if (GATHER) {
         // ---- G2P (solver.py:628-732) from the smem velocity arena
         int lb[3];
@@ -540,9 +628,7 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
         float v0 = 0, v1 = 0, v2 = 0;
         float b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
         float a00 = 0, a01 = 0, a02 = 0, a10 = 0, a11 = 0, a12 = 0, a20 = 0, a21 = 0, a22 = 0;
-        const float* g0p = &sm.gv[0][aaddr(lb[0], lb[1], lb[2])];
-        const float* g1p = &sm.gv[1][aaddr(lb[0], lb[1], lb[2])];
-        const float* g2p = &sm.gv[2][aaddr(lb[0], lb[1], lb[2])];
+        const float4* ga = sm.garena[buf];
         float wzd[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) wzd[k] = w[2][k] * (float(k) - d[2]);
@@ -551,19 +637,19 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
 #pragma unroll
           for (int oj = 0; oj < 3; ++oj) {
             float S0 = 0, S1 = 0, S2 = 0, T0 = 0, T1 = 0, T2 = 0, U0 = 0, U1 = 0, U2 = 0;
+            const int gi = lb[0] + oi, gj = lb[1] + oj;
 #pragma unroll
             for (int ok = 0; ok < 3; ++ok) {
-              int o = aaddr(oi, oj, ok);
-              float q0 = g0p[o], q1 = g1p[o], q2 = g2p[o];
-              S0 += w[2][ok] * q0;
-              S1 += w[2][ok] * q1;
-              S2 += w[2][ok] * q2;
-              T0 += wzd[ok] * q0;
-              T1 += wzd[ok] * q1;
-              T2 += wzd[ok] * q2;
-              U0 += g[2][ok] * q0;
-              U1 += g[2][ok] * q1;
-              U2 += g[2][ok] * q2;
+              const float4 q = ga[gaddr(gi, gj, lb[2] + ok)];
+              S0 += w[2][ok] * q.x;
+              S1 += w[2][ok] * q.y;
+              S2 += w[2][ok] * q.z;
+              T0 += wzd[ok] * q.x;
+              T1 += wzd[ok] * q.y;
+              T2 += wzd[ok] * q.z;
+              U0 += g[2][ok] * q.x;
+              U1 += g[2][ok] * q.y;
+              U2 += g[2][ok] * q.z;
             }
             float wij = w[0][oi] * w[1][oj];
             float dxi = wij * (float(oi) - d[0]), dyj = wij * (float(oj) - d[1]);
@@ -618,14 +704,22 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
         xn[1] = __dadd_rn(xn[1], __dmul_rn(dt, double(v1)));
         xn[2] = __dadd_rn(xn[2], __dmul_rn(dt, double(v2)));
       } else {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) vn[a] = A.src.v[a][src];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) Cn[q] = A.src.C[q][src];
+        vn[0] = c4.z;
+        vn[1] = c4.w;
+        vn[2] = c5.x;
+        Cn[0] = c5.y;
+        Cn[1] = c5.z;
+        Cn[2] = c5.w;
+        Cn[3] = c6.x;
+        Cn[4] = c6.y;
+        Cn[5] = c6.z;
+        Cn[6] = c6.w;
+        Cn[7] = c7.x;
+        Cn[8] = c7.y;
       }
       // ---- stress of the next step (materials.py:169-238)
       float tau[6], J;
-      const Material& mat = sm.mats[mt < 8 ? mt : 0];
+      const Material& mat = sm.mats[mt];
       if (!hencky_dp(F, mat, A.project != 0, tau, J)) {
         err_report(A.err, ERR_DEGENERATE_F, pidv);
         ok = false;
@@ -633,20 +727,21 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
       }
 #pragma unroll
       for (int q = 0; q < 6; ++q) M[q] = V0 * tau[q];
-      // ---- write the particle at its sorted position (next storage order)
-      A.dst.x[0][pos] = xn[0];
-      A.dst.x[1][pos] = xn[1];
-      A.dst.x[2][pos] = xn[2];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) A.dst.v[a][pos] = vn[a];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) A.dst.C[q][pos] = Cn[q];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) A.dst.F[q][pos] = F[q];
-      A.dst.m[pos] = m;
-      A.dst.V0[pos] = V0;
-      A.dst.mat[pos] = mt;
-      A.dst.pid[pos] = pidv;
+      // ---- write the particle record at its sorted position
+      {
+        float4* o = A.dst.rec + size_t(pos) * 8;
+        int2 x0 = make_int2(__double2loint(xn[0]), __double2hiint(xn[0]));
+        int2 x1 = make_int2(__double2loint(xn[1]), __double2hiint(xn[1]));
+        int2 x2 = make_int2(__double2loint(xn[2]), __double2hiint(xn[2]));
+        o[0] = make_float4(__int_as_float(x0.x), __int_as_float(x0.y), __int_as_float(x1.x), __int_as_float(x1.y));
+        o[1] = make_float4(__int_as_float(x2.x), __int_as_float(x2.y), m, V0);
+        o[2] = make_float4(F[0], F[1], F[2], F[3]);
+        o[3] = make_float4(F[4], F[5], F[6], F[7]);
+        o[4] = make_float4(F[8], __uint_as_float(pm), vn[0], vn[1]);
+        o[5] = make_float4(vn[2], Cn[0], Cn[1], Cn[2]);
+        o[6] = make_float4(Cn[3], Cn[4], Cn[5], Cn[6]);
+        o[7] = make_float4(Cn[7], Cn[8], 0.f, 0.f);
+      }
       float vv = vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2];
       vmax2_local = max(vmax2_local, __float_as_uint(vv));
       // ---- next step's keys
@@ -665,45 +760,108 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
         ab[1] = nb[1] - (4 * B1 - 1);
         ab[2] = nb[2] - (4 * B2 - 1);
         far = ab[0] < 0 || ab[0] > 5 || ab[1] < 0 || ab[1] > 5 || ab[2] < 0 || ab[2] > 5;
+        // contribution bounds: |w| <= prod_a max_o w_a(o); |grad w_a| <= max|g_a| prod_{b!=a} max w_b / h;
+        // |dx_a| <= h * max(d_a, 2 - d_a)
+        float wmax[3], gmax[3], dxm[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const float dd = d1[a];
+          const float w0 = 0.5f * (1.5f - dd) * (1.5f - dd), w1 = 0.75f - (dd - 1.f) * (dd - 1.f),
+                      w2 = 0.5f * (dd - 0.5f) * (dd - 0.5f);
+          wmax[a] = fmaxf(w0, fmaxf(w1, w2));
+          gmax[a] = fmaxf(fabsf(dd - 1.5f), fmaxf(fabsf(2.f * (dd - 1.f)), fabsf(dd - 0.5f)));
+          dxm[a] = hf_ * fmaxf(dd, 2.f - dd);
+        }
+        const float W = wmax[0] * wmax[1] * wmax[2];
+        const float G0 = gmax[0] * wmax[1] * wmax[2] * ih, G1 = wmax[0] * gmax[1] * wmax[2] * ih,
+                    G2 = wmax[0] * wmax[1] * gmax[2] * ih;
         float cm = 0.f;
 #pragma unroll
         for (int a = 0; a < 3; ++a)
-          cm = fmaxf(cm, fabsf(vn[a]) + 1.5f * hf_ * (fabsf(Cn[3 * a]) + fabsf(Cn[3 * a + 1]) + fabsf(Cn[3 * a + 2])));
-        float fm = fmaxf(fabsf(M[0]) + fabsf(M[3]) + fabsf(M[4]),
-                         fmaxf(fabsf(M[3]) + fabsf(M[1]) + fabsf(M[5]), fabsf(M[4]) + fabsf(M[5]) + fabsf(M[2])));
+          cm = fmaxf(cm, fabsf(vn[a]) + fabsf(Cn[3 * a]) * dxm[0] + fabsf(Cn[3 * a + 1]) * dxm[1] +
+                             fabsf(Cn[3 * a + 2]) * dxm[2]);
+        const float fm = fmaxf(fabsf(M[0]) * G0 + fabsf(M[3]) * G1 + fabsf(M[4]) * G2,
+                               fmaxf(fabsf(M[3]) * G0 + fabsf(M[1]) * G1 + fabsf(M[5]) * G2,
+                                     fabsf(M[4]) * G0 + fabsf(M[5]) * G1 + fabsf(M[2]) * G2));
         if (!far) {
-          bm = m * 0.421875f * 1.001f;
-          bp = m * 0.421875f * cm * 1.001f;
-          bf = fm * 0.5625f * ih * 1.001f;
+          bm = m * W * 1.0001f;
+          bp = m * W * cm * 1.0001f;
+          bf = fm * 1.0001f;
         }
       }
     }
-    // ---- block-wide maxima of the contribution bounds
+    // base-cell occupancy of the next step (exact touched-node set = its 3x3x3
+    // dilation) and the per-cell particle count (bin size, local bin index)
+    if (ok && !far) {
+      const int row = ab[0] * 8 + ab[1];
+      atomicOr(&sm.occ[row >> 2], 1u << (((row & 3) << 3) | ab[2]));
+      atomicAdd(&sm.cnt[aaddr(ab[0], ab[1], ab[2])], 1u);
+    }
     {
-      uint32_t um = __float_as_uint(bm), up = __float_as_uint(bp), uf = __float_as_uint(bf);
-      um = warp_max(um);
-      up = warp_max(up);
-      uf = warp_max(uf);
+      uint32_t um = warp_max(__float_as_uint(bm)), up = warp_max(__float_as_uint(bp)),
+               uf = warp_max(__float_as_uint(bf));
       if ((tid & 31) == 0) {
         atomicMax(&sm.bmax[0], um);
         atomicMax(&sm.bmax[1], up);
         atomicMax(&sm.bmax[2], uf);
       }
     }
-    __syncthreads();
+    __syncthreads();  // [B2] bounds; occupancy; next item's neighbour ranks
+    if (GATHER && nxt.r != BAD_KEY) prefetch_arena(sm, A, nxt, buf ^ 1, tid);
+    cp_async_commit();
+    if (tid < 32) {
+      // ---- warp 0: touched-node masks of the 27 neighbour blocks by dilating
+      // the occupancy bitmap (node n touched iff a base in n - {0,1,2}^3 is
+      // occupied), then the block inserts of the next table.  The insert
+      // latency overlaps the other warps' scatter.
+      const unsigned char* ob = reinterpret_cast<const unsigned char*>(sm.occ);
+      uint32_t rows2 = 0;  // dilated rows (i, j) for row = tid and row = tid + 32, one byte each
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int row = tid + 32 * h2, i = row >> 3, j = row & 7;
+        uint32_t acc8 = 0;
+#pragma unroll
+        for (int di = 0; di < 3; ++di)
+#pragma unroll
+          for (int dj = 0; dj < 3; ++dj)
+            if (i - di >= 0 && j - dj >= 0) acc8 |= ob[(i - di) * 8 + (j - dj)];
+        acc8 = (acc8 | (acc8 << 1) | (acc8 << 2)) & 0xFFu;
+        rows2 |= acc8 << (8 * h2);
+      }
+      uint32_t rk = BAD_KEY;
+      uint64_t mk = 0;
+      const int di = tid / 9 - 1, dj = (tid / 3) % 3 - 1, dk = tid % 3 - 1;
+#pragma unroll
+      for (int li = 0; li < 4; ++li)
+#pragma unroll
+        for (int lj = 0; lj < 4; ++lj) {
+          const int ai = 4 * di + 1 + li, aj = 4 * dj + 1 + lj;
+          const bool in = ai >= 0 && ai < 8 && aj >= 0 && aj < 8;
+          const int row = in ? ai * 8 + aj : 0;
+          const uint32_t r8 = (__shfl_sync(0xffffffffu, rows2, row & 31) >> (8 * (row >> 5))) & 0xFFu;
+          uint32_t nib = dk < 0 ? (r8 & 1u) << 3 : (dk == 0 ? (r8 >> 1) & 15u : (r8 >> 5) & 7u);
+          if (in) mk |= uint64_t(nib) << ((li << 4) | (lj << 2));
+        }
+      if (tid < 27 && mk) {
+        rk = hash_insert(A.S.hv, pack_key(B0 + di, B1 + dj, B2 + dk));
+        if (rk < A.S.hv.cap_blocks)
+          atomicOr((unsigned long long*)&A.S.nodemask[rk], (unsigned long long)mk);
+        else
+          rk = BAD_KEY;
+      }
+      if (tid < 27) sm.rank[tid] = rk;
+    }
     float iSm, iSp, iSf;
     const float Sm = fx_scale(__uint_as_float(sm.bmax[0]), iSm);
     const float Sp = fx_scale(__uint_as_float(sm.bmax[1]), iSp);
     const float Sf = fx_scale(__uint_as_float(sm.bmax[2]), iSf);
-    uint32_t lidx = 0;
-    uint2 binv = make_uint2(BAD_KEY, 0);
+    uint32_t binv = BAD_KEY;
     if (ok && !far) {
       // ---- P2G of the next step into the fixed-point arena
       float w[3][3], g[3][3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) bspline(d1[a], w[a], g[a]);
       const int ad0 = aaddr(ab[0], ab[1], ab[2]);
-      lidx = atomicAdd(&sm.cnt[ad0], 1u);
       const float mSm = m * Sm, mSp = m * Sp;
       // force: f = -(M grad w); grad w = (g0 w1 w2, w0 g1 w2, w0 w1 g2)/h
       const float fs = -Sf * ih;
@@ -744,89 +902,40 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
             sred(a0 + 4 * SCAT_N + o, magic_q(fmaf(wz, r0, fmaf(gz, s0, MAGIC))));
             sred(a0 + 5 * SCAT_N + o, magic_q(fmaf(wz, r1, fmaf(gz, s1, MAGIC))));
             sred(a0 + 6 * SCAT_N + o, magic_q(fmaf(wz, r2, fmaf(gz, s2, MAGIC))));
+            sred(a0 + 7 * SCAT_N + o, 1);
           }
         }
       }
     } else if (ok && far) {
-      scatter_global(A, nb, d1, m, vn, Cn, M, 0, binv);
+      scatter_global(A, nb, d1, m, vn, Cn, M, binv);
     }
-    __syncthreads();
-    // ---- K(n) = number of contributions to node n: 3x3x3 box sum of the
-    // base-cell counts (separable), plus node masks of the 27 blocks
-    for (int n = tid; n < 512; n += CTA) {
-      int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
-      int ad = aaddr(i, j, k);
-      uint32_t s = sm.cnt[ad];
-      if (k >= 1) s += sm.cnt[ad - 1];
-      if (k >= 2) s += sm.cnt[ad - 2];
-      sm.t1[ad] = s;
-    }
-    __syncthreads();
-    for (int n = tid; n < 512; n += CTA) {
-      int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
-      int ad = aaddr(i, j, k);
-      uint32_t s = sm.t1[ad];
-      if (j >= 1) s += sm.t1[ad - AJ];
-      if (j >= 2) s += sm.t1[ad - 2 * AJ];
-      sm.t2[ad] = s;
-    }
-    __syncthreads();
-    for (int n = tid; n < 512; n += CTA) {
-      int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
-      int ad = aaddr(i, j, k);
-      uint32_t s = sm.t2[ad];
-      if (i >= 1) s += sm.t2[ad - AI];
-      if (i >= 2) s += sm.t2[ad - 2 * AI];
-      sm.t1[ad] = s;  // K
-      if (s) {
-        int di = (i + 3) >> 2, dj = (j + 3) >> 2, dk = (k + 3) >> 2;
-        int l = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
-        atomicOr(&sm.mask[di * 9 + dj * 3 + dk][l >> 5], 1u << (l & 31));
-      }
-    }
-    __syncthreads();
-    if (tid < 27) {
-      uint64_t mk = (uint64_t(sm.mask[tid][1]) << 32) | sm.mask[tid][0];
-      uint32_t rk = BAD_KEY;
-      if (mk) {
-        int di = tid / 9 - 1, dj = (tid / 3) % 3 - 1, dk = tid % 3 - 1;
-        rk = hash_insert(A.S.hv, pack_key(B0 + di, B1 + dj, B2 + dk));
-        if (rk < A.S.hv.cap_blocks) atomicOr((unsigned long long*)&A.S.nodemask[rk], (unsigned long long)mk);
-        else rk = BAD_KEY;
-      }
-      sm.rank[tid] = rk;
-    }
-    __syncthreads();
-    // ---- bin reservations per arena base cell (one global atomic per cell)
-    for (int n = tid; n < 216; n += CTA) {
-      int i = n / 36, j = (n / 6) % 6, k = n % 6;
-      int ad = aaddr(i, j, k);
-      uint32_t c = sm.cnt[ad];
-      if (c) {
-        int di = (i + 3) >> 2, dj = (j + 3) >> 2, dk = (k + 3) >> 2;
-        uint32_t rk = sm.rank[di * 9 + dj * 3 + dk];
-        uint32_t lc = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
-        sm.t2[ad] = rk == BAD_KEY ? BAD_KEY : rk * 64 + lc;
-        sm.cnt[ad] = rk == BAD_KEY ? 0 : atomicAdd(&A.S.cell_count[rk * 64 + lc], c);
-      }
-    }
-    __syncthreads();
+    __syncthreads();  // [B3] arena complete; ranks and bin bases of the next table known
+    // ---- bins of the next step: cell key only; positions are assigned by
+    // k_bin.  Cell counts go out as fire-and-forget reductions.
     if (valid) {
       if (ok && !far) {
-        int ad0 = aaddr(ab[0], ab[1], ab[2]);
-        uint32_t k2 = sm.t2[ad0];
-        binv = k2 == BAD_KEY ? make_uint2(BAD_KEY, 0) : make_uint2(k2, sm.cnt[ad0] + lidx);
+        uint32_t rk = sm.rank[((ab[0] + 3) >> 2) * 9 + ((ab[1] + 3) >> 2) * 3 + ((ab[2] + 3) >> 2)];
+        uint32_t lc = (((ab[0] + 3) & 3) << 4) | (((ab[1] + 3) & 3) << 2) | ((ab[2] + 3) & 3);
+        binv = rk == BAD_KEY ? BAD_KEY : rk * 64 + lc;
       }
       A.bin_out[pos] = binv;
+    }
+    for (int n = tid; n < 216; n += CTA) {
+      int i = n / 36, j = (n / 6) % 6, k = n % 6;
+      uint32_t cc = sm.cnt[aaddr(i, j, k)];
+      if (cc) {
+        uint32_t rq = sm.rank[((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
+        uint32_t lc = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
+        if (rq != BAD_KEY) atomicAdd(&A.S.cell_count[rq * 64 + lc], cc);
+      }
     }
     // ---- flush the arena: value = (sum - K * MAGIC_BITS) / S
     for (int n = tid; n < 512; n += CTA) {
       int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
       int ad = aaddr(i, j, k);
-      uint32_t K = sm.t1[ad];
+      uint32_t K = uint32_t(sm.acc[7][ad]);
       if (!K) continue;
-      int di = (i + 3) >> 2, dj = (j + 3) >> 2, dk = (k + 3) >> 2;
-      uint32_t rk = sm.rank[di * 9 + dj * 3 + dk];
+      uint32_t rk = sm.rank[((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
       if (rk == BAD_KEY) continue;
       int l = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
       const uint32_t bias = K * MAGIC_BITS;
@@ -837,27 +946,43 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
       red_v4(&A.acc[2 * node], vals[0] * iSm, vals[1] * iSp, vals[2] * iSp, vals[3] * iSp);
       red_v4(&A.acc[2 * node + 1], vals[4] * iSf, vals[5] * iSf, vals[6] * iSf, 0.f);
     }
+    // ---- rotate: item i+3's metadata goes into this item's ring slot
+    if (tid == 0) fetch_item(A, n_items, sm.info[c]);
+    if (tid < 3) sm.bmax[tid] = 0;
+    pos = pos1;
+    valid = valid1;
+    pos1 = pos2;
+    valid1 = valid2;
+    src1 = src2;
+    buf ^= 1;
+    c = c == 2 ? 0 : c + 1;
   }
   vmax2_local = warp_max(vmax2_local);
   if ((tid & 31) == 0 && vmax2_local) atomicMax(&A.stS->vmax2_bits, vmax2_local);
 }
 
 // ------------------------------------------------------- state transfer
-// Upload: reference layout f64 -> SoA (x f64, rest f32).
+// Upload: reference layout f64 -> 128-byte records (x f64, rest f32).
 __global__ void k_upload(Particles P, int64_t off, int64_t n, const double* __restrict__ x,
                          const double* __restrict__ v, const double* __restrict__ C, const double* __restrict__ F,
                          const double* __restrict__ m, const double* __restrict__ V0,
                          const int64_t* __restrict__ mat) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     int64_t j = off + i;
-    for (int a = 0; a < 3; ++a) P.x[a][j] = x[3 * i + a];
-    for (int a = 0; a < 3; ++a) P.v[a][j] = float(v[3 * i + a]);
-    for (int q = 0; q < 9; ++q) P.C[q][j] = float(C[9 * i + q]);
-    for (int q = 0; q < 9; ++q) P.F[q][j] = float(F[9 * i + q]);
-    P.m[j] = float(m[i]);
-    P.V0[j] = float(V0[i]);
-    P.mat[j] = uint8_t(mat[i]);
-    P.pid[j] = uint32_t(j);
+    float w[REC_W];
+    for (int a = 0; a < 3; ++a) {
+      w[2 * a] = __int_as_float(__double2loint(x[3 * i + a]));
+      w[2 * a + 1] = __int_as_float(__double2hiint(x[3 * i + a]));
+    }
+    w[W_M] = float(m[i]);
+    w[W_V0] = float(V0[i]);
+    for (int q = 0; q < 9; ++q) w[W_F + q] = float(F[9 * i + q]);
+    w[W_PM] = __uint_as_float((uint32_t(j) & PID_MASK) | (uint32_t(mat[i]) << 29));
+    for (int a = 0; a < 3; ++a) w[W_V + a] = float(v[3 * i + a]);
+    for (int q = 0; q < 9; ++q) w[W_C + q] = float(C[9 * i + q]);
+    w[30] = w[31] = 0.f;
+    float4* o = P.rec + j * 8;
+    for (int c = 0; c < 8; ++c) o[c] = make_float4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
   }
 }
 
@@ -865,22 +990,32 @@ __global__ void k_upload(Particles P, int64_t off, int64_t n, const double* __re
 __global__ void k_download(Particles P, int64_t n, int64_t lo, int64_t hi, double* x, double* v, double* C,
                            double* F, double* sigma, double* jac, const Material* mats, int n_mat) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    int64_t p = P.pid[i];
+    const float4* r4 = P.rec + i * 8;
+    float w[REC_W];
+    for (int c = 0; c < 8; ++c) {
+      float4 q = r4[c];
+      w[4 * c] = q.x;
+      w[4 * c + 1] = q.y;
+      w[4 * c + 2] = q.z;
+      w[4 * c + 3] = q.w;
+    }
+    const uint32_t pm = __float_as_uint(w[W_PM]);
+    int64_t p = pm & PID_MASK;
     if (p < lo || p >= hi) continue;
     int64_t o = p - lo;
     if (x)
-      for (int a = 0; a < 3; ++a) x[3 * o + a] = P.x[a][i];
+      for (int a = 0; a < 3; ++a) x[3 * o + a] = __hiloint2double(__float_as_int(w[2 * a + 1]), __float_as_int(w[2 * a]));
     if (v)
-      for (int a = 0; a < 3; ++a) v[3 * o + a] = P.v[a][i];
+      for (int a = 0; a < 3; ++a) v[3 * o + a] = w[W_V + a];
     if (C)
-      for (int q = 0; q < 9; ++q) C[9 * o + q] = P.C[q][i];
+      for (int q = 0; q < 9; ++q) C[9 * o + q] = w[W_C + q];
     float Fl[9];
-    for (int q = 0; q < 9; ++q) Fl[q] = P.F[q][i];
+    for (int q = 0; q < 9; ++q) Fl[q] = w[W_F + q];
     if (F)
       for (int q = 0; q < 9; ++q) F[9 * o + q] = Fl[q];
     if (sigma || jac) {
       float tau[6], J = 1.f;
-      int mt = P.mat[i];
+      int mt = int(pm >> 29);
       Material mm = mats[mt < n_mat ? mt : 0];
       if (!hencky_dp(Fl, mm, false, tau, J)) {
         for (int q = 0; q < 6; ++q) tau[q] = NAN;
@@ -897,6 +1032,7 @@ __global__ void k_download(Particles P, int64_t n, int64_t lo, int64_t hi, doubl
 }
 
 }  // namespace smpm
+
 
 // =================================================================== host
 using namespace smpm;
@@ -915,7 +1051,7 @@ struct smpm_sim {
   std::vector<void*> allocs;
   Particles state[2];
   int cur = 0;  // state buffer holding the current particles
-  uint2* bin = nullptr;
+  uint32_t* bin = nullptr;
   uint32_t* perm = nullptr;
   TableDev tab[2];
   int S = 0;  // table holding the current particles' bins
@@ -993,14 +1129,7 @@ uint64_t next_pow2(uint64_t v) {
 }
 
 int alloc_particles(smpm_sim* s, Particles& P, int64_t cap) {
-  for (int a = 0; a < 3; ++a) DA(P.x[a], cap);
-  for (int a = 0; a < 3; ++a) DA(P.v[a], cap);
-  for (int q = 0; q < 9; ++q) DA(P.C[q], cap);
-  for (int q = 0; q < 9; ++q) DA(P.F[q], cap);
-  DA(P.m, cap);
-  DA(P.V0, cap);
-  DA(P.mat, cap);
-  DA(P.pid, cap);
+  DA(P.rec, size_t(cap) * 8);
   return SMPM_OK;
 }
 
@@ -1025,6 +1154,7 @@ int alloc_grid(smpm_sim* s) {
     DA(T.cell_off, size_t(cb) * 64);
     DA(T.block_total, cb);
     DA(T.block_items, cb);
+    DA(T.nbr8, size_t(cb) * 8);
     DA(T.items, s->cap_items);
     DA(T.tile_sums, 3 * size_t(s->max_tiles));
     CK(cudaMemsetAsync(T.hv.keys, 0xFF, s->n_slots * 8, s->stream));
@@ -1127,7 +1257,7 @@ int grow_grid(smpm_sim* s, uint32_t need) {
   for (int t = 0; t < 2; ++t) {
     TableDev& T = s->tab[t];
     void* ps[] = {T.hv.keys, T.hv.vals, T.hv.counter, T.hv.active_keys, T.hv.slot_of_rank, T.nodemask,
-                  T.cell_count, T.cell_off, T.block_total, T.block_items, T.items, T.tile_sums};
+                  T.cell_count, T.cell_off, T.block_total, T.block_items, T.nbr8, T.items, T.tile_sums};
     for (void* p : ps) grid_ptrs.push_back(p);
   }
   grid_ptrs.push_back(s->acc);
