@@ -162,15 +162,19 @@ struct Material {
 
 __device__ inline void jacobi_rotate(float& app, float& arr, float& apr, float& aop, float& aor, float* q, int r0,
                                      int r1) {
-  // materials.py:88-122 in fp32: annihilate a[r0][r1]
+  // materials.py:88-122 in fp32: annihilate a[r0][r1].  The angle only needs
+  // to be approximately right (c and s are exactly normalised from t, so the
+  // accumulated frame stays orthonormal); fast reciprocals are used.
   if (apr == 0.0f) return;
-  float theta = 0.5f * (arr - app) / apr;
-  float th2 = theta * theta;
-  float t = isinf(th2) ? 0.5f / fabsf(theta) : 1.0f / (fabsf(theta) + sqrtf(1.0f + th2));
+  const float theta = __fdividef(0.5f * (arr - app), apr);
+  const float th2 = theta * theta;
+  // t = sign(theta) / (|theta| + sqrt(1 + theta^2)); for huge |theta|, 1/(2 theta)
+  const float q1 = 1.0f + th2;
+  float t = th2 < 1e30f ? __fdividef(1.0f, fabsf(theta) + q1 * rsqrtf(q1)) : __fdividef(0.5f, fabsf(theta));
   if (theta < 0.0f) t = -t;
-  float c = rsqrtf(1.0f + t * t);
-  float s = t * c;
-  float tau = s / (1.0f + c);
+  const float c = rsqrtf(1.0f + t * t);
+  const float s = t * c;
+  const float tau = __fdividef(s, 1.0f + c);
   app = app - t * apr;
   arr = arr + t * apr;
   apr = 0.0f;
@@ -185,43 +189,82 @@ __device__ inline void jacobi_rotate(float& app, float& arr, float& apr, float& 
   }
 }
 
+// log1p / expm1 for the small arguments of the constitutive update (strains,
+// return-map increments): odd atanh series / Taylor polynomial, ~1 ulp for
+// |x| <= 1/4, libm beyond.
+__device__ __forceinline__ float log1p_small(float x) {
+  if (fabsf(x) > 0.25f) return log1pf(x);
+  const float z = x / (2.0f + x);  // log1p(x) = 2 atanh(z), |z| <= 1/7
+  const float z2 = z * z;
+  float p = fmaf(z2, 1.0f / 11.0f, 1.0f / 9.0f);
+  p = fmaf(p, z2, 1.0f / 7.0f);
+  p = fmaf(p, z2, 1.0f / 5.0f);
+  p = fmaf(p, z2, 1.0f / 3.0f);
+  return 2.0f * z * fmaf(p, z2, 1.0f);
+}
+__device__ __forceinline__ float expm1_small(float x) {
+  if (fabsf(x) > 0.25f) return expm1f(x);
+  float p = fmaf(x, 1.0f / 40320.0f, 1.0f / 5040.0f);
+  p = fmaf(p, x, 1.0f / 720.0f);
+  p = fmaf(p, x, 1.0f / 120.0f);
+  p = fmaf(p, x, 1.0f / 24.0f);
+  p = fmaf(p, x, 1.0f / 6.0f);
+  p = fmaf(p, x, 0.5f);
+  p = fmaf(p, x, 1.0f);
+  return p * x;
+}
+
 // Hencky elasticity + cohesionless Drucker-Prager return map in principal
-// space (materials.py:169-238), fp32.  F is row-major 3x3.  Returns false on a
-// degenerate F.  Outputs the Kirchhoff stress tau = J sigma (xx,yy,zz,xy,xz,yz)
-// and J; when `project`, the return-mapped F is written back.
-__device__ inline bool hencky_dp(float F[9], const Material& mat, bool project, float tau[6], float& J) {
-  float det = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
-              F[2] * (F[3] * F[7] - F[4] * F[6]);
+// space (materials.py:169-238), fp32, on H = F - I (row-major).  Carrying the
+// displacement gradient instead of F keeps small strains exact: C - I =
+// H + H^T + H^T H has no cancellation, eigen-strains come from log1p, and the
+// return-mapped update H += (I + H) V diag(expm1(e' - e)) V^T never forms
+// I + small.  Returns false on a degenerate F (det F <= 0 or non-finite).
+// Outputs the Kirchhoff stress tau = J sigma (xx,yy,zz,xy,xz,yz) and J; when
+// `project`, the return-mapped H is written back.
+__device__ inline bool hencky_dp_eig(float H[9], const Material& mat, bool project, float tau[6], float& J) {
+  // det(I + H) = 1 + tr H + (principal 2x2 minors of H) + det H
+  const float trH = H[0] + H[4] + H[8];
+  const float m2 = (H[0] * H[4] - H[1] * H[3]) + (H[0] * H[8] - H[2] * H[6]) + (H[4] * H[8] - H[5] * H[7]);
+  const float dH = H[0] * (H[4] * H[8] - H[5] * H[7]) - H[1] * (H[3] * H[8] - H[5] * H[6]) +
+                   H[2] * (H[3] * H[7] - H[4] * H[6]);
+  const float det = 1.0f + (trH + (m2 + dH));
   if (!(det > 0.0f) || !isfinite(det)) return false;
-  // C = F^T F (materials.py:181-189)
-  float a00 = F[0] * F[0] + F[3] * F[3] + F[6] * F[6];
-  float a11 = F[1] * F[1] + F[4] * F[4] + F[7] * F[7];
-  float a22 = F[2] * F[2] + F[5] * F[5] + F[8] * F[8];
-  float a01 = F[0] * F[1] + F[3] * F[4] + F[6] * F[7];
-  float a02 = F[0] * F[2] + F[3] * F[5] + F[6] * F[8];
-  float a12 = F[1] * F[2] + F[4] * F[5] + F[7] * F[8];
+  // C - I = H + H^T + H^T H  (materials.py:181-189 shifted by I)
+  float a00 = 2.f * H[0] + (H[0] * H[0] + H[3] * H[3] + H[6] * H[6]);
+  float a11 = 2.f * H[4] + (H[1] * H[1] + H[4] * H[4] + H[7] * H[7]);
+  float a22 = 2.f * H[8] + (H[2] * H[2] + H[5] * H[5] + H[8] * H[8]);
+  float a01 = (H[1] + H[3]) + (H[0] * H[1] + H[3] * H[4] + H[6] * H[7]);
+  float a02 = (H[2] + H[6]) + (H[0] * H[2] + H[3] * H[5] + H[6] * H[8]);
+  float a12 = (H[5] + H[7]) + (H[1] * H[2] + H[4] * H[5] + H[7] * H[8]);
   float V[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
-  // cyclic Jacobi (materials.py:125-144); fp32 stopping rule
+  // cyclic Jacobi (materials.py:125-144); rotations are shift-invariant, the
+  // stopping rule is relative to |C - I|
 #pragma unroll 1
   for (int sweep = 0; sweep < 8; ++sweep) {
     float off = fabsf(a01) + fabsf(a02) + fabsf(a12);
     float scale = fabsf(a00) + fabsf(a11) + fabsf(a22) + off;
-    if (off <= 1e-7f * scale) break;
-    jacobi_rotate(a00, a11, a01, a02, a12, V, 0, 1);  // o = 2: a[2][0], a[2][1]
-    jacobi_rotate(a00, a22, a02, a01, a12, V, 0, 2);  // o = 1: a[1][0], a[1][2]
-    jacobi_rotate(a11, a22, a12, a01, a02, V, 1, 2);  // o = 0: a[0][1], a[0][2]
+    if (off <= 1e-6f * scale) break;
+    // threshold Jacobi: elements already below the per-element share of the
+    // tolerance are not rotated
+    const float thr = 3e-7f * scale;
+    if (fabsf(a01) > thr) jacobi_rotate(a00, a11, a01, a02, a12, V, 0, 1);  // o = 2: a[2][0], a[2][1]
+    if (fabsf(a02) > thr) jacobi_rotate(a00, a22, a02, a01, a12, V, 0, 2);  // o = 1: a[1][0], a[1][2]
+    if (fabsf(a12) > thr) jacobi_rotate(a11, a22, a12, a01, a02, V, 1, 2);  // o = 0: a[0][1], a[0][2]
   }
-  if (!(a00 > 0.0f) || !(a11 > 0.0f) || !(a22 > 0.0f)) return false;
-  float lam3[3] = {a00, a11, a22};
-  float U[9];
-  float e[3];
+  // eigenvalues of C are 1 + mu_k
+  if (!(a00 > -1.0f) || !(a11 > -1.0f) || !(a22 > -1.0f)) return false;
+  const float mu3[3] = {a00, a11, a22};
+  float U[9], e[3], e0[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    float inv_s = rsqrtf(lam3[k]);
+    const float inv_s = rsqrtf(1.0f + mu3[k]);
+    // u_k = (I + H) v_k / s_k
 #pragma unroll
     for (int i = 0; i < 3; ++i)
-      U[3 * i + k] = (F[3 * i] * V[k] + F[3 * i + 1] * V[3 + k] + F[3 * i + 2] * V[6 + k]) * inv_s;
-    e[k] = 0.5f * logf(lam3[k]);
+      U[3 * i + k] = (V[3 * i + k] + (H[3 * i] * V[k] + H[3 * i + 1] * V[3 + k] + H[3 * i + 2] * V[6 + k])) * inv_s;
+    e[k] = 0.5f * log1p_small(mu3[k]);
+    e0[k] = e[k];
   }
   if (mat.kind == 1) {
     // materials.py:147-166
@@ -244,12 +287,23 @@ __device__ inline bool hencky_dp(float F[9], const Material& mat, bool project, 
       }
     }
     if (changed && project) {
-      float q0 = expf(e[0]), q1 = expf(e[1]), q2 = expf(e[2]);
+      // F' = U diag(exp e') V^T = F V diag(exp(e' - e)) V^T
+      //  => H' = H + (I + H) D,  D = V diag(expm1(e' - e)) V^T
+      const float r0 = expm1_small(e[0] - e0[0]), r1 = expm1_small(e[1] - e0[1]), r2 = expm1_small(e[2] - e0[2]);
+      float D[9];
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-          F[3 * i + j] = U[3 * i] * q0 * V[3 * j] + U[3 * i + 1] * q1 * V[3 * j + 1] + U[3 * i + 2] * q2 * V[3 * j + 2];
+          D[3 * i + j] = V[3 * i] * r0 * V[3 * j] + V[3 * i + 1] * r1 * V[3 * j + 1] + V[3 * i + 2] * r2 * V[3 * j + 2];
+      float Hn[9];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          Hn[3 * i + j] = H[3 * i + j] + (D[3 * i + j] + (H[3 * i] * D[j] + H[3 * i + 1] * D[3 + j] + H[3 * i + 2] * D[6 + j]));
+#pragma unroll
+      for (int q = 0; q < 9; ++q) H[q] = Hn[q];
     }
   }
   float tr = e[0] + e[1] + e[2];
@@ -264,6 +318,139 @@ __device__ inline bool hencky_dp(float F[9], const Material& mat, bool project, 
   tau[3] = t0 * U[0] * U[3] + t1 * U[1] * U[4] + t2 * U[2] * U[5];
   tau[4] = t0 * U[0] * U[6] + t1 * U[1] * U[7] + t2 * U[2] * U[8];
   tau[5] = t0 * U[3] * U[6] + t1 * U[4] * U[7] + t2 * U[5] * U[8];
+  return true;
+}
+
+// symmetric 3x3 stored (xx, yy, zz, xy, xz, yz); product of two commuting
+// symmetric matrices (powers / polynomials of one matrix)
+__device__ __forceinline__ void sym_mul(const float a[6], const float b[6], float c[6]) {
+  c[0] = a[0] * b[0] + a[3] * b[3] + a[4] * b[4];
+  c[1] = a[3] * b[3] + a[1] * b[1] + a[5] * b[5];
+  c[2] = a[4] * b[4] + a[5] * b[5] + a[2] * b[2];
+  c[3] = a[0] * b[3] + a[3] * b[1] + a[4] * b[5];
+  c[4] = a[0] * b[4] + a[3] * b[5] + a[4] * b[2];
+  c[5] = a[3] * b[4] + a[1] * b[5] + a[5] * b[2];
+}
+
+// Same model without an eigen-decomposition, for small elastic strain
+// (||B - I||_inf <= 0.05, the normal case: Drucker-Prager keeps elastic
+// strains small).  Hencky strain eps = 1/2 log(B), B = F F^T = I + X, as a
+// 7-term series (truncation < 0.05^8/8 relative); the return map is isotropic
+// so it acts on the tensor (deviator norm = Frobenius norm = principal norm,
+// materials.py:147-166); tau = 2 mu eps' + lam tr(eps') I equals
+// sum_k t_k u_k u_k^T of materials.py:233-238; and since eps' is a polynomial
+// of eps, F' = U exp(e') V^T = exp(eps' - eps) F.
+__device__ inline bool hencky_dp(float H[9], const Material& mat, bool project, float tau[6], float& J) {
+  const float trH = H[0] + H[4] + H[8];
+  const float m2 = (H[0] * H[4] - H[1] * H[3]) + (H[0] * H[8] - H[2] * H[6]) + (H[4] * H[8] - H[5] * H[7]);
+  const float dH = H[0] * (H[4] * H[8] - H[5] * H[7]) - H[1] * (H[3] * H[8] - H[5] * H[6]) +
+                   H[2] * (H[3] * H[7] - H[4] * H[6]);
+  const float det = 1.0f + (trH + (m2 + dH));
+  if (!(det > 0.0f) || !isfinite(det)) return false;
+  // X = B - I = H + H^T + H H^T
+  float X[6];
+  X[0] = 2.f * H[0] + (H[0] * H[0] + H[1] * H[1] + H[2] * H[2]);
+  X[1] = 2.f * H[4] + (H[3] * H[3] + H[4] * H[4] + H[5] * H[5]);
+  X[2] = 2.f * H[8] + (H[6] * H[6] + H[7] * H[7] + H[8] * H[8]);
+  X[3] = (H[1] + H[3]) + (H[0] * H[3] + H[1] * H[4] + H[2] * H[5]);
+  X[4] = (H[2] + H[6]) + (H[0] * H[6] + H[1] * H[7] + H[2] * H[8]);
+  X[5] = (H[5] + H[7]) + (H[3] * H[6] + H[4] * H[7] + H[5] * H[8]);
+  const float nx = fmaxf(fabsf(X[0]) + fabsf(X[3]) + fabsf(X[4]),
+                         fmaxf(fabsf(X[3]) + fabsf(X[1]) + fabsf(X[5]), fabsf(X[4]) + fabsf(X[5]) + fabsf(X[2])));
+  if (!(nx <= 0.05f)) return hencky_dp_eig(H, mat, project, tau, J);
+  // log(I + X) = X (1 - X (1/2 - X (1/3 - X (1/4 - X (1/5 - X (1/6 - X/7))))))  (Horner)
+  float P[6], T[6];
+  const float coef[6] = {1.f / 6.f, 1.f / 5.f, 1.f / 4.f, 1.f / 3.f, 1.f / 2.f, 1.f};
+#pragma unroll
+  for (int q = 0; q < 6; ++q) P[q] = -X[q] * (1.f / 7.f);
+  P[0] += coef[0];
+  P[1] += coef[0];
+  P[2] += coef[0];
+#pragma unroll
+  for (int it = 1; it < 6; ++it) {
+    sym_mul(X, P, T);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) P[q] = -T[q];
+    P[0] += coef[it];
+    P[1] += coef[it];
+    P[2] += coef[it];
+  }
+  float eps[6];
+  sym_mul(X, P, eps);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) eps[q] *= 0.5f;
+  float e2[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) e2[q] = eps[q];
+  float tr = eps[0] + eps[1] + eps[2];
+  bool changed = false;
+  if (mat.kind == 1) {
+    if (tr > 0.0f) {  // apex: no tensile strength
+      changed = (eps[0] != 0.f) || (eps[1] != 0.f) || (eps[2] != 0.f) || (eps[3] != 0.f) || (eps[4] != 0.f) ||
+                (eps[5] != 0.f);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) e2[q] = 0.f;
+    } else {
+      const float m = tr * (1.0f / 3.0f);
+      const float h0 = eps[0] - m, h1 = eps[1] - m, h2 = eps[2] - m;
+      const float en = sqrtf(h0 * h0 + h1 * h1 + h2 * h2 + 2.f * (eps[3] * eps[3] + eps[4] * eps[4] + eps[5] * eps[5]));
+      const float dg = en + mat.alpha * mat.ratio * tr;
+      if (dg > 0.0f && en > 0.0f) {
+        const float c = dg / en;
+        e2[0] = eps[0] - c * h0;
+        e2[1] = eps[1] - c * h1;
+        e2[2] = eps[2] - c * h2;
+        e2[3] = eps[3] - c * eps[3];
+        e2[4] = eps[4] - c * eps[4];
+        e2[5] = eps[5] - c * eps[5];
+        changed = true;
+      }
+    }
+  }
+  if (changed && project) {
+    // H' = H + E (I + H), E = exp(D) - I = D (1 + D/2 (1 + D/3 (1 + D/4))), D = eps' - eps
+    float D[6], E[6], Q[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      D[q] = e2[q] - eps[q];
+      Q[q] = D[q] * 0.25f;
+    }
+    Q[0] += 1.f;
+    Q[1] += 1.f;
+    Q[2] += 1.f;
+    sym_mul(D, Q, T);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) Q[q] = T[q] * (1.f / 3.f);
+    Q[0] += 1.f;
+    Q[1] += 1.f;
+    Q[2] += 1.f;
+    sym_mul(D, Q, T);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) Q[q] = T[q] * 0.5f;
+    Q[0] += 1.f;
+    Q[1] += 1.f;
+    Q[2] += 1.f;
+    sym_mul(D, Q, E);
+    // full 3x3 of E (symmetric)
+    const float Ef[9] = {E[0], E[3], E[4], E[3], E[1], E[5], E[4], E[5], E[2]};
+    float Hn[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        Hn[3 * i + j] = H[3 * i + j] + (Ef[3 * i + j] + (Ef[3 * i] * H[j] + Ef[3 * i + 1] * H[3 + j] + Ef[3 * i + 2] * H[6 + j]));
+#pragma unroll
+    for (int q = 0; q < 9; ++q) H[q] = Hn[q];
+  }
+  const float tr2 = e2[0] + e2[1] + e2[2];
+  const float lt = mat.lam * tr2, m2u = 2.0f * mat.mu;
+  tau[0] = m2u * e2[0] + lt;
+  tau[1] = m2u * e2[1] + lt;
+  tau[2] = m2u * e2[2] + lt;
+  tau[3] = m2u * e2[3];
+  tau[4] = m2u * e2[4];
+  tau[5] = m2u * e2[5];
+  J = expf(tr2);
   return true;
 }
 

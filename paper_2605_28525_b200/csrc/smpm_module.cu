@@ -382,14 +382,15 @@ __global__ void k_g2p(HashView h, double inv_h, double hh, double dt, int64_t n,
           }
         }
     const float dinv = 4.0f * ih * ih;
-    float Fo[9];
-    for (int q = 0; q < 9; ++q) Fo[q] = float(F[9 * p + q]);
+    float Ho[9];  // H = F - I: F <- F + dt a F  <=>  H <- H + dt a (I + H)
+    for (int q = 0; q < 9; ++q) Ho[q] = float(F[9 * p + q] - ((q == 0 || q == 4 || q == 8) ? 1.0 : 0.0));
     for (int a = 0; a < 3; ++a) {
       v[3 * p + a] = vv[a];
       for (int b = 0; b < 3; ++b) {
         C[9 * p + 3 * a + b] = B[3 * a + b] * dinv;
-        F[9 * p + 3 * a + b] =
-            Fo[3 * a + b] + float(dt) * (A[3 * a] * Fo[b] + A[3 * a + 1] * Fo[3 + b] + A[3 * a + 2] * Fo[6 + b]);
+        const float hn = Ho[3 * a + b] + float(dt) * (A[3 * a + b] + (A[3 * a] * Ho[b] + A[3 * a + 1] * Ho[3 + b] +
+                                                                    A[3 * a + 2] * Ho[6 + b]));
+        F[9 * p + 3 * a + b] = double(hn) + (a == b ? 1.0 : 0.0);
       }
       x[3 * p + a] = __dadd_rn(x[3 * p + a], __dmul_rn(dt, double(vv[a])));
     }
@@ -399,15 +400,15 @@ __global__ void k_g2p(HashView h, double inv_h, double hh, double dt, int64_t n,
 __global__ void k_stress(const Material* __restrict__ mats, int n_mat, int64_t n, double* F, double* sigma,
                          double* jac, const int64_t* __restrict__ mat_id, unsigned long long* err) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
-    float Fl[9], tau[6], J;
-    for (int q = 0; q < 9; ++q) Fl[q] = float(F[9 * p + q]);
+    float Fl[9], tau[6], J;  // H = F - I
+    for (int q = 0; q < 9; ++q) Fl[q] = float(F[9 * p + q] - ((q == 0 || q == 4 || q == 8) ? 1.0 : 0.0));
     int64_t mid = mat_id[p];
     Material m = mats[(mid >= 0 && mid < n_mat) ? mid : 0];
     if (!hencky_dp(Fl, m, true, tau, J)) {
       err_report(err, ERR_DEGENERATE_F, p);
       continue;
     }
-    for (int q = 0; q < 9; ++q) F[9 * p + q] = Fl[q];
+    for (int q = 0; q < 9; ++q) F[9 * p + q] = double(Fl[q]) + ((q == 0 || q == 4 || q == 8) ? 1.0 : 0.0);
     jac[p] = J;
     const int map[9] = {0, 3, 4, 3, 1, 5, 4, 5, 2};
     float iJ = 1.0f / J;

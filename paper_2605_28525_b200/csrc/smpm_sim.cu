@@ -55,7 +55,7 @@ __device__ __forceinline__ int aaddr(int i, int j, int k) { return k + AJ * j + 
 __device__ __forceinline__ int gaddr(int i, int j, int k) { return (k ^ ((j & 1) << 2)) + 8 * j + 48 * i; }
 
 // Particle record: one 128-byte line per particle (float word offsets).
-//   x f64[3] @0 | m @6 | V0 @7 | F[9] @8 | pid|mat<<29 @17 | v[3] @18 | C[9] @21 | pad @30
+//   x f64[3] @0 | m @6 | V0 @7 | H = F - I [9] @8 | pid|mat<<29 @17 | v[3] @18 | C[9] @21 | pad @30
 // G2P reads chunks 0..4 (80 B: x, m, V0, F, pid/mat); the kernel writes all 8.
 constexpr int REC_W = 32;
 constexpr int W_M = 6, W_V0 = 7, W_F = 8, W_PM = 17, W_V = 18, W_C = 21;
@@ -593,10 +593,6 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
       }
     }
     if (valid1) prefetch_record<GATHER>(sm, A, tid, src1);
-    // item i+2: sorted position and source index (consumed one item later)
-    uint32_t pos2 = 0, src2 = 0;
-    const bool valid2 = item_slot(A, nn.r, nn.g, tid, pos2);
-    if (valid2) src2 = A.perm[pos2];
 
     double xn[3];
     float vn[3], Cn[9], M[6], m = 0.f, d1[3];
@@ -692,12 +688,14 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
         vn[2] = v2;
         const float dth = float(dt) * ih;  // a = (sum v g) / h
         float A9[9] = {a00 * dth, a01 * dth, a02 * dth, a10 * dth, a11 * dth, a12 * dth, a20 * dth, a21 * dth, a22 * dth};
+        // F <- (I + dt a) F on H = F - I:  H <- H + dt a + dt a H
         float Fn[9];
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
           for (int j = 0; j < 3; ++j)
-            Fn[3 * i + j] = F[3 * i + j] + (A9[3 * i] * F[j] + A9[3 * i + 1] * F[3 + j] + A9[3 * i + 2] * F[6 + j]);
+            Fn[3 * i + j] =
+                F[3 * i + j] + (A9[3 * i + j] + (A9[3 * i] * F[j] + A9[3 * i + 1] * F[3 + j] + A9[3 * i + 2] * F[6 + j]));
 #pragma unroll
         for (int q = 0; q < 9; ++q) F[q] = Fn[q];
         xn[0] = __dadd_rn(xn[0], __dmul_rn(dt, double(v0)));
@@ -809,11 +807,22 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
     __syncthreads();  // [B2] bounds; occupancy; next item's neighbour ranks
     if (GATHER && nxt.r != BAD_KEY) prefetch_arena(sm, A, nxt, buf ^ 1, tid);
     cp_async_commit();
+    // item i+2: raw index loads now, consumed after the scatter
+    const uint32_t key2 = nn.r == BAD_KEY ? 0u : nn.r * 64 + (tid & 63);
+    const uint32_t slot2 = nn.g * SLOTS + (tid >> 6);
+    uint32_t cnt2 = 0, off2 = 0;
+    if (nn.r != BAD_KEY) {
+      cnt2 = A.B.cell_count[key2];
+      off2 = A.B.cell_off[key2];
+    }
+    // ---- warp 0: touched-node masks of the 27 neighbour blocks by dilating
+    // the occupancy bitmap (node n touched iff a base in n - {0,1,2}^3 is
+    // occupied) and a probe of each block's hash slot; the probe latency
+    // overlaps the scatter, the insert resolves after it.
+    uint64_t mk = 0;
+    uint64_t ins_key = 0, probe_key = 0;
+    uint32_t probe_val = EMPTY_VAL;
     if (tid < 32) {
-      // ---- warp 0: touched-node masks of the 27 neighbour blocks by dilating
-      // the occupancy bitmap (node n touched iff a base in n - {0,1,2}^3 is
-      // occupied), then the block inserts of the next table.  The insert
-      // latency overlaps the other warps' scatter.
       const unsigned char* ob = reinterpret_cast<const unsigned char*>(sm.occ);
       uint32_t rows2 = 0;  // dilated rows (i, j) for row = tid and row = tid + 32, one byte each
 #pragma unroll
@@ -828,8 +837,6 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
         acc8 = (acc8 | (acc8 << 1) | (acc8 << 2)) & 0xFFu;
         rows2 |= acc8 << (8 * h2);
       }
-      uint32_t rk = BAD_KEY;
-      uint64_t mk = 0;
       const int di = tid / 9 - 1, dj = (tid / 3) % 3 - 1, dk = tid % 3 - 1;
 #pragma unroll
       for (int li = 0; li < 4; ++li)
@@ -843,13 +850,11 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
           if (in) mk |= uint64_t(nib) << ((li << 4) | (lj << 2));
         }
       if (tid < 27 && mk) {
-        rk = hash_insert(A.S.hv, pack_key(B0 + di, B1 + dj, B2 + dk));
-        if (rk < A.S.hv.cap_blocks)
-          atomicOr((unsigned long long*)&A.S.nodemask[rk], (unsigned long long)mk);
-        else
-          rk = BAD_KEY;
+        ins_key = pack_key(B0 + di, B1 + dj, B2 + dk);
+        const uint32_t sl = uint32_t(mix64(ins_key)) & A.S.hv.mask;
+        probe_key = ld_volatile_u64(&A.S.hv.keys[sl]);
+        probe_val = ld_volatile_u32(&A.S.hv.vals[sl]);
       }
-      if (tid < 27) sm.rank[tid] = rk;
     }
     float iSm, iSp, iSf;
     const float Sm = fx_scale(__uint_as_float(sm.bmax[0]), iSm);
@@ -909,7 +914,25 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
     } else if (ok && far) {
       scatter_global(A, nb, d1, m, vn, Cn, M, binv);
     }
-    __syncthreads();  // [B3] arena complete; ranks and bin bases of the next table known
+    if (tid < 27) {
+      uint32_t rk = BAD_KEY;
+      if (mk) {
+        rk = (probe_key == ins_key && probe_val != EMPTY_VAL) ? probe_val : hash_insert(A.S.hv, ins_key);
+        if (rk < A.S.hv.cap_blocks)
+          atomicOr((unsigned long long*)&A.S.nodemask[rk], (unsigned long long)mk);
+        else
+          rk = BAD_KEY;
+      }
+      sm.rank[tid] = rk;
+    }
+    // item i+2's sorted position and source index (consumed one item later)
+    uint32_t pos2 = 0, src2 = 0;
+    const bool valid2 = nn.r != BAD_KEY && slot2 < cnt2;
+    if (valid2) {
+      pos2 = off2 - cnt2 + slot2;  // k_bin advanced cell_off to the cell's end
+      src2 = A.perm[pos2];
+    }
+    __syncthreads();  // [B3] arena complete; ranks of the next table known
     // ---- bins of the next step: cell key only; positions are assigned by
     // k_bin.  Cell counts go out as fire-and-forget reductions.
     if (valid) {
@@ -976,7 +999,7 @@ __global__ void k_upload(Particles P, int64_t off, int64_t n, const double* __re
     }
     w[W_M] = float(m[i]);
     w[W_V0] = float(V0[i]);
-    for (int q = 0; q < 9; ++q) w[W_F + q] = float(F[9 * i + q]);
+    for (int q = 0; q < 9; ++q) w[W_F + q] = float(F[9 * i + q] - ((q == 0 || q == 4 || q == 8) ? 1.0 : 0.0));
     w[W_PM] = __uint_as_float((uint32_t(j) & PID_MASK) | (uint32_t(mat[i]) << 29));
     for (int a = 0; a < 3; ++a) w[W_V + a] = float(v[3 * i + a]);
     for (int q = 0; q < 9; ++q) w[W_C + q] = float(C[9 * i + q]);
@@ -1009,10 +1032,10 @@ __global__ void k_download(Particles P, int64_t n, int64_t lo, int64_t hi, doubl
       for (int a = 0; a < 3; ++a) v[3 * o + a] = w[W_V + a];
     if (C)
       for (int q = 0; q < 9; ++q) C[9 * o + q] = w[W_C + q];
-    float Fl[9];
+    float Fl[9];  // H = F - I
     for (int q = 0; q < 9; ++q) Fl[q] = w[W_F + q];
     if (F)
-      for (int q = 0; q < 9; ++q) F[9 * o + q] = Fl[q];
+      for (int q = 0; q < 9; ++q) F[9 * o + q] = double(Fl[q]) + ((q == 0 || q == 4 || q == 8) ? 1.0 : 0.0);
     if (sigma || jac) {
       float tau[6], J = 1.f;
       int mt = int(pm >> 29);
