@@ -193,6 +193,31 @@ int64_t smpm_sim_num_particles(const smpm_sim* s);
 double smpm_sim_vmax(smpm_sim* s);
 int smpm_sim_launch_count(const smpm_sim* s, int64_t* kernels_per_step);
 
+/* ---------------------------------------------------- slab decomposition
+ * Multi-GPU (the reference is single-process, PAPER.md:335-337
+ * lists multi-GPU as future work).  A rank owns the particles whose base
+ * block has block-x in [bx0, bx1).  After smpm_sim_step the caller (NCCL via
+ * torch.distributed) moves:
+ *   1. smpm_sim_exchange_pack(mode 0/1): partial node sums of blocks left /
+ *      right of the slab -> owner, which smpm_sim_exchange_unpack(set=0)s them;
+ *   2. smpm_sim_exchange_pack(mode 2): the owner's full sums of its layer
+ *      bx == bx0 -> left neighbour, unpacked with set=1 (identical bits on
+ *      both sides of the interface);
+ *   3. smpm_sim_migrants(side, out): 128-byte records of particles that left the
+ *      slab -> neighbour's smpm_sim_accept (appended and binned).
+ * Block records are 2064 bytes (key, node mask, 64 x 8 floats). */
+int smpm_sim_set_slab(smpm_sim* s, int32_t bx0, int32_t bx1, int64_t pid_base, int64_t migrant_capacity);
+int smpm_sim_exchange_pack(smpm_sim* s, int mode, void* out /*device*/, int64_t cap_blocks, int64_t* n_out);
+int smpm_sim_exchange_unpack(smpm_sim* s, const void* in /*device*/, int64_t n, int set);
+/* count of departing particles (side 0 left, 1 right); copies their records
+ * into out (device or host, >= cap records) when out != NULL */
+int smpm_sim_migrants(smpm_sim* s, int side, void* out, int64_t cap, int64_t* n);
+int smpm_sim_accept(smpm_sim* s, const void* recs /*device*/, int64_t n);
+/* Live particles of this rank: global pid, x, v (host or device pointers
+ * sized >= smpm_sim_num_stored). */
+int smpm_sim_get_local(smpm_sim* s, int64_t* n_live, int64_t* pid, double* x, double* v);
+int64_t smpm_sim_num_stored(const smpm_sim* s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -104,6 +104,13 @@ _SIGS = {
     "smpm_sim_vmax": (D, [P]),
     "smpm_sim_launch_count": (ctypes.c_int, [P, P]),
     "smpm_sim_grid_size": (ctypes.c_int, [P, P]),
+    "smpm_sim_set_slab": (ctypes.c_int, [P, I32, I32, I64, I64]),
+    "smpm_sim_exchange_pack": (ctypes.c_int, [P, ctypes.c_int, P, I64, P]),
+    "smpm_sim_exchange_unpack": (ctypes.c_int, [P, P, I64, ctypes.c_int]),
+    "smpm_sim_migrants": (ctypes.c_int, [P, ctypes.c_int, P, I64, P]),
+    "smpm_sim_accept": (ctypes.c_int, [P, P, I64]),
+    "smpm_sim_get_local": (ctypes.c_int, [P, P, P, P, P]),
+    "smpm_sim_num_stored": (I64, [P]),
 }
 
 

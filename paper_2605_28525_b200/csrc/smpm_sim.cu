@@ -89,6 +89,8 @@ struct DevStats {
   uint32_t vmax2_bits;      // max |v|^2 of the particles binned here
   uint32_t prev_blocks;     // snapshot of the other table's block count
   uint32_t n_binned;
+  uint32_t n_owned;         // blocks inside this rank's slab
+  uint32_t pad2;
   unsigned long long n_active;
   double dt;
   double mass_sum, mom_sum[3];
@@ -98,6 +100,7 @@ struct StepParams {
   double h, inv_h, dt_req, cfl, wave_speed;
   int record_conservation;
   int project;
+  int bx0, bx1;  // owned block-x range (n_active / n_owned count owned blocks only)
 };
 
 // ------------------------------------------------------------------ scan
@@ -146,13 +149,13 @@ __device__ inline uint32_t cta_excl_scan(uint32_t v, uint32_t* sh /*[8]*/, uint3
 // scans tile sums and finalises the step scalars.
 __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
                                                unsigned long long* err, StepParams sp) {
-  __shared__ uint32_t red[3][8];
+  __shared__ uint32_t red[4][8];
   __shared__ bool last;
   const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
   const int ntiles = (nb + TB - 1) / TB;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    uint32_t s_tot = 0, s_items = 0, s_pop = 0;
+    uint32_t s_tot = 0, s_items = 0, s_pop = 0, s_own = 0;
     for (int b = w; b < TB; b += 8) {
       uint32_t r = tile * TB + b;
       if (r >= nb) break;
@@ -171,19 +174,25 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
         S.block_items[r] = items;
         s_tot += tot;
         s_items += items;
-        s_pop += __popcll(S.nodemask[r]);
+        int bi, bj, bk;
+        unpack_key(S.hv.active_keys[r], bi, bj, bk);
+        if (bi >= sp.bx0 && bi < sp.bx1) {
+          s_pop += __popcll(S.nodemask[r]);
+          s_own += 1;
+        }
       }
     }
     if (lane == 0) {
       red[0][w] = s_tot;
       red[1][w] = s_items;
       red[2][w] = s_pop;
+      red[3][w] = s_own;
     }
     __syncthreads();
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < 4) {
       uint32_t a = 0;
       for (int i = 0; i < 8; ++i) a += red[threadIdx.x][i];
-      S.tile_sums[3 * tile + threadIdx.x] = a;
+      S.tile_sums[4 * tile + threadIdx.x] = a;
     }
     __syncthreads();
   }
@@ -193,16 +202,16 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
   __syncthreads();
   if (!last) return;
   __threadfence();
-  uint32_t carry[3] = {0, 0, 0};
+  uint32_t carry[4] = {0, 0, 0, 0};
   __shared__ uint32_t sh[8];
   unsigned long long n_active = 0;
   for (int base = 0; base < ntiles; base += 256) {
     int t = base + threadIdx.x;
-    for (int ch = 0; ch < 3; ++ch) {
-      uint32_t v = t < ntiles ? ((volatile uint32_t*)S.tile_sums)[3 * t + ch] : 0;
+    for (int ch = 0; ch < 4; ++ch) {
+      uint32_t v = t < ntiles ? ((volatile uint32_t*)S.tile_sums)[4 * t + ch] : 0;
       uint32_t tot;
       uint32_t ex = cta_excl_scan(v, sh, tot);
-      if (t < ntiles && ch < 2) S.tile_sums[3 * t + ch] = ex + carry[ch];
+      if (t < ntiles && ch < 2) S.tile_sums[4 * t + ch] = ex + carry[ch];
       if (ch == 2) n_active += tot;
       carry[ch] += tot;
     }
@@ -215,6 +224,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
     st->n_items = carry[1];
     st->n_binned = carry[0];
     st->n_active = n_active;
+    st->n_owned = carry[3];
     st->overflow = *S.hv.overflow | (*S.hv.counter > S.hv.cap_blocks ? 1u : 0u);
     // dt is validated on the host against the CFL bound (solver.py:1021-1030)
     st->dt = sp.dt_req;
@@ -241,8 +251,8 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S) {
     uint32_t tot = r < nb ? S.block_total[r] : 0, it = r < nb ? S.block_items[r] : 0, t1, t2;
     uint32_t e1 = cta_excl_scan(tot, sh, t1);
     uint32_t e2 = cta_excl_scan(it, sh, t2);
-    boff[threadIdx.x] = e1 + S.tile_sums[3 * tile];
-    ioff[threadIdx.x] = e2 + S.tile_sums[3 * tile + 1];
+    boff[threadIdx.x] = e1 + S.tile_sums[4 * tile];
+    ioff[threadIdx.x] = e2 + S.tile_sums[4 * tile + 1];
     __syncthreads();
     for (int b = w; b < TB; b += 8) {
       uint32_t rr = tile * TB + b;
@@ -339,6 +349,7 @@ __global__ void __launch_bounds__(256) k_grid(TableDev S, TableDev T, DevStats* 
 __global__ void k_prologue_keys(Particles P, int64_t n, TableDev B, uint32_t* __restrict__ bin, double inv_h,
                                 unsigned long long* err) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    if (bin[i] == BAD_KEY) continue;  // hole left by a particle that moved to another rank
     const double* xr = reinterpret_cast<const double*>(&P.rec[i * 8]);
     const uint32_t pid = __float_as_uint(reinterpret_cast<const float*>(&P.rec[i * 8])[W_PM]) & PID_MASK;
     int base[3];
@@ -389,6 +400,11 @@ struct FusedArgs {
   DevStats* stS;
   unsigned long long* err;
   int project;
+  // slab decomposition (multi-GPU): this rank owns base blocks bx in [bx0, bx1)
+  int bx0, bx1;
+  float4* mig[2];        // departing particle records (left, right)
+  uint32_t* mig_count;   // [2]
+  uint32_t mig_cap;
 };
 
 struct ItemInfo {
@@ -438,7 +454,7 @@ __device__ __forceinline__ float fx_scale(float b, float& inv) {
 // Global (slow-path) scatter of a particle that moved outside its block's
 // 8^3 arena: direct inserts and float atomics (rare: |dx| > 1 cell/step).
 __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float d[3], float m, const float v[3],
-                               const float C[9], const float M[6], uint32_t& binv) {
+                               const float C[9], const float M[6], uint32_t& binv, bool bin) {
   float w[3][3], g[3][3];
   for (int a = 0; a < 3; ++a) bspline(d[a], w[a], g[a]);
   const float h = float(A.h), ih = float(A.inv_h);
@@ -465,6 +481,10 @@ __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float 
         red_v4(&A.acc[2 * node + 1], f0, f1, f2, 0.f);
         atomicOr((unsigned long long*)&A.S.nodemask[r], 1ull << l);
       }
+  if (!bin) {
+    binv = BAD_KEY;
+    return;
+  }
   uint32_t r = hash_insert(A.S.hv, pack_key(nb[0] >> 2, nb[1] >> 2, nb[2] >> 2));
   if (r >= A.S.hv.cap_blocks) {
     binv = BAD_KEY;
@@ -598,6 +618,7 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
     float vn[3], Cn[9], M[6], m = 0.f, d1[3];
     int nb[3], ab[3];
     bool far = false, ok = valid;
+    int mig = -1;
     float bm = 0.f, bp = 0.f, bf = 0.f;
     uint32_t pidv = 0;
     if (valid) {
@@ -758,6 +779,21 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
         ab[1] = nb[1] - (4 * B1 - 1);
         ab[2] = nb[2] - (4 * B2 - 1);
         far = ab[0] < 0 || ab[0] > 5 || ab[1] < 0 || ab[1] > 5 || ab[2] < 0 || ab[2] > 5;
+        const int nbx = nb[0] >> 2;
+        mig = nbx < A.bx0 ? 0 : (nbx >= A.bx1 ? 1 : -1);
+        if (mig >= 0) {
+          // leaves this rank's slab: still scattered here (P2G belongs to the
+          // step that moved it), binned by the neighbour
+          const uint32_t slot = atomicAdd(&A.mig_count[mig], 1u);
+          if (slot < A.mig_cap) {
+            const float4* src4 = A.dst.rec + size_t(pos) * 8;
+            float4* o4 = A.mig[mig] + size_t(slot) * 8;
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) o4[c8] = src4[c8];
+          } else {
+            err_report(A.err, ERR_CAPACITY, pidv);
+          }
+        }
         // contribution bounds: |w| <= prod_a max_o w_a(o); |grad w_a| <= max|g_a| prod_{b!=a} max w_b / h;
         // |dx_a| <= h * max(d_a, 2 - d_a)
         float wmax[3], gmax[3], dxm[3];
@@ -793,7 +829,7 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
     if (ok && !far) {
       const int row = ab[0] * 8 + ab[1];
       atomicOr(&sm.occ[row >> 2], 1u << (((row & 3) << 3) | ab[2]));
-      atomicAdd(&sm.cnt[aaddr(ab[0], ab[1], ab[2])], 1u);
+      if (mig < 0) atomicAdd(&sm.cnt[aaddr(ab[0], ab[1], ab[2])], 1u);
     }
     {
       uint32_t um = warp_max(__float_as_uint(bm)), up = warp_max(__float_as_uint(bp)),
@@ -912,7 +948,7 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
         }
       }
     } else if (ok && far) {
-      scatter_global(A, nb, d1, m, vn, Cn, M, binv);
+      scatter_global(A, nb, d1, m, vn, Cn, M, binv, mig < 0);
     }
     if (tid < 27) {
       uint32_t rk = BAD_KEY;
@@ -936,7 +972,7 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
     // ---- bins of the next step: cell key only; positions are assigned by
     // k_bin.  Cell counts go out as fire-and-forget reductions.
     if (valid) {
-      if (ok && !far) {
+      if (ok && !far && mig < 0) {
         uint32_t rk = sm.rank[((ab[0] + 3) >> 2) * 9 + ((ab[1] + 3) >> 2) * 3 + ((ab[2] + 3) >> 2)];
         uint32_t lc = (((ab[0] + 3) & 3) << 4) | (((ab[1] + 3) & 3) << 2) | ((ab[2] + 3) & 3);
         binv = rk == BAD_KEY ? BAD_KEY : rk * 64 + lc;
@@ -986,7 +1022,7 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
 
 // ------------------------------------------------------- state transfer
 // Upload: reference layout f64 -> 128-byte records (x f64, rest f32).
-__global__ void k_upload(Particles P, int64_t off, int64_t n, const double* __restrict__ x,
+__global__ void k_upload(Particles P, int64_t off, int64_t pid_base, int64_t n, const double* __restrict__ x,
                          const double* __restrict__ v, const double* __restrict__ C, const double* __restrict__ F,
                          const double* __restrict__ m, const double* __restrict__ V0,
                          const int64_t* __restrict__ mat) {
@@ -1000,7 +1036,7 @@ __global__ void k_upload(Particles P, int64_t off, int64_t n, const double* __re
     w[W_M] = float(m[i]);
     w[W_V0] = float(V0[i]);
     for (int q = 0; q < 9; ++q) w[W_F + q] = float(F[9 * i + q] - ((q == 0 || q == 4 || q == 8) ? 1.0 : 0.0));
-    w[W_PM] = __uint_as_float((uint32_t(j) & PID_MASK) | (uint32_t(mat[i]) << 29));
+    w[W_PM] = __uint_as_float((uint32_t(pid_base + j) & PID_MASK) | (uint32_t(mat[i]) << 29));
     for (int a = 0; a < 3; ++a) w[W_V + a] = float(v[3 * i + a]);
     for (int q = 0; q < 9; ++q) w[W_C + q] = float(C[9 * i + q]);
     w[30] = w[31] = 0.f;
@@ -1054,6 +1090,115 @@ __global__ void k_download(Particles P, int64_t n, int64_t lo, int64_t hi, doubl
   }
 }
 
+// ------------------------------------------------------- slab exchange
+// Multi-GPU slab decomposition along x.  Block record: key, node
+// mask and the 64 node accumulators (m, p0, p1, p2 | f0, f1, f2, 0).
+struct BlockRec {
+  unsigned long long key, mask;
+  float4 v[128];
+};
+
+// mode 0: blocks with bx < x0 (partials for the left owner); 1: bx >= x1
+// (partials for the right owner); 2: bx == x0 (full sums of the left boundary
+// layer, needed as halo by the left neighbour).  One warp per block.
+__global__ void k_pack_blocks(TableDev S, const float4* __restrict__ acc, int mode, int x0, int x1, BlockRec* out,
+                              uint32_t* count, uint32_t cap) {
+  const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nb; r += nw) {
+    const uint64_t key = S.hv.active_keys[r];
+    int bi, bj, bk;
+    unpack_key(key, bi, bj, bk);
+    const bool sel = mode == 0 ? bi < x0 : (mode == 1 ? bi >= x1 : bi == x0);
+    if (!sel) continue;
+    uint32_t slot = 0;
+    if (lane == 0) slot = atomicAdd(count, 1u);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (slot >= cap) continue;
+    BlockRec& o = out[slot];
+    if (lane == 0) {
+      o.key = key;
+      o.mask = S.nodemask[r];
+    }
+    for (int q = lane; q < 128; q += 32) o.v[q] = acc[size_t(r) * 128 + q];
+  }
+}
+
+// Insert-if-absent, OR the node mask, then add (set = 0) or overwrite (set = 1)
+// the node accumulators.  Both neighbours of a shared layer end with the same
+// bits: the owner sums the partials once and sends the sum back.
+__global__ void k_unpack_blocks(TableDev S, float4* acc, const BlockRec* __restrict__ in, uint32_t n, int set,
+                                unsigned long long* err) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    uint32_t r = 0;
+    if (lane == 0) {
+      r = hash_insert(S.hv, in[i].key);
+      if (r < S.hv.cap_blocks) atomicOr((unsigned long long*)&S.nodemask[r], in[i].mask);
+    }
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= S.hv.cap_blocks) {
+      if (lane == 0) err_report(err, ERR_CAPACITY, 0);
+      continue;
+    }
+    for (int q = lane; q < 128; q += 32) {
+      const float4 v = in[i].v[q];
+      float4* d = &acc[size_t(r) * 128 + q];
+      if (set)
+        *d = v;
+      else
+        red_v4(d, v.x, v.y, v.z, v.w);
+    }
+  }
+}
+
+// Arriving particles: append their records at dst[off..] and bin them in S.
+// Their P2G was done by the sender, so only the bin (and cell count) is new.
+__global__ void k_accept(const float4* __restrict__ in, uint32_t n, Particles dst, uint32_t off, TableDev S,
+                         uint32_t* bin, double inv_h, unsigned long long* err) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float4* o = dst.rec + size_t(off + i) * 8;
+    for (int c = 0; c < 8; ++c) o[c] = in[size_t(i) * 8 + c];
+    const double* xr = reinterpret_cast<const double*>(o);
+    int b[3];
+    float d;
+    bool ok = true;
+    for (int a = 0; a < 3; ++a) ok = ok && axis_base(xr[a], inv_h, b[a], d);
+    uint32_t key = BAD_KEY;
+    if (ok) {
+      const uint32_t r = hash_insert(S.hv, pack_key(b[0] >> 2, b[1] >> 2, b[2] >> 2));
+      if (r < S.hv.cap_blocks) {
+        key = r * 64 + uint32_t(((b[0] & 3) << 4) | ((b[1] & 3) << 2) | (b[2] & 3));
+        atomicAdd(&S.cell_count[key], 1u);
+      } else {
+        err_report(err, ERR_CAPACITY, 0);
+      }
+    }
+    bin[off + i] = key;
+  }
+}
+
+// Live particles of this rank in storage order (holes left by departed
+// particles carry no bin): pid + reference-layout fields.
+__global__ void k_download_local(Particles P, const uint32_t* __restrict__ bin, uint32_t n_store, uint32_t* count,
+                                 int64_t* pid, double* x, double* v) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_store; i += gridDim.x * blockDim.x) {
+    if (bin[i] == BAD_KEY) continue;
+    const uint32_t o = atomicAdd(count, 1u);
+    const float4* r4 = P.rec + size_t(i) * 8;
+    const float4 c0 = r4[0], c1 = r4[1], c4 = r4[4], c5 = r4[5];
+    pid[o] = int64_t(__float_as_uint(c4.y) & PID_MASK);
+    x[3 * o] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
+    x[3 * o + 1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
+    x[3 * o + 2] = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
+    v[3 * o] = c4.z;
+    v[3 * o + 1] = c4.w;
+    v[3 * o + 2] = c5.x;
+  }
+}
+
 }  // namespace smpm
 
 
@@ -1101,6 +1246,13 @@ struct smpm_sim {
   cudaEvent_t ev[5];
   smpm_step_stats last{};
   double vmax = 0;        // max |v| of the current particles (CFL bound input)
+  // slab decomposition
+  int bx0 = INT32_MIN, bx1 = INT32_MAX;
+  int64_t pid_base = 0;
+  uint32_t n_store = 0;   // storage slots of the current buffer (incl. holes)
+  float4* mig[2] = {nullptr, nullptr};
+  uint32_t* mig_count = nullptr;
+  uint32_t mig_cap = 0;
   bool in_flight = false; // a step was launched and not yet synced
   uint32_t* hcount = nullptr;  // pinned: counter/overflow of the table just filled
   std::vector<smpm_material> host_mats;
@@ -1179,7 +1331,7 @@ int alloc_grid(smpm_sim* s) {
     DA(T.block_items, cb);
     DA(T.nbr8, size_t(cb) * 8);
     DA(T.items, s->cap_items);
-    DA(T.tile_sums, 3 * size_t(s->max_tiles));
+    DA(T.tile_sums, 4 * size_t(s->max_tiles));
     CK(cudaMemsetAsync(T.hv.keys, 0xFF, s->n_slots * 8, s->stream));
     CK(cudaMemsetAsync(T.hv.vals, 0xFF, s->n_slots * 4, s->stream));
     CK(cudaMemsetAsync(T.hv.counter, 0, 16, s->stream));
@@ -1212,6 +1364,12 @@ FusedArgs fused_args(smpm_sim* s, int B, int dstbuf, int project) {
   A.stS = s->dstats + (1 - B);
   A.err = s->derr;
   A.project = project;
+  A.bx0 = s->bx0;
+  A.bx1 = s->bx1;
+  A.mig[0] = s->mig[0];
+  A.mig[1] = s->mig[1];
+  A.mig_count = s->mig_count;
+  A.mig_cap = s->mig_cap;
   return A;
 }
 
@@ -1224,6 +1382,8 @@ StepParams step_params(smpm_sim* s, double dt) {
   sp.wave_speed = s->wave_speed;
   sp.record_conservation = s->record;
   sp.project = 1;
+  sp.bx0 = s->bx0;
+  sp.bx1 = s->bx1;
   return sp;
 }
 
@@ -1232,13 +1392,14 @@ int scan_and_bin(smpm_sim* s, int Sx, double dt) {
   int grid = std::max(1, std::min<int>(s->max_tiles, 148 * 8));
   k_scan1<<<grid, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp);
   k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx]);
-  k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n, s->tab[Sx], s->perm);
+  k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm);
   CK(cudaGetLastError());
   return SMPM_OK;
 }
 
 int launch_fused(smpm_sim* s, bool gather, int project) {
   int dstbuf = 1 - s->cur;
+  if (s->mig_count) CK(cudaMemsetAsync(s->mig_count, 0, 8, s->stream));
   FusedArgs A = fused_args(s, s->S, dstbuf, project);
   size_t smem = smem_bytes();
   if (gather)
@@ -1324,7 +1485,8 @@ int run_prologue(smpm_sim* s, int project) {
     CK(cudaMemsetAsync(s->dstats, 0, 2 * sizeof(DevStats), s->stream));
     CK(cudaMemsetAsync(s->derr, 0xFF, 8, s->stream));
     s->S = 0;
-    k_prologue_keys<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n, s->tab[0], s->bin, s->inv_h, s->derr);
+    k_prologue_keys<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n_store, s->tab[0], s->bin, s->inv_h,
+                                                    s->derr);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(s->herr, s->derr, 8, cudaMemcpyDeviceToHost, s->stream));
     uint32_t need = 0;
@@ -1502,7 +1664,9 @@ int smpm_sim_set_particles(smpm_sim* s, int64_t n, const double* x, const double
     if (rc) return rc;
   }
   s->n = n;
+  s->n_store = uint32_t(n);
   s->cur = 0;
+  CK(cudaMemsetAsync(s->bin, 0, size_t(n) * 4, s->stream));  // live (non-BAD) marker
   // staged chunks (inputs may be host or device memory)
   const int64_t CH = 1 << 22;
   double *sx, *sv, *sC, *sF, *sm, *sV;
@@ -1523,7 +1687,7 @@ int smpm_sim_set_particles(smpm_sim* s, int64_t n, const double* x, const double
     CK(cudaMemcpyAsync(sm, m + off, c * 8, cudaMemcpyDefault, s->stream));
     CK(cudaMemcpyAsync(sV, V0 + off, c * 8, cudaMemcpyDefault, s->stream));
     CK(cudaMemcpyAsync(smat, mat_id + off, c * 8, cudaMemcpyDefault, s->stream));
-    k_upload<<<148 * 4, 256, 0, s->stream>>>(s->state[0], off, c, sx, sv, sC, sF, sm, sV, smat);
+    k_upload<<<148 * 4, 256, 0, s->stream>>>(s->state[0], off, s->pid_base, c, sx, sv, sC, sF, sm, sV, smat);
     CK(cudaGetLastError());
   }
   CK(cudaFreeAsync(sx, s->stream));
@@ -1638,7 +1802,8 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
     smpm_step_stats r{};
     r.dt = st.dt;
     r.n_active = int64_t(st.n_active);
-    r.n_blocks = int64_t(st.n_blocks);
+    r.n_blocks = int64_t(st.n_owned);
+    s->n_store = st.n_binned;  // positions written by the fused kernel (holes included)
     s->vmax = std::sqrt(double(__uint_as_float_host(nx.vmax2_bits)));
     r.vmax = s->vmax;
     r.mass_sum = st.mass_sum;
@@ -1728,6 +1893,122 @@ int smpm_sim_grid_size(smpm_sim* s, int64_t* n_blocks) {
 }
 
 int64_t smpm_sim_num_particles(const smpm_sim* s) { return s ? s->n : 0; }
+
+int smpm_sim_set_slab(smpm_sim* s, int32_t bx0, int32_t bx1, int64_t pid_base, int64_t migrant_capacity) {
+  if (!s || bx1 <= bx0) return set_err(SMPM_ERR_ARG, "invalid slab");
+  CK(cudaSetDevice(s->device));
+  s->bx0 = bx0;
+  s->bx1 = bx1;
+  s->pid_base = pid_base;
+  if (migrant_capacity > 0 && !s->mig_count) {
+    int rc = dalloc(s, &s->mig[0], size_t(migrant_capacity) * 8);
+    if (rc) return rc;
+    rc = dalloc(s, &s->mig[1], size_t(migrant_capacity) * 8);
+    if (rc) return rc;
+    rc = dalloc(s, &s->mig_count, 2);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(s->mig_count, 0, 8, s->stream));
+    s->mig_cap = uint32_t(migrant_capacity);
+  }
+  return SMPM_OK;
+}
+
+int smpm_sim_exchange_pack(smpm_sim* s, int mode, void* out, int64_t cap_blocks, int64_t* n_out) {
+  if (!s || !n_out) return set_err(SMPM_ERR_ARG, "null argument");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  uint32_t* cnt = s->mig_count ? s->mig_count : nullptr;
+  uint32_t* dcnt = nullptr;
+  CK(cudaMallocAsync(&dcnt, 4, s->stream));
+  CK(cudaMemsetAsync(dcnt, 0, 4, s->stream));
+  k_pack_blocks<<<148 * 8, 256, 0, s->stream>>>(s->tab[s->S], s->acc, mode, s->bx0, s->bx1,
+                                                reinterpret_cast<BlockRec*>(out), dcnt, uint32_t(cap_blocks));
+  CK(cudaGetLastError());
+  uint32_t h = 0;
+  CK(cudaMemcpyAsync(&h, dcnt, 4, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaFreeAsync(dcnt, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  (void)cnt;
+  *n_out = int64_t(h);
+  if (int64_t(h) > cap_blocks) return set_err(SMPM_ERR_CAPACITY, "exchange buffer too small");
+  return SMPM_OK;
+}
+
+int smpm_sim_exchange_unpack(smpm_sim* s, const void* in, int64_t n, int set) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  if (n <= 0) return SMPM_OK;
+  CK(cudaSetDevice(s->device));
+  k_unpack_blocks<<<148 * 4, 256, 0, s->stream>>>(s->tab[s->S], s->acc, reinterpret_cast<const BlockRec*>(in),
+                                                  uint32_t(n), set, s->derr);
+  CK(cudaGetLastError());
+  return SMPM_OK;
+}
+
+int smpm_sim_migrants(smpm_sim* s, int side, void* out, int64_t cap, int64_t* n) {
+  if (!s || !n || side < 0 || side > 1) return set_err(SMPM_ERR_ARG, "invalid argument");
+  CK(cudaSetDevice(s->device));
+  *n = 0;
+  if (!s->mig_count) return SMPM_OK;
+  uint32_t c[2];
+  CK(cudaMemcpyAsync(c, s->mig_count, 8, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (c[side] > s->mig_cap) return set_err(SMPM_ERR_CAPACITY, "migrant buffer overflow");
+  *n = int64_t(c[side]);
+  if (out && c[side]) {
+    if (int64_t(c[side]) > cap) return set_err(SMPM_ERR_ARG, "output buffer too small");
+    CK(cudaMemcpyAsync(out, s->mig[side], size_t(c[side]) * 128, cudaMemcpyDefault, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  }
+  return SMPM_OK;
+}
+
+int smpm_sim_accept(smpm_sim* s, const void* recs, int64_t n) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  if (n <= 0) return SMPM_OK;
+  if (int64_t(s->n_store) + n > s->cap_p) return set_err(SMPM_ERR_CAPACITY, "particle capacity exceeded");
+  CK(cudaSetDevice(s->device));
+  k_accept<<<std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, s->stream>>>(
+      reinterpret_cast<const float4*>(recs), uint32_t(n), s->state[s->cur], s->n_store, s->tab[s->S], s->bin,
+      s->inv_h, s->derr);
+  CK(cudaGetLastError());
+  s->n_store += uint32_t(n);
+  return SMPM_OK;
+}
+
+int smpm_sim_get_local(smpm_sim* s, int64_t* n_live, int64_t* pid, double* x, double* v) {
+  if (!s || !n_live) return set_err(SMPM_ERR_ARG, "null argument");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  const size_t ns = std::max<uint32_t>(s->n_store, 1);
+  int64_t* dp;
+  double *dx, *dv;
+  uint32_t* dc;
+  CK(cudaMallocAsync(&dp, ns * 8, s->stream));
+  CK(cudaMallocAsync(&dx, ns * 24, s->stream));
+  CK(cudaMallocAsync(&dv, ns * 24, s->stream));
+  CK(cudaMallocAsync(&dc, 4, s->stream));
+  CK(cudaMemsetAsync(dc, 0, 4, s->stream));
+  k_download_local<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], s->bin, s->n_store, dc, dp, dx, dv);
+  CK(cudaGetLastError());
+  uint32_t c = 0;
+  CK(cudaMemcpyAsync(&c, dc, 4, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (pid) CK(cudaMemcpyAsync(pid, dp, size_t(c) * 8, cudaMemcpyDefault, s->stream));
+  if (x) CK(cudaMemcpyAsync(x, dx, size_t(c) * 24, cudaMemcpyDefault, s->stream));
+  if (v) CK(cudaMemcpyAsync(v, dv, size_t(c) * 24, cudaMemcpyDefault, s->stream));
+  for (void* p : {(void*)dp, (void*)dx, (void*)dv, (void*)dc}) CK(cudaFreeAsync(p, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  *n_live = int64_t(c);
+  return SMPM_OK;
+}
+
+int64_t smpm_sim_num_stored(const smpm_sim* s) { return s ? int64_t(s->n_store) : 0; }
 
 double smpm_sim_vmax(smpm_sim* s) {
   if (!s) return 0;

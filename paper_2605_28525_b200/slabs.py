@@ -1,0 +1,280 @@
+"""Multi-GPU slab decomposition of the sparse-MPM step.
+
+The reference is single-process (its paper lists multi-GPU as future work,
+/root/reference/PAPER.md:335-337); this module is the B200 build's
+extension.  One process per GPU; the domain is cut into slabs along the
+runout axis x at block boundaries.  A rank owns the particles whose base
+block has block-x in [bx0, bx1) and the grid blocks in that range.
+
+Per step, after the fused kernel (libsmpm.so, include/smpm.h):
+  1. partial node sums of blocks outside the slab go to their owner, which
+     adds them (insert-if-absent);
+  2. the owner sends the full sums of its first block layer (bx == bx0) back
+     to the left neighbour, whose particles' stencils reach it -- both sides
+     of an interface then hold identical bits;
+  3. particles whose new base block left the slab travel as 128-byte records
+     and are binned by the receiver (their P2G was already done).
+n_active / n_blocks are sums over owned blocks; the CFL bound uses the global
+max |v|.  Transport is torch.distributed point-to-point (NCCL over NVLink on
+a GPU box; gloo with host staging in the CPU tests).
+"""
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _lib
+from .solver import PHASES, Simulation, StepStats
+
+BLOCK_REC_BYTES = 2064  # key, node mask, 64 nodes x 8 floats
+PARTICLE_REC_BYTES = 128
+INT32_MIN = -(1 << 31)
+INT32_MAX = (1 << 31) - 1
+
+
+def base_block_x(x, h):
+    """Block-x of each particle's base node: floor(floor(x/h - 0.5) / 4),
+    computed like the device (fp64, same inv_h)."""
+    inv_h = 1.0 / float(h)
+    base = np.floor(np.asarray(x, dtype=np.float64)[:, 0] * inv_h - 0.5).astype(np.int64)
+    return base >> 2
+
+
+def slab_bounds(bx, world):
+    """Block-aligned cut points giving each rank ~N/world particles.
+    Returns [(bx0, bx1)] with bx0 of rank 0 = -inf and bx1 of the last = +inf
+    (as int32 sentinels)."""
+    bx = np.asarray(bx, dtype=np.int64)
+    if world == 1:
+        return [(INT32_MIN, INT32_MAX)]
+    order = np.sort(bx)
+    cuts = []
+    for r in range(1, world):
+        c = int(order[min(len(order) - 1, (r * len(order)) // world)])
+        cuts.append(c)
+    # strictly increasing, every slab at least 2 blocks wide so contributions
+    # to a block come from at most two ranks
+    for i in range(1, len(cuts)):
+        cuts[i] = max(cuts[i], cuts[i - 1] + 2)
+    lo = [INT32_MIN] + cuts
+    hi = cuts + [INT32_MAX]
+    return list(zip(lo, hi))
+
+
+def partition(particles, h, world):
+    """Split a ParticleSet into per-rank index arrays (by base block) and the
+    slab bounds.  Every particle lands in exactly one slab."""
+    bx = base_block_x(particles.x, h)
+    bounds = slab_bounds(bx, world)
+    parts = [np.nonzero((bx >= lo) & (bx < hi))[0] for lo, hi in bounds]
+    return bounds, parts
+
+
+def subset(ps, idx):
+    from .solver import ParticleSet
+
+    return ParticleSet(**{k: np.ascontiguousarray(getattr(ps, k)[idx]) for k in
+                          ("x", "v", "C", "F", "m", "V0", "mat_id", "sigma", "jac")})
+
+
+class _Transport:
+    """Neighbour point-to-point exchange of byte buffers (device tensors)."""
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+    def _dev(self, t):
+        return t if self.nccl else t.cpu()
+
+    def exchange(self, to_left, to_right):
+        """to_left / to_right: uint8 CUDA tensors (or None).  Returns the
+        buffers received from the left and the right neighbour (CUDA)."""
+        import torch
+
+        dist = self.dist
+        left = self.rank - 1 if self.rank > 0 else None
+        right = self.rank + 1 if self.rank + 1 < self.world else None
+        dev = self.device
+        # sizes first
+        n_to = {"l": 0 if to_left is None else to_left.numel(), "r": 0 if to_right is None else to_right.numel()}
+        sz_dev = dev if self.nccl else torch.device("cpu")
+        send_l = torch.tensor([n_to["l"]], dtype=torch.int64, device=sz_dev)
+        send_r = torch.tensor([n_to["r"]], dtype=torch.int64, device=sz_dev)
+        recv_l = torch.zeros(1, dtype=torch.int64, device=sz_dev)
+        recv_r = torch.zeros(1, dtype=torch.int64, device=sz_dev)
+        ops = []
+        if left is not None:
+            ops += [dist.P2POp(dist.isend, send_l, left, self.group), dist.P2POp(dist.irecv, recv_l, left, self.group)]
+        if right is not None:
+            ops += [dist.P2POp(dist.isend, send_r, right, self.group), dist.P2POp(dist.irecv, recv_r, right, self.group)]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        nl, nr = int(recv_l.item()), int(recv_r.item())
+        bufs = {}
+        ops = []
+        if left is not None:
+            if n_to["l"]:
+                ops.append(dist.P2POp(dist.isend, self._dev(to_left), left, self.group))
+            if nl:
+                bufs["l"] = torch.empty(nl, dtype=torch.uint8, device=sz_dev)
+                ops.append(dist.P2POp(dist.irecv, bufs["l"], left, self.group))
+        if right is not None:
+            if n_to["r"]:
+                ops.append(dist.P2POp(dist.isend, self._dev(to_right), right, self.group))
+            if nr:
+                bufs["r"] = torch.empty(nr, dtype=torch.uint8, device=sz_dev)
+                ops.append(dist.P2POp(dist.irecv, bufs["r"], right, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        out_l = bufs.get("l")
+        out_r = bufs.get("r")
+        out_l = None if out_l is None else out_l.to(dev)
+        out_r = None if out_r is None else out_r.to(dev)
+        if dev.type == "cuda":
+            torch.cuda.synchronize()  # the library consumes these on its own stream
+        return out_l, out_r
+
+    def allreduce(self, arr, op="sum"):
+        import torch
+
+        dist = self.dist
+        dev = self.device if self.nccl else torch.device("cpu")
+        t = torch.tensor(np.asarray(arr, dtype=np.float64), device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM, group=self.group)
+        return t.cpu().numpy()
+
+
+class DistributedSimulation:
+    """Slab-decomposed Simulation: call on every rank with that rank's
+    particles (``partition``/``subset``), its slab bounds and the global id of
+    its first particle."""
+
+    def __init__(self, particles, config, materials, boundaries, bounds, pid_base, group=None,
+                 migrant_capacity=None, block_capacity=None, record_conservation=False):
+        torch = _lib.torch_cuda()
+        self.config = config
+        self.tr = _Transport(group)
+        self.bounds = bounds
+        n = particles.n
+        # capacity: local particles + arrivals (slabs rebalance slowly)
+        cap_mig = int(migrant_capacity or max(4096, n // 8))
+        self._cap_mig = cap_mig
+        self.sim = Simulation(particles, config, materials, boundaries, record_conservation=record_conservation,
+                              block_capacity=block_capacity, particle_capacity=n + 4 * cap_mig,
+                              slab=(int(bounds[0]), int(bounds[1]), int(pid_base), cap_mig))
+        self._h = self.sim._h
+        self.lib = _lib.load()
+        self.t = 0.0
+        self.step_count = 0
+        self._torch = torch
+        # step 0: P2G of the initial state on every rank, then the halo exchange
+        nb = ctypes.c_int64(0)
+        _lib.check(self.lib.smpm_sim_grid_size(self._h, ctypes.byref(nb)), "prologue")
+        self._exchange()
+
+    # -- exchange -------------------------------------------------------------
+    def _pack(self, mode):
+        torch = self._torch
+        nb = ctypes.c_int64(0)
+        _lib.check(self.lib.smpm_sim_grid_size(self._h, ctypes.byref(nb)), "grid size")
+        cap = max(int(nb.value), 1)
+        buf = torch.empty(cap * BLOCK_REC_BYTES, dtype=torch.uint8, device="cuda")
+        n = ctypes.c_int64(0)
+        _lib.check(self.lib.smpm_sim_exchange_pack(self._h, mode, _lib.ptr(buf), cap, ctypes.byref(n)), "pack")
+        return buf[: n.value * BLOCK_REC_BYTES] if n.value else None
+
+    def _unpack(self, buf, set_):
+        if buf is None or buf.numel() == 0:
+            return
+        _lib.check(self.lib.smpm_sim_exchange_unpack(self._h, _lib.ptr(buf), buf.numel() // BLOCK_REC_BYTES,
+                                                     int(set_)), "unpack")
+
+    def _migrants(self, side):
+        torch = self._torch
+        n = ctypes.c_int64(0)
+        _lib.check(self.lib.smpm_sim_migrants(self._h, side, None, 0, ctypes.byref(n)), "migrants")
+        if n.value == 0:
+            return None
+        out = torch.empty(n.value * PARTICLE_REC_BYTES, dtype=torch.uint8, device="cuda")
+        _lib.check(self.lib.smpm_sim_migrants(self._h, side, _lib.ptr(out), n.value, ctypes.byref(n)), "migrants")
+        return out
+
+    def _exchange(self):
+        self._torch.cuda.synchronize()
+        # 1. partial sums of blocks outside the slab -> owners
+        from_l, from_r = self.tr.exchange(self._pack(0), self._pack(1))
+        self._unpack(from_l, False)
+        self._unpack(from_r, False)
+        self._torch.cuda.synchronize()
+        self.sim.stream.synchronize()
+        # 2. owner's first layer (full sums) -> left neighbour
+        _, from_r = self.tr.exchange(self._pack(2), None)
+        self._unpack(from_r, True)
+        self.sim.stream.synchronize()
+        # 3. departing particles
+        from_l, from_r = self.tr.exchange(self._migrants(0), self._migrants(1))
+        for buf in (from_l, from_r):
+            if buf is not None:
+                _lib.check(self.lib.smpm_sim_accept(self._h, _lib.ptr(buf), buf.numel() // PARTICLE_REC_BYTES),
+                           "accept")
+        self.sim.stream.synchronize()
+
+    # -- API ------------------------------------------------------------------
+    def dt_bound(self):
+        vmax = float(self.lib.smpm_sim_vmax(self._h))
+        vmax = float(self.tr.allreduce([vmax], "max")[0])
+        return self.config.cfl * self.config.h / (self.sim._wave_speed + vmax)
+
+    def step(self, dt=None):
+        cfg = self.config
+        if dt is None:
+            dt = cfg.dt if cfg.dt is not None else self.dt_bound()
+        st = self.sim.step(float(dt))
+        red = self.tr.allreduce([st.n_active, st.n_allocated, st.mass_sum or 0.0,
+                                 *(st.mom_sum if st.mom_sum is not None else (0.0, 0.0, 0.0))])
+        self._exchange()
+        self.t += st.dt
+        self.step_count += 1
+        return StepStats(step=self.step_count, t=self.t, dt=st.dt, n_active=int(red[0]), n_allocated=int(red[1]),
+                         times=dict(st.times), mass_sum=float(red[2]) if st.mass_sum is not None else None,
+                         mom_sum=red[3:6] if st.mom_sum is not None else None)
+
+    def local_particles(self):
+        """(pid, x, v) of the particles this rank owns."""
+        ns = int(self.lib.smpm_sim_num_stored(self._h))
+        pid = np.empty(max(ns, 1), dtype=np.int64)
+        x = np.empty((max(ns, 1), 3))
+        v = np.empty((max(ns, 1), 3))
+        n = ctypes.c_int64(0)
+        _lib.check(self.lib.smpm_sim_get_local(self._h, ctypes.byref(n), pid.ctypes.data, x.ctypes.data,
+                                               v.ctypes.data), "get local")
+        k = int(n.value)
+        return pid[:k], x[:k], v[:k]
+
+    def gather_particles(self):
+        """All ranks' (x, v) ordered by global particle id (on every rank)."""
+        import torch.distributed as dist
+
+        pid, x, v = self.local_particles()
+        objs = [None] * self.tr.world
+        dist.all_gather_object(objs, (pid, x, v), group=self.tr.group)
+        P = np.concatenate([o[0] for o in objs])
+        X = np.concatenate([o[1] for o in objs])
+        V = np.concatenate([o[2] for o in objs])
+        order = np.argsort(P)
+        return P[order], X[order], V[order]
+
+
+__all__ = ["DistributedSimulation", "partition", "slab_bounds", "subset", "base_block_x", "PHASES"]
+_ = math

@@ -449,7 +449,7 @@ class Simulation:
     """
 
     def __init__(self, particles, config, materials, boundaries=(), record_conservation=False,
-                 block_capacity=None, device=0, stream=None):
+                 block_capacity=None, device=0, stream=None, particle_capacity=None, slab=None):
         import ctypes
 
         self._particles = particles
@@ -493,7 +493,7 @@ class Simulation:
             cfg.hf_x0, cfg.hf_y0, cfg.hf_cell = float(hf.x0), float(hf.y0), float(hf.cell)
         else:
             cfg.hf_cell = 1.0
-        cfg.particle_capacity = particles.n
+        cfg.particle_capacity = max(particles.n, int(particle_capacity or 0))
         cfg.block_capacity = int(block_capacity or 0)
         cfg.deterministic = int(bool(config.deterministic))
         cfg.record_conservation = int(bool(record_conservation))
@@ -503,6 +503,8 @@ class Simulation:
         h = ctypes.c_void_p()
         _lib.check(lib.smpm_sim_create(ctypes.byref(cfg), ctypes.byref(h)), "sim create")
         self._h = h
+        if slab is not None:  # (bx0, bx1, pid_base, migrant_capacity): see slabs.py
+            _lib.check(lib.smpm_sim_set_slab(h, *[int(v) for v in slab]), "set slab")
         self._upload(particles)
         self.t = 0.0
         self.step_count = 0

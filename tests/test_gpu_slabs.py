@@ -1,0 +1,94 @@
+"""Slab decomposition on 2 ranks vs 1 GPU (SURVEY section 8e gate).
+
+Two processes share the box's single B200 and talk over gloo (host-staged
+buffers); on an 8-GPU box the same code runs one rank per GPU over NCCL.
+Particles are given enough x velocity to cross the slab cut, so halo sums,
+the boundary-layer send-back and particle migration are all exercised."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+STEPS = 8
+
+
+def _scene():
+    from tests.test_gpu_sim import column_scene
+
+    ps, cfg, mats, bc = column_scene(bcs="mixed", vx=3.0)
+    return ps, cfg, mats, bc
+
+
+def _dt_sequence(ps, cfg, mats, bc):
+    from paper_2605_28525_b200.solver import Simulation
+
+    sim = Simulation(ps.copy(), cfg, mats, bc)
+    out = []
+    for _ in range(STEPS):
+        dt = 0.8 * sim.dt_bound()
+        st = sim.step(dt)
+        out.append((dt, st.n_active, st.n_allocated))
+    return out, sim.particles.x.copy(), sim.particles.v.copy()
+
+
+def _worker(rank, world, port, dts, outdir):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_28525_b200 import slabs
+
+    ps, cfg, mats, bc = _scene()
+    bounds, parts = slabs.partition(ps, cfg.h, world)
+    local = slabs.subset(ps, parts[rank])
+    pid_base = int(sum(len(p) for p in parts[:rank]))
+    # partition keeps global order inside a slab only if particles are sorted by
+    # slab; map local -> global ids explicitly through the pid base trick
+    assert np.all(np.diff(parts[rank]) > 0)
+    ds = slabs.DistributedSimulation(local, cfg, mats, bc, bounds[rank], pid_base)
+    stats = []
+    for dt, _, _ in dts:
+        st = ds.step(dt)
+        stats.append((st.n_active, st.n_allocated))
+    pid, x, v = ds.gather_particles()
+    # pid -> original index
+    order = np.concatenate(parts)
+    if rank == 0:
+        np.savez(os.path.join(outdir, "dist.npz"), stats=np.array(stats), pid=order[pid], x=x, v=v,
+                 counts=np.array([len(p) for p in parts]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_slabs_match_single_gpu(tmp_path):
+    import torch.multiprocessing as mp
+
+    ps, cfg, mats, bc = _scene()
+    dts, x1, v1 = _dt_sequence(ps, cfg, mats, bc)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_worker, args=(2, port, dts, str(tmp_path)), nprocs=2, join=True)
+    d = np.load(tmp_path / "dist.npz")
+    assert d["counts"].min() > 0.3 * ps.n  # both slabs populated
+    stats = d["stats"]
+    # step 1 is computed from identical initial positions: exact
+    assert stats[0][0] == dts[0][1]
+    assert stats[0][1] == dts[0][2]
+    for s in range(STEPS):
+        assert abs(int(stats[s][0]) - dts[s][1]) <= 2e-3 * dts[s][1], s
+        assert abs(int(stats[s][1]) - dts[s][2]) <= 2e-3 * dts[s][2], s
+    assert len(d["pid"]) == ps.n and np.array_equal(np.sort(d["pid"]), np.arange(ps.n))
+    x = np.empty_like(d["x"])
+    v = np.empty_like(d["v"])
+    x[d["pid"]] = d["x"]
+    v[d["pid"]] = d["v"]
+    assert np.abs(x - x1).max() < 1e-6 * np.abs(x1).max()
+    assert np.abs(v - v1).max() < 1e-4 * np.abs(v1).max()
