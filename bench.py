@@ -151,103 +151,136 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def _phase_means(hist):
+    return {k: float(np.mean(v)) for k, v in hist.items()}
+
+
 def ours(args):
     import torch
 
-    from paper_2605_28525_b200 import _lib
+    from paper_2605_28525_b200 import _lib, scenes
     from paper_2605_28525_b200.solver import Simulation
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
-    sc = make_scene(args.config, args.scale)
-    n = sc.particles.n
+        dist.init_process_group(os.environ.get("SMPM_DIST_BACKEND", "nccl"))
+        if args.config != "C4":
+            raise SystemExit("multi-GPU bench runs the C4 landslide (C5 = C4 on N GPUs)")
+        slab = scenes.landslide_slabs(world, fraction=args.scale)[rank]
+        sc = scenes.landslide(fraction=args.scale, columns=(slab[2], slab[3]))
+        per_col = sc.particles.n // max(1, slab[3] - slab[2])
+    else:
+        sc = make_scene(args.config, args.scale)
+    n_local = sc.particles.n
+
+    def make_sim(ps):
+        if world == 1:
+            return Simulation(ps, sc.config, sc.materials, sc.boundaries)
+        from paper_2605_28525_b200.slabs import DistributedSimulation
+
+        return DistributedSimulation(ps, sc.config, sc.materials, sc.boundaries, (slab[0], slab[1]),
+                                     pid_base=slab[2] * per_col)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda" if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda" if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    n = int(sum_over_ranks(n_local))
     # ---- value: device-resident state, K steps timed on the sim's stream
-    sim = Simulation(sc.particles, sc.config, sc.materials, sc.boundaries)
-    stream = sim.stream
+    sim = make_sim(sc.particles)
+    inner = sim if world == 1 else sim.sim
+    stream = inner.stream
     for _ in range(args.warmup):
         sim.step()
-    dts = []
-    fused_ms, grid_ms, map_ms, nalloc = [], [], [], []
+    hist = {"map": [], "grid": [], "fused": []}
+    nalloc = []
     torch.cuda.synchronize()
     if world > 1:
-        torch.distributed.barrier()
+        dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local % max(1, torch.cuda.device_count())) as clk:
         start.record(stream)
         for _ in range(args.steps):
             st = sim.step()
-            dts.append(st.dt)
-            fused_ms.append(st.times["g2p"] * 1e3)
-            grid_ms.append(st.times["grid_update"] * 1e3)
-            map_ms.append(st.times["map_build"] * 1e3)
+            hist["fused"].append(st.times["g2p"] * 1e3)
+            hist["grid"].append(st.times["grid_update"] * 1e3)
+            hist["map"].append(st.times["map_build"] * 1e3)
             nalloc.append(st.n_allocated)
         end.record(stream)
         torch.cuda.synchronize()
-    ms = start.elapsed_time(end)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(start.elapsed_time(end))
     value = n * args.steps / (ms * 1e-3)
-    # ---- roofline of the dominant kernel (fused g2p->stress->p2g)
+    # ---- roofline of the dominant kernel (fused g2p->stress->p2g), this rank
     peak, peak_kind = measured_peaks()
-    n_alloc = float(np.mean(nalloc))
-    fused_bytes = 204.0 * n + 40.0 * n_alloc  # SURVEY 8d per-unit figures
-    f_ms = float(np.mean(fused_ms))
-    achieved = fused_bytes / (f_ms * 1e-3) / 1e9
-    step_bytes = 204.0 * n + 80.0 * n_alloc
+    ph = _phase_means(hist)
+    n_alloc_local = float(np.mean(nalloc)) if world == 1 else float(np.mean(nalloc)) / world
+    fused_bytes = 204.0 * n_local + 40.0 * n_alloc_local  # SURVEY 8d per-unit figures
+    achieved = fused_bytes / (ph["fused"] * 1e-3) / 1e9
+    step_bytes = 204.0 * n + 80.0 * float(np.mean(nalloc))
     traffic = None
-    tf = ROOT / "profiles" / "r01_fused_traffic.json"
+    tf = ROOT / "profiles" / "fused_traffic.json"
     if tf.exists():
         try:
             traffic = json.loads(tf.read_text()).get(args.config)
         except Exception:  # noqa: BLE001
             traffic = None
-    del sim
+    del sim, inner
     torch.cuda.empty_cache()
     # ---- e2e: public API from host buffers (upload + K steps + download x,v)
     host = sc.particles
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
-    sim2 = Simulation(host, sc.config, sc.materials, sc.boundaries)
-    stats_bytes = 0
+    sim2 = make_sim(host)
     for _ in range(args.steps):
         sim2.step()
-        stats_bytes += 2 * 128 + 24  # DevStats x2 + error word + counters (pinned copies)
-    out_x = np.empty_like(host.x)
-    out_v = np.empty_like(host.v)
-    from paper_2605_28525_b200 import _lib as L
-
-    L.check(L.load().smpm_sim_get_particles(sim2._h, out_x.ctypes.data, out_v.ctypes.data, None, None, None, None))
-    t1 = time.perf_counter()
+    if world == 1:
+        out_x = np.empty_like(host.x)
+        out_v = np.empty_like(host.v)
+        _lib.check(_lib.load().smpm_sim_get_particles(sim2._h, out_x.ctypes.data, out_v.ctypes.data, None, None,
+                                                      None, None))
+    else:
+        sim2.local_particles()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    stats_bytes = args.steps * (2 * 128 + 24)
     h2d = n * (24 + 24 + 72 + 72 + 8 + 8 + 8)
     d2h = n * 48
-    e2e_value = n * args.steps / (t1 - t0)
+    e2e_value = n * args.steps / e2e_s
     del sim2
     line = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[args.config], "config": args.config, "n_particles": n,
-                   "h": sc.config.h, "ppc": 2, "mean_allocated_nodes": n_alloc,
+        "config": {"workload": CONFIG_NAMES[args.config], "config": args.config if world == 1 else "C5",
+                   "n_particles": n, "h": sc.config.h, "ppc": 2, "mean_allocated_nodes": float(np.mean(nalloc)),
                    "l2": "inputs larger than L2 (state %.1f GB)" % (n * 242 / 1e9),
                    "dt": "CFL bound (cfl=0.4)", "parallelism": f"slab{world}" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_g2p2g (G2P+F+return map+next P2G)",
-                     "peak_kind": peak_kind, "kernel_ms": f_ms,
-                     "step_frac": step_bytes / (ms / args.steps * 1e-3) / 1e9 / peak},
-        "phases_ms": {"map_build(scan+bin)": float(np.mean(map_ms)), "grid_update": float(np.mean(grid_ms)),
-                      "fused": f_ms},
+                     "peak_kind": peak_kind, "kernel_ms": ph["fused"],
+                     "step_frac": step_bytes / world / (ms / args.steps * 1e-3) / 1e9 / peak},
+        "phases_ms": {"map_build(scan+bin)": ph["map"], "grid_update": ph["grid"], "fused": ph["fused"]},
         "e2e": {"value": e2e_value, "unit": METRIC,
                 "h2d_bytes_per_step": int(h2d / args.steps) + 8,
-                "d2h_bytes_per_step": int(d2h / args.steps + stats_bytes / args.steps)},
+                "d2h_bytes_per_step": int((d2h + stats_bytes) / args.steps)},
         "gpu_launches": 5 * args.steps,
         "clocks": clk.summary(),
     }
@@ -257,7 +290,8 @@ def ours(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        torch.distributed.destroy_process_group()
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def main():

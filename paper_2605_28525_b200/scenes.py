@@ -120,14 +120,15 @@ def landslide_terrain(cell=5.0):
 
 
 def landslide(h=0.5, ppc=2, release=((100.0, 350.0), (-62.5, 62.5)), depth=(0.5, 50.0), mu=0.35, x_stride=1,
-              fraction=1.0):
+              fraction=1.0, columns=None):
     """C4: terrain-conforming release zone over the analytic DEM.
 
     Particles sit on a lattice of spacing h/ppc in x and y; each (x,y) column
     is filled from z_s + depth[0] to z_s + depth[1] (z_s the bilinear DEM
     height, i.e. what the grid boundary sees).  ``x_stride`` > 1 keeps every
     k-th x column; ``fraction`` < 1 keeps the leading fraction of the release
-    zone in x (contiguous: same block occupancy as the full scene).
+    zone in x (contiguous: same block occupancy as the full scene);
+    ``columns=(c0, c1)`` keeps x-lattice columns c0..c1-1 (one rank's slab).
     """
     hf = landslide_terrain()
     sp = h / ppc
@@ -135,6 +136,8 @@ def landslide(h=0.5, ppc=2, release=((100.0, 350.0), (-62.5, 62.5)), depth=(0.5,
     xs = x0 + (np.arange(int(round((x1 - x0) / sp))) + 0.5) * sp
     ys = y0 + (np.arange(int(round((y1 - y0) / sp))) + 0.5) * sp
     xs = xs[: max(1, int(round(xs.shape[0] * fraction)))][::x_stride]
+    if columns is not None:
+        xs = xs[columns[0]:columns[1]]
     nz = int(round((depth[1] - depth[0]) / sp))
     zoff = depth[0] + (np.arange(nz) + 0.5) * sp
     gx, gy = np.meshgrid(xs, ys, indexing="ij")
@@ -150,6 +153,39 @@ def landslide(h=0.5, ppc=2, release=((100.0, 350.0), (-62.5, 62.5)), depth=(0.5,
                     domain_max=np.array([2000.0, 250.0, 700.0]))
     bc = BoundaryCondition(kind="heightfield", mu=mu, heightfield=hf)
     return Scene("landslide", ps, cfg, [SAND], [bc])
+
+
+def landslide_columns(h=0.5, ppc=2, release=((100.0, 350.0), (-62.5, 62.5)), fraction=1.0):
+    """x of every lattice column of the landslide release zone."""
+    sp = h / ppc
+    (x0, x1), _ = release
+    xs = x0 + (np.arange(int(round((x1 - x0) / sp))) + 0.5) * sp
+    return xs[: max(1, int(round(xs.shape[0] * fraction)))]
+
+
+def landslide_slabs(world, h=0.5, ppc=2, fraction=1.0):
+    """Block-aligned slab cuts of the landslide for ``world`` ranks with equal
+    particle counts (every column holds the same number of particles):
+    [(bx0, bx1, c0, c1)], columns c0..c1-1 belong to the slab."""
+    from .slabs import INT32_MAX, INT32_MIN
+
+    xs = landslide_columns(h, ppc, fraction=fraction)
+    bx = np.floor(xs * (1.0 / h) - 0.5).astype(np.int64) >> 2
+    out = []
+    cuts = [0]
+    for r in range(1, world):
+        c = int(round(r * len(xs) / world))
+        # move the cut to a block boundary
+        while 0 < c < len(xs) and bx[c] == bx[c - 1]:
+            c += 1
+        cuts.append(c)
+    cuts.append(len(xs))
+    for r in range(world):
+        c0, c1 = cuts[r], cuts[r + 1]
+        lo = INT32_MIN if r == 0 else int(bx[c0])
+        hi = INT32_MAX if r == world - 1 else int(bx[c1])
+        out.append((lo, hi, c0, c1))
+    return out
 
 
 CONFIGS = {

@@ -177,6 +177,7 @@ class DistributedSimulation:
         self.lib = _lib.load()
         self.t = 0.0
         self.step_count = 0
+        self.migrated = 0  # particles received from neighbours so far
         self._torch = torch
         # step 0: P2G of the initial state on every rank, then the halo exchange
         nb = ctypes.c_int64(0)
@@ -226,6 +227,7 @@ class DistributedSimulation:
         from_l, from_r = self.tr.exchange(self._migrants(0), self._migrants(1))
         for buf in (from_l, from_r):
             if buf is not None:
+                self.migrated += buf.numel() // PARTICLE_REC_BYTES
                 _lib.check(self.lib.smpm_sim_accept(self._h, _lib.ptr(buf), buf.numel() // PARTICLE_REC_BYTES),
                            "accept")
         self.sim.stream.synchronize()

@@ -19,7 +19,7 @@ STEPS = 8
 def _scene():
     from tests.test_gpu_sim import column_scene
 
-    ps, cfg, mats, bc = column_scene(bcs="mixed", vx=3.0)
+    ps, cfg, mats, bc = column_scene(bcs="mixed", vx=3.0, size=(1.2, 0.2, 0.3))
     return ps, cfg, mats, bc
 
 
@@ -58,11 +58,12 @@ def _worker(rank, world, port, dts, outdir):
         st = ds.step(dt)
         stats.append((st.n_active, st.n_allocated))
     pid, x, v = ds.gather_particles()
+    moved = ds.tr.allreduce([ds.migrated], "sum")
     # pid -> original index
     order = np.concatenate(parts)
     if rank == 0:
         np.savez(os.path.join(outdir, "dist.npz"), stats=np.array(stats), pid=order[pid], x=x, v=v,
-                 counts=np.array([len(p) for p in parts]))
+                 counts=np.array([len(p) for p in parts]), moved=moved)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -78,6 +79,7 @@ def test_two_slabs_match_single_gpu(tmp_path):
     mp.spawn(_worker, args=(2, port, dts, str(tmp_path)), nprocs=2, join=True)
     d = np.load(tmp_path / "dist.npz")
     assert d["counts"].min() > 0.3 * ps.n  # both slabs populated
+    assert d["moved"][0] > 0  # particles crossed the slab cut
     stats = d["stats"]
     # step 1 is computed from identical initial positions: exact
     assert stats[0][0] == dts[0][1]
