@@ -7,6 +7,7 @@ PyTorch is used only for device memory and the current stream.
 """
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
@@ -14,7 +15,8 @@ import numpy as np
 from .errors import ConfigError, InactiveNodeError, KeyRangeError, SimulationError
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "libsmpm.so"
+# SMPM_LIB selects an in-tree build variant (tools/build_variant.sh) for A/B timing
+LIB_PATH = HERE / os.environ.get("SMPM_LIB", "libsmpm.so")
 
 OK = 0
 ERR_NONFINITE_X = 1

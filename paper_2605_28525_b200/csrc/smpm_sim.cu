@@ -36,6 +36,9 @@ namespace smpm {
 // stencil offset the 32 lanes hit 32 distinct banks (68 = 4 mod 32); measured
 // 29 lane-atomics/clk/SM vs 8.6 for a naive layout
 // (profiles/r01_ubench_atomics.md).
+#ifndef SMPM_MINB
+#define SMPM_MINB 2  // resident CTAs per SM the fused kernel is register-budgeted for
+#endif
 constexpr int AI = 68, AJ = 8;
 constexpr int SCAT_N = 8 * AI;   // scatter arena: nodes 4B-1 .. 4B+6 per axis
 constexpr int NF = 7;            // m, p0..2, f0..2
@@ -44,7 +47,8 @@ constexpr int CTA = 256;         // 64 cells x 4 slots
 constexpr int SLOTS = 4;
 constexpr uint32_t MAGIC_BITS = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float MAGIC = 12582912.0f;
-constexpr uint32_t BAD_KEY = 0xFFFFFFFFu;
+constexpr uint32_t BAD_KEY = 0xFFFFFFFFu;  // bin of a hole (departed particle) or an invalid one
+constexpr uint32_t OVF_KEY = 0xFFFFFFFEu;  // live particle whose block did not fit (replayed after growth)
 // Gather arena: float4 velocity per node, nodes 4B .. 4B+5 per axis, address
 // (k ^ 4*(j&1)) + 8 j + 48 i in float4 units: each quarter-warp (2x4 cells)
 // reads 8 distinct 16-byte bank groups, so the 27 LDS.128 per particle are
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S) {
 __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     uint32_t key = bin[i];
-    if (key == BAD_KEY) continue;
+    if (key >= OVF_KEY) continue;
     perm[atomicAdd(&S.cell_off[key], 1u)] = uint32_t(i);
   }
 }
@@ -375,7 +379,7 @@ __global__ void k_prologue_keys(Particles P, int64_t n, TableDev B, uint32_t* __
     uint64_t key = pack_key(base[0] >> 2, base[1] >> 2, base[2] >> 2);
     uint32_t rank = hash_insert(B.hv, key);
     if (rank >= B.hv.cap_blocks) {
-      bin[i] = BAD_KEY;
+      bin[i] = OVF_KEY;
       continue;
     }
     uint32_t cell = uint32_t(((base[0] & 3) << 4) | ((base[1] & 3) << 2) | (base[2] & 3));
@@ -487,7 +491,7 @@ __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float 
   }
   uint32_t r = hash_insert(A.S.hv, pack_key(nb[0] >> 2, nb[1] >> 2, nb[2] >> 2));
   if (r >= A.S.hv.cap_blocks) {
-    binv = BAD_KEY;
+    binv = OVF_KEY;
     return;
   }
   uint32_t cell = uint32_t(((nb[0] & 3) << 4) | ((nb[1] & 3) << 2) | (nb[2] & 3));
@@ -541,7 +545,7 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
 }
 
 template <bool GATHER>
-__global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
+__global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
   FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smraw);
   const int tid = threadIdx.x;
@@ -975,7 +979,7 @@ __global__ void __launch_bounds__(CTA, 2) k_g2p2g(FusedArgs A) {
       if (ok && !far && mig < 0) {
         uint32_t rk = sm.rank[((ab[0] + 3) >> 2) * 9 + ((ab[1] + 3) >> 2) * 3 + ((ab[2] + 3) >> 2)];
         uint32_t lc = (((ab[0] + 3) & 3) << 4) | (((ab[1] + 3) & 3) << 2) | ((ab[2] + 3) & 3);
-        binv = rk == BAD_KEY ? BAD_KEY : rk * 64 + lc;
+        binv = rk == BAD_KEY ? OVF_KEY : rk * 64 + lc;
       }
       A.bin_out[pos] = binv;
     }
@@ -1516,6 +1520,7 @@ int run_prologue(smpm_sim* s, int project) {
     need = 0;
     rc = table_state(s, s->S, &need, &over);
     if (rc) return rc;
+    s->n_store = s->hstats[0].n_binned;  // the P2G pass wrote every binned particle at its sorted position
     code = decode_err(*s->herr, &p);
     if (code) {
       s->pending_err = code;
