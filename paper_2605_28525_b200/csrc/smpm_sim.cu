@@ -2,10 +2,10 @@
 // (reference: /root/reference/pkg/src/sparsempm/solver.py:1001-1093).
 //
 // Per step (S = table of this step's particles, T = the other table):
-//   scan1(S)  block totals, n_active (popcount of node masks), dt, snapshot T
+//   scan1(S)  block totals, item counts, dt, snapshot T
 //   scan2(S)  cell offsets + work items (block rank, slot group)
 //   bin(S)    perm[cell_off[key] + idx] = storage index
-//   grid(S)   momentum -> velocity + boundaries over active nodes; zero the
+//   grid(S)   momentum -> velocity + boundaries over active nodes, n_active; zero the
 //             accumulators; clear table T
 //   g2p2g(S -> T)  per work item: G2P from the smem velocity arena, F update,
 //             advection, Hencky/DP return map of the *next* step's stress,
@@ -71,7 +71,6 @@ struct Particles {
 
 struct TableDev {
   HashView hv;
-  uint64_t* nodemask;    // [cap_b]
   uint32_t* cell_count;  // [cap_b*64]
   uint32_t* cell_off;    // [cap_b*64]
   uint32_t* block_total; // [cap_b]
@@ -159,7 +158,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
   const int ntiles = (nb + TB - 1) / TB;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    uint32_t s_tot = 0, s_items = 0, s_pop = 0, s_own = 0;
+    uint32_t s_tot = 0, s_items = 0, s_own = 0;
     for (int b = w; b < TB; b += 8) {
       uint32_t r = tile * TB + b;
       if (r >= nb) break;
@@ -180,16 +179,13 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
         s_items += items;
         int bi, bj, bk;
         unpack_key(S.hv.active_keys[r], bi, bj, bk);
-        if (bi >= sp.bx0 && bi < sp.bx1) {
-          s_pop += __popcll(S.nodemask[r]);
-          s_own += 1;
-        }
+        if (bi >= sp.bx0 && bi < sp.bx1) s_own += 1;
       }
     }
     if (lane == 0) {
       red[0][w] = s_tot;
       red[1][w] = s_items;
-      red[2][w] = s_pop;
+      red[2][w] = 0;
       red[3][w] = s_own;
     }
     __syncthreads();
@@ -208,7 +204,6 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
   __threadfence();
   uint32_t carry[4] = {0, 0, 0, 0};
   __shared__ uint32_t sh[8];
-  unsigned long long n_active = 0;
   for (int base = 0; base < ntiles; base += 256) {
     int t = base + threadIdx.x;
     for (int ch = 0; ch < 4; ++ch) {
@@ -216,7 +211,6 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
       uint32_t tot;
       uint32_t ex = cta_excl_scan(v, sh, tot);
       if (t < ntiles && ch < 2) S.tile_sums[4 * t + ch] = ex + carry[ch];
-      if (ch == 2) n_active += tot;
       carry[ch] += tot;
     }
   }
@@ -227,7 +221,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
     st->n_blocks = nb;
     st->n_items = carry[1];
     st->n_binned = carry[0];
-    st->n_active = n_active;
+    st->n_active = 0;  // counted by k_grid (nodes with a stencil contribution, acc .w > 0)
     st->n_owned = carry[3];
     st->overflow = *S.hv.overflow | (*S.hv.counter > S.hv.cap_blocks ? 1u : 0u);
     // dt is validated on the host against the CFL bound (solver.py:1021-1030)
@@ -298,11 +292,12 @@ __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, u
 // table T for reuse by the next P2G).
 __global__ void __launch_bounds__(256) k_grid(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
                                               float4* __restrict__ acc, float4* __restrict__ gv, GridParams gp,
-                                              int record) {
+                                              int record, int bx0, int bx1) {
   const uint32_t nb = stS->n_blocks;
   gp.dt = stS->dt;
   const size_t nn = size_t(nb) * 64;
   double msum = 0, p0s = 0, p1s = 0, p2s = 0;
+  uint32_t act = 0;
   for (size_t c = blockIdx.x * size_t(blockDim.x) + threadIdx.x; c < nn; c += size_t(gridDim.x) * blockDim.x) {
     uint32_t r = uint32_t(c >> 6), l = uint32_t(c & 63);
     float4 a = acc[2 * c], b = acc[2 * c + 1];
@@ -314,6 +309,7 @@ __global__ void __launch_bounds__(256) k_grid(TableDev S, TableDev T, DevStats* 
     grid_node(gp, bi * 4 + int(l >> 4), bj * 4 + int((l >> 2) & 3), bk * 4 + int(l & 3), a.x, a.y, a.z, a.w, b.x,
               b.y, b.z, o0, o1, o2);
     gv[c] = make_float4(o0, o1, o2, 0.f);
+    act += (b.w > 0.f && bi >= bx0 && bi < bx1) ? 1u : 0u;
     if (record) {
       msum += a.x;
       p0s += a.y;
@@ -321,6 +317,8 @@ __global__ void __launch_bounds__(256) k_grid(TableDev S, TableDev T, DevStats* 
       p2s += a.w;
     }
   }
+  act = warp_sum(act);
+  if ((threadIdx.x & 31) == 0 && act) atomicAdd(&stS->n_active, (unsigned long long)act);
   if (record) {
     for (int o = 16; o; o >>= 1) {
       msum += __shfl_xor_sync(0xffffffffu, msum, o);
@@ -341,7 +339,6 @@ __global__ void __launch_bounds__(256) k_grid(TableDev S, TableDev T, DevStats* 
     uint32_t s = T.hv.slot_of_rank[r];
     T.hv.keys[s] = EMPTY_KEY;
     T.hv.vals[s] = EMPTY_VAL;
-    T.nodemask[r] = 0;
   }
   for (size_t c = blockIdx.x * size_t(blockDim.x) + threadIdx.x; c < size_t(nbt) * 64;
        c += size_t(gridDim.x) * blockDim.x)
@@ -417,14 +414,17 @@ struct ItemInfo {
   uint32_t nbr[8];
 };
 
+// Item i scatters into arena X[i&1] while item i-1's arena X[(i-1)&1] is
+// flushed; counts, bound maxima, touched-block masks and block ranks are
+// double-buffered the same way (see the loop in k_g2p2g).
 struct __align__(16) FusedSmem {
   float4 stage[CTA * 8];     // prefetched particle records (chunk c of thread t at t*8 + ((c+t)&7))
   float4 garena[2][GATH_N];  // double-buffered velocity arena
-  int acc[NA][SCAT_N];       // fixed-point arena (+ contribution count)
-  uint32_t cnt[SCAT_N];      // particles per arena base cell; later: bin base
-  uint32_t occ[16];          // base-cell occupancy bitmap: 8x8 rows (i,j) of 8 k-bits
-  uint32_t rank[27];
-  uint32_t bmax[3];
+  int acc[2][NA][SCAT_N];    // fixed-point arenas (+ contribution count K)
+  uint32_t cnt[2][SCAT_N];   // particles per arena base cell (bin sizes)
+  uint32_t touched[2];       // 27-bit masks of the neighbour blocks the item's stencils touch
+  uint32_t rank[2][27];      // next-table ranks of those blocks
+  uint32_t bmax[2][3];       // contribution bounds (mass, momentum, force)
   ItemInfo info[3];          // ring: items i, i+1, i+2
   Material mats[8];
 };
@@ -447,12 +447,26 @@ __device__ __forceinline__ int magic_q(float t) { return __float_as_int(t); }
 // power-of-two fixed-point scale for contributions bounded by b: b*S <= 2^22
 // (exact magic-add conversion) and 256 contributions fit in int32
 __device__ __forceinline__ float fx_scale(float b, float& inv) {
-  int e = 0;
-  if (b > 0.f) frexpf(b, &e);
-  int s = 22 - e;
-  s = max(-100, min(100, s));
-  inv = ldexpf(1.0f, -s);
-  return ldexpf(1.0f, s);
+  // b = f 2^e, f in [0.5, 1): e from the exponent field (b >= 0 finite)
+  const int e = b > 0.f ? int((__float_as_uint(b) >> 23) & 0xFFu) - 126 : 0;
+  const int s = max(-100, min(100, 22 - e));
+  inv = __uint_as_float(uint32_t(127 - s) << 23);
+  return __uint_as_float(uint32_t(127 + s) << 23);
+}
+
+// Blocks (arena block index 0..2 per axis: arena node coordinate 0 -> 0,
+// 1..4 -> 1, 5..7 -> 2) touched by a stencil with arena base coordinate ab
+// (nodes ab .. ab+2): a 3-bit range mask.
+__device__ __forceinline__ uint32_t axis_blocks(int ab) {
+  const int lo = (ab + 3) >> 2, hi = (ab + 5) >> 2;
+  return (2u << hi) - (1u << lo);
+}
+// 27-bit outer product, bit index 9 bi + 3 bj + bk
+__device__ __forceinline__ uint32_t touched27(uint32_t mx, uint32_t my, uint32_t mz) {
+  const uint32_t X = ((mx & 1u) ? 0x1FFu : 0u) | ((mx & 2u) ? 0x3FE00u : 0u) | ((mx & 4u) ? 0x7FC0000u : 0u);
+  const uint32_t Y = ((my & 1u) ? 0x1C0E07u : 0u) | ((my & 2u) ? 0xE07038u : 0u) | ((my & 4u) ? 0x70381C0u : 0u);
+  const uint32_t Z = ((mz & 1u) ? 0x1249249u : 0u) | ((mz & 2u) ? 0x2492492u : 0u) | ((mz & 4u) ? 0x4924924u : 0u);
+  return X & Y & Z;
 }
 
 // Global (slow-path) scatter of a particle that moved outside its block's
@@ -482,8 +496,7 @@ __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float 
         float f2 = -(M[4] * gx + M[5] * gy + M[2] * gz);
         size_t node = size_t(r) * 64 + l;
         red_v4(&A.acc[2 * node], wm, wm * mv0, wm * mv1, wm * mv2);
-        red_v4(&A.acc[2 * node + 1], f0, f1, f2, 0.f);
-        atomicOr((unsigned long long*)&A.S.nodemask[r], 1ull << l);
+        red_v4(&A.acc[2 * node + 1], f0, f1, f2, 1.f);  // .w: contribution count K (n_active)
       }
   if (!bin) {
     binv = BAD_KEY;
@@ -544,6 +557,21 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
   }
 }
 
+// One persistent CTA works through items (block, group of SLOTS particles per
+// cell), 256 threads = 64 cells x 4 slots.  Item i, parity p = i & 1:
+//   [B1]  records / velocity arena of item i have landed; item i-1 is fully
+//         scattered into X[p^1] and its blocks are inserted (rank[p^1]).
+//   A     zero X[p]; G2P, F update, advection, stress of the next step, record
+//         store, next-step keys, contribution bounds, touched-block mask and
+//         bin counts of item i.
+//   [B2]  bounds / masks / counts of item i complete.
+//   B     warp 0 probes the next table for item i's touched blocks; all
+//         threads scatter item i into X[p] (fixed point), then flush item i-1
+//         from X[p^1] (red.global.add.v4.f32; .w carries the contribution
+//         count K), write its bins and cell counts; warp 0 resolves item i's
+//         ranks into rank[p].
+// Two barriers per item; the hash-insert latency of item i is hidden behind
+// the flush of item i-1 (the flush of the last item runs after the loop).
 template <bool GATHER>
 __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -555,11 +583,18 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   const float ih = float(A.inv_h);
   const float hf_ = float(A.h);
   uint32_t vmax2_local = 0;
+  {
+    int4* z = reinterpret_cast<int4*>(&sm.acc[0][0][0]);
+    for (int i = tid; i < 2 * NA * SCAT_N / 4; i += CTA) z[i] = make_int4(0, 0, 0, 0);
+    int4* zc = reinterpret_cast<int4*>(&sm.cnt[0][0]);
+    for (int i = tid; i < 2 * SCAT_N / 4; i += CTA) zc[i] = make_int4(0, 0, 0, 0);
+    if (tid < 6) sm.bmax[tid / 3][tid % 3] = 0;
+    if (tid < 2) sm.touched[tid] = 0;
+  }
 
   // ---- prime the pipeline: records of item 0, indices of item 1, metadata
   // of item 2.  In steady state item i computes while item i+1's records and
   // velocity arena are in flight and item i+2's indices are being loaded.
-  if (tid < 3) sm.bmax[tid] = 0;  // re-zeroed after [B3] each item (read after [B2])
   if (tid == 0) fetch_item(A, n_items, sm.info[0]);
   __syncthreads();
   uint32_t pos = 0, pos1 = 0, src1 = 0;
@@ -580,24 +615,69 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   }
   if (GATHER && sm.info[0].r != BAD_KEY) prefetch_arena(sm, A, sm.info[0], 0, tid);
   cp_async_commit();
-  int buf = 0, c = 0;
+  int buf = 0, c = 0, p = 0;
+  bool have_prev = false;
+  // bin of this thread's particle of item i-1: kind 0 none, 1 final value
+  // prev_bin, 2 arena cell (packed ab) resolved with rank[p^1]
+  int prev_kind = 0;
+  uint32_t prev_pos = 0, prev_bin = 0;
+  float piSm = 0.f, piSp = 0.f, piSf = 0.f;
+
+  // flush of the item scattered into X[q] with ranks rank[q] (and its bins)
+  auto flush = [&](int q) {
+    if (prev_kind == 1) {
+      A.bin_out[prev_pos] = prev_bin;
+    } else if (prev_kind == 2) {
+      const int a0 = int(prev_bin >> 6), a1 = int((prev_bin >> 3) & 7u), a2 = int(prev_bin & 7u);
+      const uint32_t rk = sm.rank[q][((a0 + 3) >> 2) * 9 + ((a1 + 3) >> 2) * 3 + ((a2 + 3) >> 2)];
+      const uint32_t lc = (((a0 + 3) & 3) << 4) | (((a1 + 3) & 3) << 2) | ((a2 + 3) & 3);
+      A.bin_out[prev_pos] = rk == BAD_KEY ? OVF_KEY : rk * 64 + lc;
+    }
+    for (int n = tid; n < 216; n += CTA) {
+      const int i = n / 36, j = (n / 6) % 6, k = n % 6;
+      const int ad = aaddr(i, j, k);
+      const uint32_t cc = sm.cnt[q][ad];
+      if (cc) {
+        sm.cnt[q][ad] = 0;
+        const uint32_t rq = sm.rank[q][((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
+        const uint32_t lc = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
+        if (rq != BAD_KEY) atomicAdd(&A.S.cell_count[rq * 64 + lc], cc);
+      }
+    }
+    // value = (sum - K * MAGIC_BITS) / S
+    for (int n = tid; n < 512; n += CTA) {
+      const int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
+      const int ad = aaddr(i, j, k);
+      const uint32_t K = uint32_t(sm.acc[q][7][ad]);
+      if (!K) continue;
+      const uint32_t rk = sm.rank[q][((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
+      if (rk == BAD_KEY) continue;
+      const int l = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
+      const uint32_t bias = K * MAGIC_BITS;
+      float vals[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) vals[f] = float(int(uint32_t(sm.acc[q][f][ad]) - bias));
+      const size_t node = size_t(rk) * 64 + l;
+      red_v4(&A.acc[2 * node], vals[0] * piSm, vals[1] * piSp, vals[2] * piSp, vals[3] * piSp);
+      red_v4(&A.acc[2 * node + 1], vals[4] * piSf, vals[5] * piSf, vals[6] * piSf, float(K));
+    }
+  };
 
   while (true) {
     cp_async_wait_all();
-    __syncthreads();  // [B1] records + arena of this item landed; previous flush done
+    __syncthreads();  // [B1]
     const ItemInfo& cur = sm.info[c];
     const ItemInfo& nxt = sm.info[c == 2 ? 0 : c + 1];
     const ItemInfo& nn = sm.info[c == 0 ? 2 : c - 1];
     const uint32_t r = cur.r;
     if (r == BAD_KEY) break;
     const int B0 = cur.b[0], B1 = cur.b[1], B2 = cur.b[2];
-    // zero the scatter arena (previous item's flush is complete)
+    // X[p] was flushed during the previous iteration: zero it for item i
     {
-      int4* z = reinterpret_cast<int4*>(&sm.acc[0][0]);
+      int4* z = reinterpret_cast<int4*>(&sm.acc[p][0][0]);
       for (int i = tid; i < NA * SCAT_N / 4; i += CTA) z[i] = make_int4(0, 0, 0, 0);
-      int4* zc = reinterpret_cast<int4*>(&sm.cnt[0]);
-      for (int i = tid; i < SCAT_N / 4; i += CTA) zc[i] = make_int4(0, 0, 0, 0);
-      if (tid < 16) sm.occ[tid] = 0;
+      if (tid < 3) sm.bmax[p ^ 1][tid] = 0;
+      if (tid == 3) sm.touched[p ^ 1] = 0;
     }
     if (GATHER && tid < 8 && nxt.r != BAD_KEY)
       sm.info[c == 2 ? 0 : c + 1].nbr[tid] = A.B.nbr8[size_t(nxt.r) * 8 + tid];
@@ -624,7 +704,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     bool far = false, ok = valid;
     int mig = -1;
     float bm = 0.f, bp = 0.f, bf = 0.f;
-    uint32_t pidv = 0;
+    uint32_t pidv = 0, tmask = 0;
     if (valid) {
       xn[0] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
       xn[1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
@@ -825,26 +905,23 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
           bm = m * W * 1.0001f;
           bp = m * W * cm * 1.0001f;
           bf = fm * 1.0001f;
+          tmask = touched27(axis_blocks(ab[0]), axis_blocks(ab[1]), axis_blocks(ab[2]));
+          if (mig < 0) atomicAdd(&sm.cnt[p][aaddr(ab[0], ab[1], ab[2])], 1u);
         }
       }
     }
-    // base-cell occupancy of the next step (exact touched-node set = its 3x3x3
-    // dilation) and the per-cell particle count (bin size, local bin index)
-    if (ok && !far) {
-      const int row = ab[0] * 8 + ab[1];
-      atomicOr(&sm.occ[row >> 2], 1u << (((row & 3) << 3) | ab[2]));
-      if (mig < 0) atomicAdd(&sm.cnt[aaddr(ab[0], ab[1], ab[2])], 1u);
-    }
     {
-      uint32_t um = warp_max(__float_as_uint(bm)), up = warp_max(__float_as_uint(bp)),
-               uf = warp_max(__float_as_uint(bf));
+      const uint32_t um = warp_max(__float_as_uint(bm)), up = warp_max(__float_as_uint(bp)),
+                     uf = warp_max(__float_as_uint(bf));
+      const uint32_t tm = __reduce_or_sync(0xffffffffu, tmask);
       if ((tid & 31) == 0) {
-        atomicMax(&sm.bmax[0], um);
-        atomicMax(&sm.bmax[1], up);
-        atomicMax(&sm.bmax[2], uf);
+        atomicMax(&sm.bmax[p][0], um);
+        atomicMax(&sm.bmax[p][1], up);
+        atomicMax(&sm.bmax[p][2], uf);
+        if (tm) atomicOr(&sm.touched[p], tm);
       }
     }
-    __syncthreads();  // [B2] bounds; occupancy; next item's neighbour ranks
+    __syncthreads();  // [B2] bounds, touched blocks and bin counts of item i
     if (GATHER && nxt.r != BAD_KEY) prefetch_arena(sm, A, nxt, buf ^ 1, tid);
     cp_async_commit();
     // item i+2: raw index loads now, consumed after the scatter
@@ -855,54 +932,28 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
       cnt2 = A.B.cell_count[key2];
       off2 = A.B.cell_off[key2];
     }
-    // ---- warp 0: touched-node masks of the 27 neighbour blocks by dilating
-    // the occupancy bitmap (node n touched iff a base in n - {0,1,2}^3 is
-    // occupied) and a probe of each block's hash slot; the probe latency
-    // overlaps the scatter, the insert resolves after it.
-    uint64_t mk = 0;
+    // warp 0: probe the home slot of each touched block of the next table;
+    // the probe latency overlaps the scatter, the insert resolves after it
+    const uint32_t tmask_all = sm.touched[p];
     uint64_t ins_key = 0, probe_key = 0;
     uint32_t probe_val = EMPTY_VAL;
-    if (tid < 32) {
-      const unsigned char* ob = reinterpret_cast<const unsigned char*>(sm.occ);
-      uint32_t rows2 = 0;  // dilated rows (i, j) for row = tid and row = tid + 32, one byte each
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int row = tid + 32 * h2, i = row >> 3, j = row & 7;
-        uint32_t acc8 = 0;
-#pragma unroll
-        for (int di = 0; di < 3; ++di)
-#pragma unroll
-          for (int dj = 0; dj < 3; ++dj)
-            if (i - di >= 0 && j - dj >= 0) acc8 |= ob[(i - di) * 8 + (j - dj)];
-        acc8 = (acc8 | (acc8 << 1) | (acc8 << 2)) & 0xFFu;
-        rows2 |= acc8 << (8 * h2);
-      }
+    const bool inserter = tid < 27 && ((tmask_all >> tid) & 1u);
+    if (inserter) {
       const int di = tid / 9 - 1, dj = (tid / 3) % 3 - 1, dk = tid % 3 - 1;
-#pragma unroll
-      for (int li = 0; li < 4; ++li)
-#pragma unroll
-        for (int lj = 0; lj < 4; ++lj) {
-          const int ai = 4 * di + 1 + li, aj = 4 * dj + 1 + lj;
-          const bool in = ai >= 0 && ai < 8 && aj >= 0 && aj < 8;
-          const int row = in ? ai * 8 + aj : 0;
-          const uint32_t r8 = (__shfl_sync(0xffffffffu, rows2, row & 31) >> (8 * (row >> 5))) & 0xFFu;
-          uint32_t nib = dk < 0 ? (r8 & 1u) << 3 : (dk == 0 ? (r8 >> 1) & 15u : (r8 >> 5) & 7u);
-          if (in) mk |= uint64_t(nib) << ((li << 4) | (lj << 2));
-        }
-      if (tid < 27 && mk) {
-        ins_key = pack_key(B0 + di, B1 + dj, B2 + dk);
-        const uint32_t sl = uint32_t(mix64(ins_key)) & A.S.hv.mask;
-        probe_key = ld_volatile_u64(&A.S.hv.keys[sl]);
-        probe_val = ld_volatile_u32(&A.S.hv.vals[sl]);
-      }
+      ins_key = pack_key(B0 + di, B1 + dj, B2 + dk);
+      const uint32_t sl = uint32_t(mix64(ins_key)) & A.S.hv.mask;
+      probe_key = ld_volatile_u64(&A.S.hv.keys[sl]);
+      probe_val = ld_volatile_u32(&A.S.hv.vals[sl]);
     }
     float iSm, iSp, iSf;
-    const float Sm = fx_scale(__uint_as_float(sm.bmax[0]), iSm);
-    const float Sp = fx_scale(__uint_as_float(sm.bmax[1]), iSp);
-    const float Sf = fx_scale(__uint_as_float(sm.bmax[2]), iSf);
+    const float Sm = fx_scale(__uint_as_float(sm.bmax[p][0]), iSm);
+    const float Sp = fx_scale(__uint_as_float(sm.bmax[p][1]), iSp);
+    const float Sf = fx_scale(__uint_as_float(sm.bmax[p][2]), iSf);
+    int kind = 0;
     uint32_t binv = BAD_KEY;
+    if (valid) kind = 1;
     if (ok && !far) {
-      // ---- P2G of the next step into the fixed-point arena
+      // ---- P2G of the next step into the fixed-point arena X[p]
       float w[3][3], g[3][3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) bspline(d1[a], w[a], g[a]);
@@ -919,7 +970,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
         cz[1][k] = Cn[5] * dz;
         cz[2][k] = Cn[8] * dz;
       }
-      int* a0 = &sm.acc[0][ad0];
+      int* a0 = &sm.acc[p][0][ad0];
 #pragma unroll
       for (int oi = 0; oi < 3; ++oi) {
         const float dx = (float(oi) - d1[0]) * hf_;
@@ -939,11 +990,11 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
           for (int ok2 = 0; ok2 < 3; ++ok2) {
             const int o = aaddr(oi, oj, ok2);
             const float wz = w[2][ok2], gz = g[2][ok2];
-            const float cm = wmp * wz;
+            const float cmz = wmp * wz;
             sred(a0 + o, magic_q(fmaf(wmm, wz, MAGIC)));
-            sred(a0 + 1 * SCAT_N + o, magic_q(fmaf(cm, q0 + cz[0][ok2], MAGIC)));
-            sred(a0 + 2 * SCAT_N + o, magic_q(fmaf(cm, q1 + cz[1][ok2], MAGIC)));
-            sred(a0 + 3 * SCAT_N + o, magic_q(fmaf(cm, q2 + cz[2][ok2], MAGIC)));
+            sred(a0 + 1 * SCAT_N + o, magic_q(fmaf(cmz, q0 + cz[0][ok2], MAGIC)));
+            sred(a0 + 2 * SCAT_N + o, magic_q(fmaf(cmz, q1 + cz[1][ok2], MAGIC)));
+            sred(a0 + 3 * SCAT_N + o, magic_q(fmaf(cmz, q2 + cz[2][ok2], MAGIC)));
             sred(a0 + 4 * SCAT_N + o, magic_q(fmaf(wz, r0, fmaf(gz, s0, MAGIC))));
             sred(a0 + 5 * SCAT_N + o, magic_q(fmaf(wz, r1, fmaf(gz, s1, MAGIC))));
             sred(a0 + 6 * SCAT_N + o, magic_q(fmaf(wz, r2, fmaf(gz, s2, MAGIC))));
@@ -951,19 +1002,23 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
           }
         }
       }
+      if (mig < 0) {
+        kind = 2;
+        binv = uint32_t((ab[0] << 6) | (ab[1] << 3) | ab[2]);
+      }
     } else if (ok && far) {
       scatter_global(A, nb, d1, m, vn, Cn, M, binv, mig < 0);
     }
+    // ---- flush item i-1 (its ranks were resolved before [B1])
+    if (have_prev) flush(p ^ 1);
+    // ---- warp 0: ranks of item i's touched blocks
     if (tid < 27) {
       uint32_t rk = BAD_KEY;
-      if (mk) {
+      if (inserter) {
         rk = (probe_key == ins_key && probe_val != EMPTY_VAL) ? probe_val : hash_insert(A.S.hv, ins_key);
-        if (rk < A.S.hv.cap_blocks)
-          atomicOr((unsigned long long*)&A.S.nodemask[rk], (unsigned long long)mk);
-        else
-          rk = BAD_KEY;
+        if (rk >= A.S.hv.cap_blocks) rk = BAD_KEY;
       }
-      sm.rank[tid] = rk;
+      sm.rank[p][tid] = rk;
     }
     // item i+2's sorted position and source index (consumed one item later)
     uint32_t pos2 = 0, src2 = 0;
@@ -972,54 +1027,26 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
       pos2 = off2 - cnt2 + slot2;  // k_bin advanced cell_off to the cell's end
       src2 = A.perm[pos2];
     }
-    __syncthreads();  // [B3] arena complete; ranks of the next table known
-    // ---- bins of the next step: cell key only; positions are assigned by
-    // k_bin.  Cell counts go out as fire-and-forget reductions.
-    if (valid) {
-      if (ok && !far && mig < 0) {
-        uint32_t rk = sm.rank[((ab[0] + 3) >> 2) * 9 + ((ab[1] + 3) >> 2) * 3 + ((ab[2] + 3) >> 2)];
-        uint32_t lc = (((ab[0] + 3) & 3) << 4) | (((ab[1] + 3) & 3) << 2) | ((ab[2] + 3) & 3);
-        binv = rk == BAD_KEY ? OVF_KEY : rk * 64 + lc;
-      }
-      A.bin_out[pos] = binv;
-    }
-    for (int n = tid; n < 216; n += CTA) {
-      int i = n / 36, j = (n / 6) % 6, k = n % 6;
-      uint32_t cc = sm.cnt[aaddr(i, j, k)];
-      if (cc) {
-        uint32_t rq = sm.rank[((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
-        uint32_t lc = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
-        if (rq != BAD_KEY) atomicAdd(&A.S.cell_count[rq * 64 + lc], cc);
-      }
-    }
-    // ---- flush the arena: value = (sum - K * MAGIC_BITS) / S
-    for (int n = tid; n < 512; n += CTA) {
-      int i = n >> 6, j = (n >> 3) & 7, k = n & 7;
-      int ad = aaddr(i, j, k);
-      uint32_t K = uint32_t(sm.acc[7][ad]);
-      if (!K) continue;
-      uint32_t rk = sm.rank[((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
-      if (rk == BAD_KEY) continue;
-      int l = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
-      const uint32_t bias = K * MAGIC_BITS;
-      float vals[NF];
-#pragma unroll
-      for (int f = 0; f < NF; ++f) vals[f] = float(int(uint32_t(sm.acc[f][ad]) - bias));
-      size_t node = size_t(rk) * 64 + l;
-      red_v4(&A.acc[2 * node], vals[0] * iSm, vals[1] * iSp, vals[2] * iSp, vals[3] * iSp);
-      red_v4(&A.acc[2 * node + 1], vals[4] * iSf, vals[5] * iSf, vals[6] * iSf, 0.f);
-    }
-    // ---- rotate: item i+3's metadata goes into this item's ring slot
+    // ---- rotate: item i+3's metadata goes into this item's ring slot (warp 0
+    // has finished reading it; the other warps read it before [B2])
     if (tid == 0) fetch_item(A, n_items, sm.info[c]);
-    if (tid < 3) sm.bmax[tid] = 0;
+    have_prev = true;
+    prev_kind = kind;
+    prev_pos = pos;
+    prev_bin = binv;
+    piSm = iSm;
+    piSp = iSp;
+    piSf = iSf;
     pos = pos1;
     valid = valid1;
     pos1 = pos2;
     valid1 = valid2;
     src1 = src2;
     buf ^= 1;
+    p ^= 1;
     c = c == 2 ? 0 : c + 1;
   }
+  if (have_prev) flush(p ^ 1);
   vmax2_local = warp_max(vmax2_local);
   if ((tid & 31) == 0 && vmax2_local) atomicMax(&A.stS->vmax2_bits, vmax2_local);
 }
@@ -1123,7 +1150,7 @@ __global__ void k_pack_blocks(TableDev S, const float4* __restrict__ acc, int mo
     BlockRec& o = out[slot];
     if (lane == 0) {
       o.key = key;
-      o.mask = S.nodemask[r];
+      o.mask = 0;  // node activity travels in the accumulators (.w = contribution count)
     }
     for (int q = lane; q < 128; q += 32) o.v[q] = acc[size_t(r) * 128 + q];
   }
@@ -1140,7 +1167,6 @@ __global__ void k_unpack_blocks(TableDev S, float4* acc, const BlockRec* __restr
     uint32_t r = 0;
     if (lane == 0) {
       r = hash_insert(S.hv, in[i].key);
-      if (r < S.hv.cap_blocks) atomicOr((unsigned long long*)&S.nodemask[r], in[i].mask);
     }
     r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= S.hv.cap_blocks) {
@@ -1328,7 +1354,6 @@ int alloc_grid(smpm_sim* s) {
     DA(T.hv.slot_of_rank, cb);
     T.hv.mask = uint32_t(s->n_slots - 1);
     T.hv.cap_blocks = cb;
-    DA(T.nodemask, cb);
     DA(T.cell_count, size_t(cb) * 64);
     DA(T.cell_off, size_t(cb) * 64);
     DA(T.block_total, cb);
@@ -1339,7 +1364,6 @@ int alloc_grid(smpm_sim* s) {
     CK(cudaMemsetAsync(T.hv.keys, 0xFF, s->n_slots * 8, s->stream));
     CK(cudaMemsetAsync(T.hv.vals, 0xFF, s->n_slots * 4, s->stream));
     CK(cudaMemsetAsync(T.hv.counter, 0, 16, s->stream));
-    CK(cudaMemsetAsync(T.nodemask, 0, size_t(cb) * 8, s->stream));
     CK(cudaMemsetAsync(T.cell_count, 0, size_t(cb) * 64 * 4, s->stream));
   }
   DA(s->acc, size_t(cb) * 64 * 2);
@@ -1444,7 +1468,7 @@ int grow_grid(smpm_sim* s, uint32_t need) {
   std::vector<void*> grid_ptrs;
   for (int t = 0; t < 2; ++t) {
     TableDev& T = s->tab[t];
-    void* ps[] = {T.hv.keys, T.hv.vals, T.hv.counter, T.hv.active_keys, T.hv.slot_of_rank, T.nodemask,
+    void* ps[] = {T.hv.keys, T.hv.vals, T.hv.counter, T.hv.active_keys, T.hv.slot_of_rank,
                   T.cell_count, T.cell_off, T.block_total, T.block_items, T.nbr8, T.items, T.tile_sums};
     for (void* p : ps) grid_ptrs.push_back(p);
   }
@@ -1482,7 +1506,6 @@ int run_prologue(smpm_sim* s, int project) {
       CK(cudaMemsetAsync(T.hv.keys, 0xFF, s->n_slots * 8, s->stream));
       CK(cudaMemsetAsync(T.hv.vals, 0xFF, s->n_slots * 4, s->stream));
       CK(cudaMemsetAsync(T.hv.counter, 0, 16, s->stream));
-      CK(cudaMemsetAsync(T.nodemask, 0, size_t(s->cap_b) * 8, s->stream));
       CK(cudaMemsetAsync(T.cell_count, 0, size_t(s->cap_b) * 64 * 4, s->stream));
     }
     CK(cudaMemsetAsync(s->acc, 0, size_t(s->cap_b) * 64 * 32, s->stream));
@@ -1780,7 +1803,7 @@ int smpm_sim_step(smpm_sim* s, double dt) {
   CK(cudaEventRecord(s->ev[1], s->stream));
   GridParams gp = grid_params(s);
   k_grid<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
-                                         s->gv, gp, s->record);
+                                         s->gv, gp, s->record, s->bx0, s->bx1);
   CK(cudaGetLastError());
   CK(cudaEventRecord(s->ev[2], s->stream));
   rc = launch_fused(s, true, 1);
