@@ -76,10 +76,9 @@ struct TableDev {
   uint32_t* block_total; // [cap_b]
   uint32_t* block_items; // [cap_b]
   uint32_t* nbr8;        // [cap_b*8] ranks of blocks B + {0,1}^3 (gather arena)
-  uint2* items;          // [cap_items] (rank, group)
+  uint4* items;          // [cap_items] (rank, group, block key lo, hi)
   uint32_t* tile_sums;   // [3*max_tiles]
   uint32_t* done;        // last-CTA counter
-  uint32_t* item_next;   // persistent-kernel work counter
 };
 
 // Device-side per-table statistics (the step whose particles are binned in
@@ -216,7 +215,6 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
   }
   if (threadIdx.x == 0) {
     *S.done = 0;
-    *S.item_next = 0;
     DevStats* st = stS;
     st->n_blocks = nb;
     st->n_items = carry[1];
@@ -271,8 +269,10 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S) {
       }
       S.cell_off[size_t(rr) * 64 + lane] = boff[b] + x0 - c0;
       S.cell_off[size_t(rr) * 64 + 32 + lane] = boff[b] + sum0 + x1 - c1;
-      uint32_t nit = S.block_items[rr];
-      for (uint32_t g = lane; g < nit; g += 32) S.items[ioff[b] + g] = make_uint2(rr, g);
+      const uint32_t nit = S.block_items[rr];
+      const uint64_t key = S.hv.active_keys[rr];
+      for (uint32_t g = lane; g < nit; g += 32)
+        S.items[ioff[b] + g] = make_uint4(rr, g, uint32_t(key), uint32_t(key >> 32));
     }
     __syncthreads();
   }
@@ -408,10 +408,14 @@ struct FusedArgs {
   uint32_t mig_cap;
 };
 
-struct ItemInfo {
-  uint32_t r, g;
-  int b[3];
+struct __align__(16) ItemInfo {
+  uint4 raw;  // (rank, group, block key lo, hi); rank BAD_KEY: no item
   uint32_t nbr[8];
+  __device__ uint32_t r() const { return raw.x; }
+  __device__ uint32_t g() const { return raw.y; }
+  __device__ void block(int& b0, int& b1, int& b2) const {
+    unpack_key(uint64_t(raw.z) | (uint64_t(raw.w) << 32), b0, b1, b2);
+  }
 };
 
 // Item i scatters into arena X[i&1] while item i-1's arena X[(i-1)&1] is
@@ -512,16 +516,18 @@ __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float 
   atomicAdd(&A.S.cell_count[binv], 1u);
 }
 
-__device__ __forceinline__ void fetch_item(const FusedArgs& A, uint32_t n_items, ItemInfo& inf) {
-  uint32_t it = atomicAdd(A.B.item_next, 1u);
-  if (it < n_items) {
-    uint2 rg = A.B.items[it];
-    inf.r = rg.x;
-    inf.g = rg.y;
-    unpack_key(A.B.hv.active_keys[rg.x], inf.b[0], inf.b[1], inf.b[2]);
-  } else {
-    inf.r = BAD_KEY;
-  }
+// Static round-robin schedule: the k-th item of CTA b is item b + k * gridDim.
+// The 16-byte item record lands in the metadata ring by cp.async (async) or
+// a plain load (pipeline priming).
+__device__ __forceinline__ void fetch_item(const FusedArgs& A, uint32_t n_items, uint32_t k, ItemInfo& inf,
+                                           bool async) {
+  const uint32_t it = blockIdx.x + k * gridDim.x;
+  if (it >= n_items)
+    inf.raw = make_uint4(BAD_KEY, 0u, 0u, 0u);
+  else if (async)
+    cp_async16(&inf.raw, &A.B.items[it]);
+  else
+    inf.raw = A.B.items[it];
 }
 
 // sorted position of this thread's particle in item (r, g); returns validity
@@ -595,27 +601,28 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   // ---- prime the pipeline: records of item 0, indices of item 1, metadata
   // of item 2.  In steady state item i computes while item i+1's records and
   // velocity arena are in flight and item i+2's indices are being loaded.
-  if (tid == 0) fetch_item(A, n_items, sm.info[0]);
+  if (tid == 0) fetch_item(A, n_items, 0, sm.info[0], false);
   __syncthreads();
   uint32_t pos = 0, pos1 = 0, src1 = 0;
   bool valid = false, valid1 = false;
   {
     const ItemInfo& i0 = sm.info[0];
-    if (GATHER && tid < 8 && i0.r != BAD_KEY) sm.info[0].nbr[tid] = A.B.nbr8[size_t(i0.r) * 8 + tid];
-    valid = item_slot(A, i0.r, i0.g, tid, pos);
+    if (GATHER && tid < 8 && i0.r() != BAD_KEY) sm.info[0].nbr[tid] = A.B.nbr8[size_t(i0.r()) * 8 + tid];
+    valid = item_slot(A, i0.r(), i0.g(), tid, pos);
     if (valid) prefetch_record<GATHER>(sm, A, tid, A.perm[pos]);
-    if (tid == 0) fetch_item(A, n_items, sm.info[1]);
+    if (tid == 0) fetch_item(A, n_items, 1, sm.info[1], false);
   }
   __syncthreads();
   {
     const ItemInfo& i1 = sm.info[1];
-    valid1 = item_slot(A, i1.r, i1.g, tid, pos1);
+    valid1 = item_slot(A, i1.r(), i1.g(), tid, pos1);
     if (valid1) src1 = A.perm[pos1];
-    if (tid == 0) fetch_item(A, n_items, sm.info[2]);
+    if (tid == 0) fetch_item(A, n_items, 2, sm.info[2], false);
   }
-  if (GATHER && sm.info[0].r != BAD_KEY) prefetch_arena(sm, A, sm.info[0], 0, tid);
+  if (GATHER && sm.info[0].r() != BAD_KEY) prefetch_arena(sm, A, sm.info[0], 0, tid);
   cp_async_commit();
   int buf = 0, c = 0, p = 0;
+  uint32_t kf = 3;  // schedule index of the next item to fetch
   bool have_prev = false;
   // bin of this thread's particle of item i-1: kind 0 none, 1 final value
   // prev_bin, 2 arena cell (packed ab) resolved with rank[p^1]
@@ -669,9 +676,10 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     const ItemInfo& cur = sm.info[c];
     const ItemInfo& nxt = sm.info[c == 2 ? 0 : c + 1];
     const ItemInfo& nn = sm.info[c == 0 ? 2 : c - 1];
-    const uint32_t r = cur.r;
+    const uint32_t r = cur.r();
     if (r == BAD_KEY) break;
-    const int B0 = cur.b[0], B1 = cur.b[1], B2 = cur.b[2];
+    int B0, B1, B2;
+    cur.block(B0, B1, B2);
     // X[p] was flushed during the previous iteration: zero it for item i
     {
       int4* z = reinterpret_cast<int4*>(&sm.acc[p][0][0]);
@@ -679,8 +687,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
       if (tid < 3) sm.bmax[p ^ 1][tid] = 0;
       if (tid == 3) sm.touched[p ^ 1] = 0;
     }
-    if (GATHER && tid < 8 && nxt.r != BAD_KEY)
-      sm.info[c == 2 ? 0 : c + 1].nbr[tid] = A.B.nbr8[size_t(nxt.r) * 8 + tid];
+    if (GATHER && tid < 8 && nxt.r() != BAD_KEY)
+      sm.info[c == 2 ? 0 : c + 1].nbr[tid] = A.B.nbr8[size_t(nxt.r()) * 8 + tid];
     // this item's record -> registers, then the stage slot takes item i+1's
     float4 c0, c1, c2, c3, c4, c5, c6, c7;
     if (valid) {
@@ -922,13 +930,17 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
       }
     }
     __syncthreads();  // [B2] bounds, touched blocks and bin counts of item i
-    if (GATHER && nxt.r != BAD_KEY) prefetch_arena(sm, A, nxt, buf ^ 1, tid);
+    if (GATHER && nxt.r() != BAD_KEY) prefetch_arena(sm, A, nxt, buf ^ 1, tid);
+    // item i+3's metadata goes into this item's ring slot (its fields are in
+    // registers; nobody reads the slot after [B2])
+    if (tid == 0) fetch_item(A, n_items, kf, sm.info[c], true);
     cp_async_commit();
     // item i+2: raw index loads now, consumed after the scatter
-    const uint32_t key2 = nn.r == BAD_KEY ? 0u : nn.r * 64 + (tid & 63);
-    const uint32_t slot2 = nn.g * SLOTS + (tid >> 6);
+    const uint32_t nnr = nn.r();
+    const uint32_t key2 = nnr == BAD_KEY ? 0u : nnr * 64 + (tid & 63);
+    const uint32_t slot2 = nn.g() * SLOTS + (tid >> 6);
     uint32_t cnt2 = 0, off2 = 0;
-    if (nn.r != BAD_KEY) {
+    if (nnr != BAD_KEY) {
       cnt2 = A.B.cell_count[key2];
       off2 = A.B.cell_off[key2];
     }
@@ -1022,14 +1034,12 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     }
     // item i+2's sorted position and source index (consumed one item later)
     uint32_t pos2 = 0, src2 = 0;
-    const bool valid2 = nn.r != BAD_KEY && slot2 < cnt2;
+    const bool valid2 = nnr != BAD_KEY && slot2 < cnt2;
     if (valid2) {
       pos2 = off2 - cnt2 + slot2;  // k_bin advanced cell_off to the cell's end
       src2 = A.perm[pos2];
     }
-    // ---- rotate: item i+3's metadata goes into this item's ring slot (warp 0
-    // has finished reading it; the other warps read it before [B2])
-    if (tid == 0) fetch_item(A, n_items, sm.info[c]);
+    ++kf;
     have_prev = true;
     prev_kind = kind;
     prev_pos = pos;
@@ -1349,7 +1359,6 @@ int alloc_grid(smpm_sim* s) {
     DA(T.hv.counter, 4);
     T.hv.overflow = T.hv.counter + 1;
     T.done = T.hv.counter + 2;
-    T.item_next = T.hv.counter + 3;
     DA(T.hv.active_keys, cb);
     DA(T.hv.slot_of_rank, cb);
     T.hv.mask = uint32_t(s->n_slots - 1);
