@@ -734,73 +734,76 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
           bspline(d[a], w[a], g[a]);
           lb[a] = bs - 4 * (a == 0 ? B0 : (a == 1 ? B1 : B2));
         }
-        float v0 = 0, v1 = 0, v2 = 0;
-        float b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
-        float a00 = 0, a01 = 0, a02 = 0, a10 = 0, a11 = 0, a12 = 0, a20 = 0, a21 = 0, a22 = 0;
+        // Packed fp32x2 (FFMA2, one issue slot for two FMAs; scalar operands
+        // broadcast): per node S = sum_k w_k q, T = sum_k w_k (k - d_z) q,
+        // U = sum_k g_k q as (x, y) pairs plus z parts; per (i, j) the seven
+        // weights wij, wij (i - d_x), wij (j - d_y), Ax, Ay (and wij for T, U)
+        // accumulate v, B = sum w q dx^T / h and a = sum q grad w^T h.
         const float4* ga = sm.garena[buf];
-        float wzd[3];
+        float2 Pz[3];  // (w_k, w_k (k - d_z))
 #pragma unroll
-        for (int k = 0; k < 3; ++k) wzd[k] = w[2][k] * (float(k) - d[2]);
+        for (int k = 0; k < 3; ++k) Pz[k] = make_float2(w[2][k], w[2][k] * (float(k) - d[2]));
+        float2 P0[3], GW0[3], W1D[3];  // (w0, w0 (i - dx)), (g0, w0), (w1, w1 (j - dy))
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+          P0[o] = make_float2(w[0][o], w[0][o] * (float(o) - d[0]));
+          GW0[o] = make_float2(g[0][o], w[0][o]);
+          W1D[o] = make_float2(w[1][o], w[1][o] * (float(o) - d[1]));
+        }
+        const float2 Z2 = make_float2(0.f, 0.f);
+        float2 Vxy = Z2, B0 = Z2, B1 = Z2, B2 = Z2, A0 = Z2, A1 = Z2, A2 = Z2;  // (.0, .1) components
+        float2 VB = Z2, AB = Z2, BA = Z2;  // (v2, b20), (a20, b21), (b22, a22)
+        float a21 = 0.f;
 #pragma unroll
         for (int oi = 0; oi < 3; ++oi) {
 #pragma unroll
           for (int oj = 0; oj < 3; ++oj) {
-            float S0 = 0, S1 = 0, S2 = 0, T0 = 0, T1 = 0, T2 = 0, U0 = 0, U1 = 0, U2 = 0;
+            float2 Sxy = Z2, Txy = Z2, Uxy = Z2, TU2 = Z2;
+            float S2 = 0.f;
             const int gi = lb[0] + oi, gj = lb[1] + oj;
 #pragma unroll
             for (int ok = 0; ok < 3; ++ok) {
               const float4 q = ga[gaddr(gi, gj, lb[2] + ok)];
-              S0 += w[2][ok] * q.x;
-              S1 += w[2][ok] * q.y;
-              S2 += w[2][ok] * q.z;
-              T0 += wzd[ok] * q.x;
-              T1 += wzd[ok] * q.y;
-              T2 += wzd[ok] * q.z;
-              U0 += g[2][ok] * q.x;
-              U1 += g[2][ok] * q.y;
-              U2 += g[2][ok] * q.z;
+              const float2 qxy = make_float2(q.x, q.y);
+              Sxy = __ffma2_rn(qxy, make_float2(Pz[ok].x, Pz[ok].x), Sxy);
+              Txy = __ffma2_rn(qxy, make_float2(Pz[ok].y, Pz[ok].y), Txy);
+              Uxy = __ffma2_rn(qxy, make_float2(g[2][ok], g[2][ok]), Uxy);
+              TU2 = __ffma2_rn(make_float2(q.z, q.z), make_float2(Pz[ok].y, g[2][ok]), TU2);
+              S2 = fmaf(q.z, Pz[ok].x, S2);
             }
-            float wij = w[0][oi] * w[1][oj];
-            float dxi = wij * (float(oi) - d[0]), dyj = wij * (float(oj) - d[1]);
-            float Ax = g[0][oi] * w[1][oj], Ay = w[0][oi] * g[1][oj];
-            v0 += wij * S0;
-            v1 += wij * S1;
-            v2 += wij * S2;
-            b00 += dxi * S0;
-            b10 += dxi * S1;
-            b20 += dxi * S2;
-            b01 += dyj * S0;
-            b11 += dyj * S1;
-            b21 += dyj * S2;
-            b02 += wij * T0;
-            b12 += wij * T1;
-            b22 += wij * T2;
-            a00 += Ax * S0;
-            a10 += Ax * S1;
-            a20 += Ax * S2;
-            a01 += Ay * S0;
-            a11 += Ay * S1;
-            a21 += Ay * S2;
-            a02 += wij * U0;
-            a12 += wij * U1;
-            a22 += wij * U2;
+            const float2 WD = __fmul2_rn(P0[oi], make_float2(w[1][oj], w[1][oj]));  // (wij, dxi)
+            const float2 AD = __fmul2_rn(GW0[oi], W1D[oj]);                         // (Ax, dyj)
+            const float wij = WD.x, Ay = w[0][oi] * g[1][oj];
+            Vxy = __ffma2_rn(Sxy, make_float2(wij, wij), Vxy);
+            B0 = __ffma2_rn(Sxy, make_float2(WD.y, WD.y), B0);
+            B1 = __ffma2_rn(Sxy, make_float2(AD.y, AD.y), B1);
+            B2 = __ffma2_rn(Txy, make_float2(wij, wij), B2);
+            A0 = __ffma2_rn(Sxy, make_float2(AD.x, AD.x), A0);
+            A1 = __ffma2_rn(Sxy, make_float2(Ay, Ay), A1);
+            A2 = __ffma2_rn(Uxy, make_float2(wij, wij), A2);
+            VB = __ffma2_rn(make_float2(S2, S2), WD, VB);
+            AB = __ffma2_rn(make_float2(S2, S2), AD, AB);
+            BA = __ffma2_rn(TU2, make_float2(wij, wij), BA);
+            a21 = fmaf(Ay, S2, a21);
           }
         }
+        const float v0 = Vxy.x, v1 = Vxy.y, v2 = VB.x;
         const float cs = 4.0f * ih;  // C = B * 4/h^2 with dx = h * (o - d)
-        Cn[0] = b00 * cs;
-        Cn[1] = b01 * cs;
-        Cn[2] = b02 * cs;
-        Cn[3] = b10 * cs;
-        Cn[4] = b11 * cs;
-        Cn[5] = b12 * cs;
-        Cn[6] = b20 * cs;
-        Cn[7] = b21 * cs;
-        Cn[8] = b22 * cs;
+        Cn[0] = B0.x * cs;
+        Cn[1] = B1.x * cs;
+        Cn[2] = B2.x * cs;
+        Cn[3] = B0.y * cs;
+        Cn[4] = B1.y * cs;
+        Cn[5] = B2.y * cs;
+        Cn[6] = VB.y * cs;
+        Cn[7] = AB.y * cs;
+        Cn[8] = BA.x * cs;
         vn[0] = v0;
         vn[1] = v1;
         vn[2] = v2;
         const float dth = float(dt) * ih;  // a = (sum v g) / h
-        float A9[9] = {a00 * dth, a01 * dth, a02 * dth, a10 * dth, a11 * dth, a12 * dth, a20 * dth, a21 * dth, a22 * dth};
+        float A9[9] = {A0.x * dth, A1.x * dth, A2.x * dth, A0.y * dth, A1.y * dth, A2.y * dth,
+                       AB.x * dth, a21 * dth,  BA.y * dth};
         // F <- (I + dt a) F on H = F - I:  H <- H + dt a + dt a H
         float Fn[9];
 #pragma unroll
@@ -970,18 +973,23 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
 #pragma unroll
       for (int a = 0; a < 3; ++a) bspline(d1[a], w[a], g[a]);
       const int ad0 = aaddr(ab[0], ab[1], ab[2]);
-      const float mSm = m * Sm, mSp = m * Sp;
+      // packed fp32x2 where two fields share an operation (FFMA2, scalar
+      // operands broadcast); the magic add is folded into each product
+      const float2 mS = make_float2(m * Sm, m * Sp);
       // force: f = -(M grad w); grad w = (g0 w1 w2, w0 g1 w2, w0 w1 g2)/h
       const float fs = -Sf * ih;
       const float Mh[6] = {M[0] * fs, M[1] * fs, M[2] * fs, M[3] * fs, M[4] * fs, M[5] * fs};
-      float cz[3][3];  // h * C_d2 * (ok - d2)
+      const float2 MhA = make_float2(Mh[0], Mh[3]), MhB = make_float2(Mh[3], Mh[1]), MhC = make_float2(Mh[4], Mh[5]);
+      const float2 V01 = make_float2(vn[0], vn[1]), C03 = make_float2(Cn[0], Cn[3]), C14 = make_float2(Cn[1], Cn[4]);
+      float2 cz01[3];  // h (C_02, C_12) (k - d2)
+      float cz2[3];    // h C_22 (k - d2)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        float dz = (float(k) - d1[2]) * hf_;
-        cz[0][k] = Cn[2] * dz;
-        cz[1][k] = Cn[5] * dz;
-        cz[2][k] = Cn[8] * dz;
+        const float dz = (float(k) - d1[2]) * hf_;
+        cz01[k] = __fmul2_rn(make_float2(Cn[2], Cn[5]), make_float2(dz, dz));
+        cz2[k] = Cn[8] * dz;
       }
+      const float2 MG2 = make_float2(MAGIC, MAGIC), M0 = make_float2(MAGIC, 0.f);
       int* a0 = &sm.acc[p][0][ad0];
 #pragma unroll
       for (int oi = 0; oi < 3; ++oi) {
@@ -990,26 +998,29 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
         for (int oj = 0; oj < 3; ++oj) {
           const float dy = (float(oj) - d1[1]) * hf_;
           const float wij = w[0][oi] * w[1][oj];
-          const float q0 = vn[0] + Cn[0] * dx + Cn[1] * dy;
-          const float q1 = vn[1] + Cn[3] * dx + Cn[4] * dy;
+          const float2 q01 = __ffma2_rn(C14, make_float2(dy, dy), __ffma2_rn(C03, make_float2(dx, dx), V01));
           const float q2 = vn[2] + Cn[6] * dx + Cn[7] * dy;
           const float Ax = g[0][oi] * w[1][oj], Ay = w[0][oi] * g[1][oj];
-          const float r0 = Mh[0] * Ax + Mh[3] * Ay, s0 = Mh[4] * wij;
-          const float r1 = Mh[3] * Ax + Mh[1] * Ay, s1 = Mh[5] * wij;
+          const float2 r01 = __ffma2_rn(MhB, make_float2(Ay, Ay), __fmul2_rn(MhA, make_float2(Ax, Ax)));
+          const float2 s01 = __fmul2_rn(MhC, make_float2(wij, wij));
           const float r2 = Mh[4] * Ax + Mh[5] * Ay, s2 = Mh[2] * wij;
-          const float wmm = wij * mSm, wmp = wij * mSp;
+          const float2 wm = __fmul2_rn(mS, make_float2(wij, wij));  // (wij m Sm, wij m Sp)
 #pragma unroll
           for (int ok2 = 0; ok2 < 3; ++ok2) {
             const int o = aaddr(oi, oj, ok2);
             const float wz = w[2][ok2], gz = g[2][ok2];
-            const float cmz = wmp * wz;
-            sred(a0 + o, magic_q(fmaf(wmm, wz, MAGIC)));
-            sred(a0 + 1 * SCAT_N + o, magic_q(fmaf(cmz, q0 + cz[0][ok2], MAGIC)));
-            sred(a0 + 2 * SCAT_N + o, magic_q(fmaf(cmz, q1 + cz[1][ok2], MAGIC)));
-            sred(a0 + 3 * SCAT_N + o, magic_q(fmaf(cmz, q2 + cz[2][ok2], MAGIC)));
-            sred(a0 + 4 * SCAT_N + o, magic_q(fmaf(wz, r0, fmaf(gz, s0, MAGIC))));
-            sred(a0 + 5 * SCAT_N + o, magic_q(fmaf(wz, r1, fmaf(gz, s1, MAGIC))));
-            sred(a0 + 6 * SCAT_N + o, magic_q(fmaf(wz, r2, fmaf(gz, s2, MAGIC))));
+            const float2 mc = __ffma2_rn(wm, make_float2(wz, wz), M0);  // (mass + MAGIC, momentum weight)
+            const float2 m01 = __ffma2_rn(make_float2(mc.y, mc.y), __fadd2_rn(q01, cz01[ok2]), MG2);
+            const float m2 = fmaf(mc.y, q2 + cz2[ok2], MAGIC);
+            const float2 f01 = __ffma2_rn(make_float2(wz, wz), r01, __ffma2_rn(make_float2(gz, gz), s01, MG2));
+            const float f2 = fmaf(wz, r2, fmaf(gz, s2, MAGIC));
+            sred(a0 + o, magic_q(mc.x));
+            sred(a0 + 1 * SCAT_N + o, magic_q(m01.x));
+            sred(a0 + 2 * SCAT_N + o, magic_q(m01.y));
+            sred(a0 + 3 * SCAT_N + o, magic_q(m2));
+            sred(a0 + 4 * SCAT_N + o, magic_q(f01.x));
+            sred(a0 + 5 * SCAT_N + o, magic_q(f01.y));
+            sred(a0 + 6 * SCAT_N + o, magic_q(f2));
             sred(a0 + 7 * SCAT_N + o, 1);
           }
         }
