@@ -335,7 +335,7 @@ __device__ __forceinline__ void sym_mul(const float a[6], const float b[6], floa
 // Same model without an eigen-decomposition, for small elastic strain
 // (||B - I||_inf <= 0.05, the normal case: Drucker-Prager keeps elastic
 // strains small).  Hencky strain eps = 1/2 log(B), B = F F^T = I + X, as a
-// 7-term series (truncation < 0.05^8/8 relative); the return map is isotropic
+// 5-term series (truncation < 0.05^6/6); the return map is isotropic
 // so it acts on the tensor (deviator norm = Frobenius norm = principal norm,
 // materials.py:147-166); tau = 2 mu eps' + lam tr(eps') I equals
 // sum_k t_k u_k u_k^T of materials.py:233-238; and since eps' is a polynomial
@@ -358,16 +358,18 @@ __device__ inline bool hencky_dp(float H[9], const Material& mat, bool project, 
   const float nx = fmaxf(fabsf(X[0]) + fabsf(X[3]) + fabsf(X[4]),
                          fmaxf(fabsf(X[3]) + fabsf(X[1]) + fabsf(X[5]), fabsf(X[4]) + fabsf(X[5]) + fabsf(X[2])));
   if (!(nx <= 0.05f)) return hencky_dp_eig(H, mat, project, tau, J);
-  // log(I + X) = X (1 - X (1/2 - X (1/3 - X (1/4 - X (1/5 - X (1/6 - X/7))))))  (Horner)
+  // log(I + X) = X (1 - X (1/2 - X (1/3 - X (1/4 - X/5))))  (Horner); for
+  // ||X|| <= 0.05 the truncation is < 0.05^6/6 = 2.6e-9, below fp32 rounding
+  // of the strains (~1e-8 absolute)
   float P[6], T[6];
-  const float coef[6] = {1.f / 6.f, 1.f / 5.f, 1.f / 4.f, 1.f / 3.f, 1.f / 2.f, 1.f};
+  const float coef[4] = {1.f / 4.f, 1.f / 3.f, 1.f / 2.f, 1.f};
 #pragma unroll
-  for (int q = 0; q < 6; ++q) P[q] = -X[q] * (1.f / 7.f);
+  for (int q = 0; q < 6; ++q) P[q] = -X[q] * (1.f / 5.f);
   P[0] += coef[0];
   P[1] += coef[0];
   P[2] += coef[0];
 #pragma unroll
-  for (int it = 1; it < 6; ++it) {
+  for (int it = 1; it < 4; ++it) {
     sym_mul(X, P, T);
 #pragma unroll
     for (int q = 0; q < 6; ++q) P[q] = -T[q];
