@@ -36,6 +36,11 @@ namespace smpm {
 // stencil offset the 32 lanes hit 32 distinct banks (68 = 4 mod 32); measured
 // 29 lane-atomics/clk/SM vs 8.6 for a naive layout
 // (profiles/r01_ubench_atomics.md).
+// SMPM_DIAG_SKIP (timing ablation only, wrong results): 1 stress, 2 shared reductions of the
+// scatter, 4 global reductions of the flush, 8 gather loads
+#ifndef SMPM_DIAG_SKIP
+#define SMPM_DIAG_SKIP 0
+#endif
 #ifndef SMPM_MINB
 #define SMPM_MINB 2  // resident CTAs per SM the fused kernel is register-budgeted for
 #endif
@@ -44,7 +49,7 @@ constexpr int SCAT_N = 8 * AI;   // scatter arena: nodes 4B-1 .. 4B+6 per axis
 constexpr int NF = 7;            // m, p0..2, f0..2
 constexpr int NA = NF + 1;       // + contribution count K
 constexpr int CTA = 256;         // 64 cells x 4 slots
-constexpr int SLOTS = 4;
+constexpr int ISLOTS = 8;     // particle slots per cell per work item (2 per thread)
 constexpr uint32_t MAGIC_BITS = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float MAGIC = 12582912.0f;
 constexpr uint32_t BAD_KEY = 0xFFFFFFFFu;  // bin of a hole (departed particle) or an invalid one
@@ -94,6 +99,8 @@ struct DevStats {
   uint32_t n_owned;         // blocks inside this rank's slab
   uint32_t pad2;
   unsigned long long n_active;
+  uint32_t bnd_bits[3];     // maxima of the P2G contribution bounds (mass, momentum, force) into this table
+  uint32_t scale_ovf;       // a contribution exceeded the fixed-point scale: replay the P2G
   double dt;
   double mass_sum, mom_sum[3];
 };
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
       if (r >= nb) break;
       uint32_t c0 = S.cell_count[size_t(r) * 64 + lane], c1 = S.cell_count[size_t(r) * 64 + 32 + lane];
       uint32_t tot = warp_sum(c0 + c1), mx = warp_max(max(c0, c1));
-      uint32_t items = (mx + SLOTS - 1) / SLOTS;
+      uint32_t items = (mx + ISLOTS - 1) / ISLOTS;
       // neighbour ranks for the gather arena of this block's work items
       if (lane < 8 && items) {
         int bi, bj, bk;
@@ -231,6 +238,8 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
     *T.hv.counter = 0;
     *T.hv.overflow = 0;
     stT->vmax2_bits = 0;
+    stT->bnd_bits[0] = stT->bnd_bits[1] = stT->bnd_bits[2] = 0;
+    stT->scale_ovf = 0;
   }
 }
 
@@ -399,8 +408,11 @@ struct FusedArgs {
   double h, inv_h;
   const DevStats* stB;
   DevStats* stS;
+  const uint32_t* scale_src;  // contribution bounds (m, p, f) the fixed-point scales derive from
+  uint32_t* bnd_dst;          // maxima of this launch's contribution bounds
   unsigned long long* err;
   int project;
+  int measure;                // 1: bounds only (prologue pass 1), nothing is written
   // slab decomposition (multi-GPU): this rank owns base blocks bx in [bx0, bx1)
   int bx0, bx1;
   float4* mig[2];        // departing particle records (left, right)
@@ -418,25 +430,35 @@ struct __align__(16) ItemInfo {
   }
 };
 
+constexpr int GCH = 5;                      // record chunks G2P reads (x, m, V0, H, pid|mat)
+constexpr uint32_t NOPOS = 0xFFFFFFFFu;     // thread has no particle in this slot
+constexpr uint32_t BIN_SKIP = 0xFFFFFFFDu;  // no bin to write
+constexpr uint32_t BIN_ARENA = 0x80000000u; // | packed arena cell: resolved with the item's ranks
+constexpr float FX_LIM = 4194304.0f;        // 2^22: |contribution| * S (exact magic-add conversion)
+
 // Item i scatters into arena X[i&1] while item i-1's arena X[(i-1)&1] is
-// flushed; counts, bound maxima, touched-block masks and block ranks are
+// flushed; counts, touched-block masks, block ranks and pending bins are
 // double-buffered the same way (see the loop in k_g2p2g).
 struct __align__(16) FusedSmem {
-  float4 stage[CTA * 8];     // prefetched particle records (chunk c of thread t at t*8 + ((c+t)&7))
-  float4 garena[2][GATH_N];  // double-buffered velocity arena
-  int acc[2][NA][SCAT_N];    // fixed-point arenas (+ contribution count K)
-  uint32_t cnt[2][SCAT_N];   // particles per arena base cell (bin sizes)
-  uint32_t touched[2];       // 27-bit masks of the neighbour blocks the item's stencils touch
-  uint32_t rank[2][27];      // next-table ranks of those blocks
-  uint32_t bmax[2][3];       // contribution bounds (mass, momentum, force)
-  ItemInfo info[3];          // ring: items i, i+1, i+2
+  float4 stage[2][GCH][CTA];    // prefetched G2P chunks of the thread's two records (item i+1)
+  float4 garena[2][GATH_N];     // double-buffered velocity arena
+  int acc[2][NA][SCAT_N];       // fixed-point arenas (+ contribution count K)
+  uint32_t cnt[2][SCAT_N];      // particles per arena base cell (bin sizes)
+  uint32_t posr[3][2][CTA];     // sorted positions of the thread's two particles, ring like info
+  uint32_t binr[2][2][CTA];     // bins of the item awaiting its ranks
+  uint32_t touched[2];          // 27-bit masks of the neighbour blocks the item's stencils touch
+  uint32_t rank[2][27];         // next-table ranks of those blocks
+  float sc[6];                  // Sm, Sp, Sf and their inverses
+  ItemInfo info[3];             // ring: items i, i+1, i+2
   Material mats[8];
 };
 
 __device__ __forceinline__ void red_v4(float4* p, float a, float b, float c, float d) {
+  if (SMPM_DIAG_SKIP & 4) return;
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 __device__ __forceinline__ void sred(int* p, int v) {
+  if (SMPM_DIAG_SKIP & 2) return;
   asm volatile("red.shared.add.s32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -448,8 +470,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ int magic_q(float t) { return __float_as_int(t); }
 
-// power-of-two fixed-point scale for contributions bounded by b: b*S <= 2^22
-// (exact magic-add conversion) and 256 contributions fit in int32
+// power-of-two fixed-point scale for contributions bounded by b: b*S <= FX_LIM
+// (exact magic-add conversion).  A node's sum stays far inside int32: the
+// weights a node receives from the <= 8 particles per cell of an item sum to
+// ~ppc^3 = 8 (<= 43 in the worst arrangement), each term <= 8 w FX_LIM.
 __device__ __forceinline__ float fx_scale(float b, float& inv) {
   // b = f 2^e, f in [0.5, 1): e from the exponent field (b >= 0 finite)
   const int e = b > 0.f ? int((__float_as_uint(b) >> 23) & 0xFFu) - 126 : 0;
@@ -530,26 +554,6 @@ __device__ __forceinline__ void fetch_item(const FusedArgs& A, uint32_t n_items,
     inf.raw = A.B.items[it];
 }
 
-// sorted position of this thread's particle in item (r, g); returns validity
-__device__ __forceinline__ bool item_slot(const FusedArgs& A, uint32_t r, uint32_t g, int tid, uint32_t& pos) {
-  if (r == BAD_KEY) return false;
-  const uint32_t key = r * 64 + (tid & 63);
-  const uint32_t slot = g * SLOTS + (tid >> 6);
-  const uint32_t cnt = A.B.cell_count[key];
-  if (slot >= cnt) return false;
-  pos = A.B.cell_off[key] - cnt + slot;  // k_bin advanced cell_off to the cell's end
-  return true;
-}
-
-template <bool GATHER>
-__device__ __forceinline__ void prefetch_record(FusedSmem& sm, const FusedArgs& A, int tid, uint32_t src) {
-  const float4* g = A.src.rec + size_t(src) * 8;
-  float4* st = &sm.stage[tid * 8];
-  constexpr int NC = GATHER ? 5 : 8;
-#pragma unroll
-  for (int c = 0; c < NC; ++c) cp_async16(&st[(c + tid) & 7], &g[c]);
-}
-
 __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A, const ItemInfo& inf, int buf,
                                                int tid) {
   for (int n = tid; n < 216; n += CTA) {
@@ -563,82 +567,120 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
   }
 }
 
-// One persistent CTA works through items (block, group of SLOTS particles per
-// cell), 256 threads = 64 cells x 4 slots.  Item i, parity p = i & 1:
+// One persistent CTA works through items = (block, group of ISLOTS particles
+// per cell); thread t owns cell t & 63 and slots s, s + 4 (s = t >> 6) of the
+// group: two particles, processed one after the other.  A full block of
+// ppc^3 = 8 particles per cell is one item.  Item i, parity p = i & 1:
 //   [B1]  records / velocity arena of item i have landed; item i-1 is fully
 //         scattered into X[p^1] and its blocks are inserted (rank[p^1]).
-//   A     zero X[p]; G2P, F update, advection, stress of the next step, record
-//         store, next-step keys, contribution bounds, touched-block mask and
-//         bin counts of item i.
-//   [B2]  bounds / masks / counts of item i complete.
+//   A     zero X[p]; per particle: G2P, F update, advection, stress of the
+//         next step, record store, next-step keys, and the next step's P2G
+//         into X[p] in fixed point.  The scales are fixed before the launch
+//         from the previous launch's contribution maxima (x2 headroom); a
+//         particle that would exceed them flags the step for replay.
+//   [B2]  touched blocks and bin counts of item i complete.
 //   B     warp 0 probes the next table for item i's touched blocks; all
-//         threads scatter item i into X[p] (fixed point), then flush item i-1
-//         from X[p^1] (red.global.add.v4.f32; .w carries the contribution
-//         count K), write its bins and cell counts; warp 0 resolves item i's
-//         ranks into rank[p].
-// Two barriers per item; the hash-insert latency of item i is hidden behind
-// the flush of item i-1 (the flush of the last item runs after the loop).
+//         threads flush item i-1 from X[p^1] (red.global.add.v4.f32, .w = the
+//         contribution count K), write its bins and cell counts; warp 0
+//         resolves item i's ranks into rank[p].
 template <bool GATHER>
 __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
   FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smraw);
   const int tid = threadIdx.x;
+  const int cell = tid & 63, s0 = tid >> 6;
   for (int i = tid; i < A.n_mat && i < 8; i += CTA) sm.mats[i] = A.mats[i];
   const uint32_t n_items = A.stB->n_items;
   const double dt = GATHER ? A.stB->dt : 0.0;
   const float ih = float(A.inv_h);
   const float hf_ = float(A.h);
   uint32_t vmax2_local = 0;
+  float mx_m = 0.f, mx_p = 0.f, mx_f = 0.f;  // contribution bounds of this launch
+  bool scale_ovf = false;
+  if (tid < 3) {
+    const float b = A.measure ? 0.f : __uint_as_float(A.scale_src[tid]) * (tid == 0 ? 1.0f : 2.0f);
+    float inv;
+    const float S = fx_scale(b, inv);
+    sm.sc[tid] = S;
+    sm.sc[3 + tid] = inv;
+  }
   {
     int4* z = reinterpret_cast<int4*>(&sm.acc[0][0][0]);
     for (int i = tid; i < 2 * NA * SCAT_N / 4; i += CTA) z[i] = make_int4(0, 0, 0, 0);
     int4* zc = reinterpret_cast<int4*>(&sm.cnt[0][0]);
     for (int i = tid; i < 2 * SCAT_N / 4; i += CTA) zc[i] = make_int4(0, 0, 0, 0);
-    if (tid < 6) sm.bmax[tid / 3][tid % 3] = 0;
     if (tid < 2) sm.touched[tid] = 0;
   }
 
-  // ---- prime the pipeline: records of item 0, indices of item 1, metadata
+  // sorted positions of the thread's two particles of an item (NOPOS: none)
+  auto slots = [&](const ItemInfo& inf, uint32_t cnt, uint32_t off, int ring) {
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint32_t slot = inf.g() * ISLOTS + s0 + 4 * kk;
+      sm.posr[ring][kk][tid] = (inf.r() != BAD_KEY && slot < cnt) ? off - cnt + slot : NOPOS;
+    }
+  };
+  // ---- prime the pipeline: records of item 0, positions of item 1, metadata
   // of item 2.  In steady state item i computes while item i+1's records and
-  // velocity arena are in flight and item i+2's indices are being loaded.
+  // velocity arena are in flight and item i+2's positions are being loaded.
   if (tid == 0) fetch_item(A, n_items, 0, sm.info[0], false);
+  if (tid == 1) fetch_item(A, n_items, 1, sm.info[1], false);
+  if (tid == 2) fetch_item(A, n_items, 2, sm.info[2], false);
   __syncthreads();
-  uint32_t pos = 0, pos1 = 0, src1 = 0;
-  bool valid = false, valid1 = false;
+  uint32_t src1a = 0, src1b = 0;  // storage indices of item i+1's particles
   {
     const ItemInfo& i0 = sm.info[0];
+    const ItemInfo& i1 = sm.info[1];
     if (GATHER && tid < 8 && i0.r() != BAD_KEY) sm.info[0].nbr[tid] = A.B.nbr8[size_t(i0.r()) * 8 + tid];
-    valid = item_slot(A, i0.r(), i0.g(), tid, pos);
-    if (valid) prefetch_record<GATHER>(sm, A, tid, A.perm[pos]);
-    if (tid == 0) fetch_item(A, n_items, 1, sm.info[1], false);
+    uint32_t c0 = 0, o0 = 0, c1 = 0, o1 = 0;
+    if (i0.r() != BAD_KEY) {
+      c0 = A.B.cell_count[i0.r() * 64 + cell];
+      o0 = A.B.cell_off[i0.r() * 64 + cell];  // k_bin advanced cell_off to the cell's end
+    }
+    if (i1.r() != BAD_KEY) {
+      c1 = A.B.cell_count[i1.r() * 64 + cell];
+      o1 = A.B.cell_off[i1.r() * 64 + cell];
+    }
+    slots(i0, c0, o0, 0);
+    slots(i1, c1, o1, 1);
+    if (GATHER) {
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint32_t ps = sm.posr[0][kk][tid];
+        if (ps != NOPOS) {
+          const float4* g = A.src.rec + size_t(A.perm[ps]) * 8;
+#pragma unroll
+          for (int c = 0; c < GCH; ++c) cp_async16(&sm.stage[kk][c][tid], &g[c]);
+        }
+      }
+    }
+    const uint32_t pa = sm.posr[1][0][tid], pb = sm.posr[1][1][tid];
+    if (pa != NOPOS) src1a = A.perm[pa];
+    if (pb != NOPOS) src1b = A.perm[pb];
   }
   __syncthreads();
-  {
-    const ItemInfo& i1 = sm.info[1];
-    valid1 = item_slot(A, i1.r(), i1.g(), tid, pos1);
-    if (valid1) src1 = A.perm[pos1];
-    if (tid == 0) fetch_item(A, n_items, 2, sm.info[2], false);
-  }
   if (GATHER && sm.info[0].r() != BAD_KEY) prefetch_arena(sm, A, sm.info[0], 0, tid);
   cp_async_commit();
   int buf = 0, c = 0, p = 0;
   uint32_t kf = 3;  // schedule index of the next item to fetch
   bool have_prev = false;
-  // bin of this thread's particle of item i-1: kind 0 none, 1 final value
-  // prev_bin, 2 arena cell (packed ab) resolved with rank[p^1]
-  int prev_kind = 0;
-  uint32_t prev_pos = 0, prev_bin = 0;
-  float piSm = 0.f, piSp = 0.f, piSf = 0.f;
 
-  // flush of the item scattered into X[q] with ranks rank[q] (and its bins)
-  auto flush = [&](int q) {
-    if (prev_kind == 1) {
-      A.bin_out[prev_pos] = prev_bin;
-    } else if (prev_kind == 2) {
-      const int a0 = int(prev_bin >> 6), a1 = int((prev_bin >> 3) & 7u), a2 = int(prev_bin & 7u);
-      const uint32_t rk = sm.rank[q][((a0 + 3) >> 2) * 9 + ((a1 + 3) >> 2) * 3 + ((a2 + 3) >> 2)];
-      const uint32_t lc = (((a0 + 3) & 3) << 4) | (((a1 + 3) & 3) << 2) | ((a2 + 3) & 3);
-      A.bin_out[prev_pos] = rk == BAD_KEY ? OVF_KEY : rk * 64 + lc;
+  // flush of the item scattered into X[q] with ranks rank[q] and its bins,
+  // positions from ring slot rq
+  auto flush = [&](int q, int rq) {
+    const float iSm = sm.sc[3], iSp = sm.sc[4], iSf = sm.sc[5];
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint32_t bv = sm.binr[q][kk][tid];
+      if (bv == BIN_SKIP) continue;
+      uint32_t out = bv;
+      if (bv >= BIN_ARENA && bv < BIN_ARENA + 512u) {
+        const int a0 = int((bv >> 6) & 7u), a1 = int((bv >> 3) & 7u), a2 = int(bv & 7u);
+        const uint32_t rk = sm.rank[q][((a0 + 3) >> 2) * 9 + ((a1 + 3) >> 2) * 3 + ((a2 + 3) >> 2)];
+        const uint32_t lc = (((a0 + 3) & 3) << 4) | (((a1 + 3) & 3) << 2) | ((a2 + 3) & 3);
+        out = rk == BAD_KEY ? OVF_KEY : rk * 64 + lc;
+      }
+      A.bin_out[sm.posr[rq][kk][tid]] = out;
     }
     for (int n = tid; n < 216; n += CTA) {
       const int i = n / 36, j = (n / 6) % 6, k = n % 6;
@@ -646,9 +688,9 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
       const uint32_t cc = sm.cnt[q][ad];
       if (cc) {
         sm.cnt[q][ad] = 0;
-        const uint32_t rq = sm.rank[q][((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
+        const uint32_t rq2 = sm.rank[q][((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
         const uint32_t lc = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
-        if (rq != BAD_KEY) atomicAdd(&A.S.cell_count[rq * 64 + lc], cc);
+        if (rq2 != BAD_KEY) atomicAdd(&A.S.cell_count[rq2 * 64 + lc], cc);
       }
     }
     // value = (sum - K * MAGIC_BITS) / S
@@ -665,8 +707,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
 #pragma unroll
       for (int f = 0; f < NF; ++f) vals[f] = float(int(uint32_t(sm.acc[q][f][ad]) - bias));
       const size_t node = size_t(rk) * 64 + l;
-      red_v4(&A.acc[2 * node], vals[0] * piSm, vals[1] * piSp, vals[2] * piSp, vals[3] * piSp);
-      red_v4(&A.acc[2 * node + 1], vals[4] * piSf, vals[5] * piSf, vals[6] * piSf, float(K));
+      red_v4(&A.acc[2 * node], vals[0] * iSm, vals[1] * iSp, vals[2] * iSp, vals[3] * iSp);
+      red_v4(&A.acc[2 * node + 1], vals[4] * iSf, vals[5] * iSf, vals[6] * iSf, float(K));
     }
   };
 
@@ -674,8 +716,9 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     cp_async_wait_all();
     __syncthreads();  // [B1]
     const ItemInfo& cur = sm.info[c];
-    const ItemInfo& nxt = sm.info[c == 2 ? 0 : c + 1];
-    const ItemInfo& nn = sm.info[c == 0 ? 2 : c - 1];
+    const int c1r = c == 2 ? 0 : c + 1, c2r = c == 0 ? 2 : c - 1;
+    const ItemInfo& nxt = sm.info[c1r];
+    const ItemInfo& nn = sm.info[c2r];
     const uint32_t r = cur.r();
     if (r == BAD_KEY) break;
     int B0, B1, B2;
@@ -684,275 +727,361 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     {
       int4* z = reinterpret_cast<int4*>(&sm.acc[p][0][0]);
       for (int i = tid; i < NA * SCAT_N / 4; i += CTA) z[i] = make_int4(0, 0, 0, 0);
-      if (tid < 3) sm.bmax[p ^ 1][tid] = 0;
       if (tid == 3) sm.touched[p ^ 1] = 0;
     }
-    if (GATHER && tid < 8 && nxt.r() != BAD_KEY)
-      sm.info[c == 2 ? 0 : c + 1].nbr[tid] = A.B.nbr8[size_t(nxt.r()) * 8 + tid];
-    // this item's record -> registers, then the stage slot takes item i+1's
-    float4 c0, c1, c2, c3, c4, c5, c6, c7;
-    if (valid) {
-      const float4* st = &sm.stage[tid * 8];
-      c0 = st[(0 + tid) & 7];
-      c1 = st[(1 + tid) & 7];
-      c2 = st[(2 + tid) & 7];
-      c3 = st[(3 + tid) & 7];
-      c4 = st[(4 + tid) & 7];
-      if (!GATHER) {
-        c5 = st[(5 + tid) & 7];
-        c6 = st[(6 + tid) & 7];
-        c7 = st[(7 + tid) & 7];
-      }
-    }
-    if (valid1) prefetch_record<GATHER>(sm, A, tid, src1);
+    if (GATHER && tid < 8 && nxt.r() != BAD_KEY) sm.info[c1r].nbr[tid] = A.B.nbr8[size_t(nxt.r()) * 8 + tid];
+    const float Sm = sm.sc[0], Sp = sm.sc[1], Sf = sm.sc[2];
+    uint32_t tmask = 0;
 
-    double xn[3];
-    float vn[3], Cn[9], M[6], m = 0.f, d1[3];
-    int nb[3], ab[3];
-    bool far = false, ok = valid;
-    int mig = -1;
-    float bm = 0.f, bp = 0.f, bf = 0.f;
-    uint32_t pidv = 0, tmask = 0;
-    if (valid) {
-      xn[0] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
-      xn[1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
-      xn[2] = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
-      m = c1.z;
-      const float V0 = c1.w;
-      float F[9] = {c2.x, c2.y, c2.z, c2.w, c3.x, c3.y, c3.z, c3.w, c4.x};
-      const uint32_t pm = __float_as_uint(c4.y);
-      pidv = pm & PID_MASK;
-      const int mt = int(pm >> 29);
+#pragma unroll 1
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint32_t pos = sm.posr[c][kk][tid];
+      const bool valid = pos != NOPOS;
+      // this item's record -> registers; the stage slot then takes item i+1's
+      float4 c0, c1, c2, c3, c4, c5, c6, c7;
+      if (valid) {
+        if (GATHER) {
+          c0 = sm.stage[kk][0][tid];
+          c1 = sm.stage[kk][1][tid];
+          c2 = sm.stage[kk][2][tid];
+          c3 = sm.stage[kk][3][tid];
+          c4 = sm.stage[kk][4][tid];
+        } else {
+          const float4* g = A.src.rec + size_t(A.perm[pos]) * 8;
+          c0 = g[0];
+          c1 = g[1];
+          c2 = g[2];
+          c3 = g[3];
+          c4 = g[4];
+          c5 = g[5];
+          c6 = g[6];
+          c7 = g[7];
+        }
+      }
       if (GATHER) {
-        // ---- G2P (solver.py:628-732) from the smem velocity arena
-        int lb[3];
-        float d[3], w[3][3], g[3][3];
+        const uint32_t p1 = sm.posr[c1r][kk][tid];
+        if (p1 != NOPOS) {
+          const float4* g = A.src.rec + size_t(kk ? src1b : src1a) * 8;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          int bs;
-          axis_base(xn[a], A.inv_h, bs, d[a]);
-          bspline(d[a], w[a], g[a]);
-          lb[a] = bs - 4 * (a == 0 ? B0 : (a == 1 ? B1 : B2));
+          for (int q = 0; q < GCH; ++q) cp_async16(&sm.stage[kk][q][tid], &g[q]);
         }
-        // Packed fp32x2 (FFMA2, one issue slot for two FMAs; scalar operands
-        // broadcast): per node S = sum_k w_k q, T = sum_k w_k (k - d_z) q,
-        // U = sum_k g_k q as (x, y) pairs plus z parts; per (i, j) the seven
-        // weights wij, wij (i - d_x), wij (j - d_y), Ax, Ay (and wij for T, U)
-        // accumulate v, B = sum w q dx^T / h and a = sum q grad w^T h.
-        const float4* ga = sm.garena[buf];
-        float2 Pz[3];  // (w_k, w_k (k - d_z))
+      }
+      uint32_t binv = BIN_SKIP;
+      if (valid) {
+        double xn[3];
+        float vn[3], Cn[9], M[6], d1[3];
+        int nb[3], ab[3];
+        bool ok = true, far = false, sovf = false;
+        int mig = -1;
+        xn[0] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
+        xn[1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
+        xn[2] = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
+        const float m = c1.z;
+        const float V0 = c1.w;
+        float F[9] = {c2.x, c2.y, c2.z, c2.w, c3.x, c3.y, c3.z, c3.w, c4.x};
+        const uint32_t pm = __float_as_uint(c4.y);
+        const uint32_t pidv = pm & PID_MASK;
+        const int mt = int(pm >> 29);
+        if (GATHER) {
+          // ---- G2P (solver.py:628-732) from the smem velocity arena.  The
+          // particle is binned by its base cell, so the block-local base is
+          // the thread's cell.
+          const int lb[3] = {cell >> 4, (cell >> 2) & 3, cell & 3};
+          float d[3], w[3][3], g[3][3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) Pz[k] = make_float2(w[2][k], w[2][k] * (float(k) - d[2]));
-        float2 P0[3], GW0[3], W1D[3];  // (w0, w0 (i - dx)), (g0, w0), (w1, w1 (j - dy))
+          for (int a = 0; a < 3; ++a) {
+            int bs;
+            axis_base(xn[a], A.inv_h, bs, d[a]);
+            bspline(d[a], w[a], g[a]);
+          }
+          // Packed fp32x2 (FFMA2, one issue slot for two FMAs; scalar operands
+          // broadcast): per node S = sum_k w_k q, T = sum_k w_k (k - d_z) q,
+          // U = sum_k g_k q as (x, y) pairs plus z parts; per (i, j) the seven
+          // weights wij, wij (i - d_x), wij (j - d_y), Ax, Ay (and wij for T, U)
+          // accumulate v, B = sum w q dx^T / h and a = sum q grad w^T h.
+          const float4* ga = sm.garena[buf];
+          float2 Pz[3];  // (w_k, w_k (k - d_z))
 #pragma unroll
-        for (int o = 0; o < 3; ++o) {
-          P0[o] = make_float2(w[0][o], w[0][o] * (float(o) - d[0]));
-          GW0[o] = make_float2(g[0][o], w[0][o]);
-          W1D[o] = make_float2(w[1][o], w[1][o] * (float(o) - d[1]));
-        }
-        const float2 Z2 = make_float2(0.f, 0.f);
-        float2 Vxy = Z2, B0 = Z2, B1 = Z2, B2 = Z2, A0 = Z2, A1 = Z2, A2 = Z2;  // (.0, .1) components
-        float2 VB = Z2, AB = Z2, BA = Z2;  // (v2, b20), (a20, b21), (b22, a22)
-        float a21 = 0.f;
+          for (int k = 0; k < 3; ++k) Pz[k] = make_float2(w[2][k], w[2][k] * (float(k) - d[2]));
+          float2 P0[3], GW0[3], W1D[3];  // (w0, w0 (i - dx)), (g0, w0), (w1, w1 (j - dy))
 #pragma unroll
-        for (int oi = 0; oi < 3; ++oi) {
+          for (int o = 0; o < 3; ++o) {
+            P0[o] = make_float2(w[0][o], w[0][o] * (float(o) - d[0]));
+            GW0[o] = make_float2(g[0][o], w[0][o]);
+            W1D[o] = make_float2(w[1][o], w[1][o] * (float(o) - d[1]));
+          }
+          const float2 Z2 = make_float2(0.f, 0.f);
+          float2 Vxy = Z2, Bx = Z2, By = Z2, Bz = Z2, Ax2 = Z2, Ay2 = Z2, Az2 = Z2;  // (.0, .1) components
+          float2 VB = Z2, AB = Z2, BA = Z2;  // (v2, b20), (a20, b21), (b22, a22)
+          float a21 = 0.f;
 #pragma unroll
-          for (int oj = 0; oj < 3; ++oj) {
-            float2 Sxy = Z2, Txy = Z2, Uxy = Z2, TU2 = Z2;
-            float S2 = 0.f;
-            const int gi = lb[0] + oi, gj = lb[1] + oj;
+          for (int oi = 0; oi < 3; ++oi) {
 #pragma unroll
-            for (int ok = 0; ok < 3; ++ok) {
-              const float4 q = ga[gaddr(gi, gj, lb[2] + ok)];
-              const float2 qxy = make_float2(q.x, q.y);
-              Sxy = __ffma2_rn(qxy, make_float2(Pz[ok].x, Pz[ok].x), Sxy);
-              Txy = __ffma2_rn(qxy, make_float2(Pz[ok].y, Pz[ok].y), Txy);
-              Uxy = __ffma2_rn(qxy, make_float2(g[2][ok], g[2][ok]), Uxy);
-              TU2 = __ffma2_rn(make_float2(q.z, q.z), make_float2(Pz[ok].y, g[2][ok]), TU2);
-              S2 = fmaf(q.z, Pz[ok].x, S2);
+            for (int oj = 0; oj < 3; ++oj) {
+              float2 Sxy = Z2, Txy = Z2, Uxy = Z2, TU2 = Z2;
+              float S2 = 0.f;
+              const int gi = lb[0] + oi, gj = lb[1] + oj;
+#pragma unroll
+              for (int ok = 0; ok < 3; ++ok) {
+                const float4 q = (SMPM_DIAG_SKIP & 8) ? make_float4(Pz[ok].x, gi, gj, 0.f)
+                                                      : ga[gaddr(gi, gj, lb[2] + ok)];
+                const float2 qxy = make_float2(q.x, q.y);
+                Sxy = __ffma2_rn(qxy, make_float2(Pz[ok].x, Pz[ok].x), Sxy);
+                Txy = __ffma2_rn(qxy, make_float2(Pz[ok].y, Pz[ok].y), Txy);
+                Uxy = __ffma2_rn(qxy, make_float2(g[2][ok], g[2][ok]), Uxy);
+                TU2 = __ffma2_rn(make_float2(q.z, q.z), make_float2(Pz[ok].y, g[2][ok]), TU2);
+                S2 = fmaf(q.z, Pz[ok].x, S2);
+              }
+              const float2 WD = __fmul2_rn(P0[oi], make_float2(w[1][oj], w[1][oj]));  // (wij, dxi)
+              const float2 AD = __fmul2_rn(GW0[oi], W1D[oj]);                         // (Ax, dyj)
+              const float wij = WD.x, Ay = w[0][oi] * g[1][oj];
+              Vxy = __ffma2_rn(Sxy, make_float2(wij, wij), Vxy);
+              Bx = __ffma2_rn(Sxy, make_float2(WD.y, WD.y), Bx);
+              By = __ffma2_rn(Sxy, make_float2(AD.y, AD.y), By);
+              Bz = __ffma2_rn(Txy, make_float2(wij, wij), Bz);
+              Ax2 = __ffma2_rn(Sxy, make_float2(AD.x, AD.x), Ax2);
+              Ay2 = __ffma2_rn(Sxy, make_float2(Ay, Ay), Ay2);
+              Az2 = __ffma2_rn(Uxy, make_float2(wij, wij), Az2);
+              VB = __ffma2_rn(make_float2(S2, S2), WD, VB);
+              AB = __ffma2_rn(make_float2(S2, S2), AD, AB);
+              BA = __ffma2_rn(TU2, make_float2(wij, wij), BA);
+              a21 = fmaf(Ay, S2, a21);
             }
-            const float2 WD = __fmul2_rn(P0[oi], make_float2(w[1][oj], w[1][oj]));  // (wij, dxi)
-            const float2 AD = __fmul2_rn(GW0[oi], W1D[oj]);                         // (Ax, dyj)
-            const float wij = WD.x, Ay = w[0][oi] * g[1][oj];
-            Vxy = __ffma2_rn(Sxy, make_float2(wij, wij), Vxy);
-            B0 = __ffma2_rn(Sxy, make_float2(WD.y, WD.y), B0);
-            B1 = __ffma2_rn(Sxy, make_float2(AD.y, AD.y), B1);
-            B2 = __ffma2_rn(Txy, make_float2(wij, wij), B2);
-            A0 = __ffma2_rn(Sxy, make_float2(AD.x, AD.x), A0);
-            A1 = __ffma2_rn(Sxy, make_float2(Ay, Ay), A1);
-            A2 = __ffma2_rn(Uxy, make_float2(wij, wij), A2);
-            VB = __ffma2_rn(make_float2(S2, S2), WD, VB);
-            AB = __ffma2_rn(make_float2(S2, S2), AD, AB);
-            BA = __ffma2_rn(TU2, make_float2(wij, wij), BA);
-            a21 = fmaf(Ay, S2, a21);
           }
+          const float cs = 4.0f * ih;  // C = B * 4/h^2 with dx = h * (o - d)
+          Cn[0] = Bx.x * cs;
+          Cn[1] = By.x * cs;
+          Cn[2] = Bz.x * cs;
+          Cn[3] = Bx.y * cs;
+          Cn[4] = By.y * cs;
+          Cn[5] = Bz.y * cs;
+          Cn[6] = VB.y * cs;
+          Cn[7] = AB.y * cs;
+          Cn[8] = BA.x * cs;
+          vn[0] = Vxy.x;
+          vn[1] = Vxy.y;
+          vn[2] = VB.x;
+          const float dth = float(dt) * ih;  // a = (sum v g) / h
+          float A9[9] = {Ax2.x * dth, Ay2.x * dth, Az2.x * dth, Ax2.y * dth, Ay2.y * dth,
+                         Az2.y * dth, AB.x * dth,  a21 * dth,   BA.y * dth};
+          // F <- (I + dt a) F on H = F - I:  H <- H + dt a + dt a H
+          float Fn[9];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+              Fn[3 * i + j] =
+                  F[3 * i + j] + (A9[3 * i + j] + (A9[3 * i] * F[j] + A9[3 * i + 1] * F[3 + j] + A9[3 * i + 2] * F[6 + j]));
+#pragma unroll
+          for (int q = 0; q < 9; ++q) F[q] = Fn[q];
+          xn[0] = __dadd_rn(xn[0], __dmul_rn(dt, double(vn[0])));
+          xn[1] = __dadd_rn(xn[1], __dmul_rn(dt, double(vn[1])));
+          xn[2] = __dadd_rn(xn[2], __dmul_rn(dt, double(vn[2])));
+        } else {
+          vn[0] = c4.z;
+          vn[1] = c4.w;
+          vn[2] = c5.x;
+          Cn[0] = c5.y;
+          Cn[1] = c5.z;
+          Cn[2] = c5.w;
+          Cn[3] = c6.x;
+          Cn[4] = c6.y;
+          Cn[5] = c6.z;
+          Cn[6] = c6.w;
+          Cn[7] = c7.x;
+          Cn[8] = c7.y;
         }
-        const float v0 = Vxy.x, v1 = Vxy.y, v2 = VB.x;
-        const float cs = 4.0f * ih;  // C = B * 4/h^2 with dx = h * (o - d)
-        Cn[0] = B0.x * cs;
-        Cn[1] = B1.x * cs;
-        Cn[2] = B2.x * cs;
-        Cn[3] = B0.y * cs;
-        Cn[4] = B1.y * cs;
-        Cn[5] = B2.y * cs;
-        Cn[6] = VB.y * cs;
-        Cn[7] = AB.y * cs;
-        Cn[8] = BA.x * cs;
-        vn[0] = v0;
-        vn[1] = v1;
-        vn[2] = v2;
-        const float dth = float(dt) * ih;  // a = (sum v g) / h
-        float A9[9] = {A0.x * dth, A1.x * dth, A2.x * dth, A0.y * dth, A1.y * dth, A2.y * dth,
-                       AB.x * dth, a21 * dth,  BA.y * dth};
-        // F <- (I + dt a) F on H = F - I:  H <- H + dt a + dt a H
-        float Fn[9];
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-            Fn[3 * i + j] =
-                F[3 * i + j] + (A9[3 * i + j] + (A9[3 * i] * F[j] + A9[3 * i + 1] * F[3 + j] + A9[3 * i + 2] * F[6 + j]));
-#pragma unroll
-        for (int q = 0; q < 9; ++q) F[q] = Fn[q];
-        xn[0] = __dadd_rn(xn[0], __dmul_rn(dt, double(v0)));
-        xn[1] = __dadd_rn(xn[1], __dmul_rn(dt, double(v1)));
-        xn[2] = __dadd_rn(xn[2], __dmul_rn(dt, double(v2)));
-      } else {
-        vn[0] = c4.z;
-        vn[1] = c4.w;
-        vn[2] = c5.x;
-        Cn[0] = c5.y;
-        Cn[1] = c5.z;
-        Cn[2] = c5.w;
-        Cn[3] = c6.x;
-        Cn[4] = c6.y;
-        Cn[5] = c6.z;
-        Cn[6] = c6.w;
-        Cn[7] = c7.x;
-        Cn[8] = c7.y;
-      }
-      // ---- stress of the next step (materials.py:169-238)
-      float tau[6], J;
-      const Material& mat = sm.mats[mt];
-      if (!hencky_dp(F, mat, A.project != 0, tau, J)) {
-        err_report(A.err, ERR_DEGENERATE_F, pidv);
-        ok = false;
-        tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = 0.f;
-      }
-#pragma unroll
-      for (int q = 0; q < 6; ++q) M[q] = V0 * tau[q];
-      // ---- write the particle record at its sorted position
-      {
-        float4* o = A.dst.rec + size_t(pos) * 8;
-        int2 x0 = make_int2(__double2loint(xn[0]), __double2hiint(xn[0]));
-        int2 x1 = make_int2(__double2loint(xn[1]), __double2hiint(xn[1]));
-        int2 x2 = make_int2(__double2loint(xn[2]), __double2hiint(xn[2]));
-        o[0] = make_float4(__int_as_float(x0.x), __int_as_float(x0.y), __int_as_float(x1.x), __int_as_float(x1.y));
-        o[1] = make_float4(__int_as_float(x2.x), __int_as_float(x2.y), m, V0);
-        o[2] = make_float4(F[0], F[1], F[2], F[3]);
-        o[3] = make_float4(F[4], F[5], F[6], F[7]);
-        o[4] = make_float4(F[8], __uint_as_float(pm), vn[0], vn[1]);
-        o[5] = make_float4(vn[2], Cn[0], Cn[1], Cn[2]);
-        o[6] = make_float4(Cn[3], Cn[4], Cn[5], Cn[6]);
-        o[7] = make_float4(Cn[7], Cn[8], 0.f, 0.f);
-      }
-      float vv = vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2];
-      vmax2_local = max(vmax2_local, __float_as_uint(vv));
-      // ---- next step's keys
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        if (!isfinite(xn[a])) {
-          if (ok) err_report(A.err, ERR_NONFINITE_X, pidv);
+        // ---- stress of the next step (materials.py:169-238)
+        float tau[6], J;
+        const Material& mat = sm.mats[mt];
+        if ((SMPM_DIAG_SKIP & 1) ? (tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = F[0] * 1e-3f, false)
+                                 : !hencky_dp(F, mat, A.project != 0 && !A.measure, tau, J)) {
+          if (!A.measure) err_report(A.err, ERR_DEGENERATE_F, pidv);
           ok = false;
-        } else if (!axis_base(xn[a], A.inv_h, nb[a], d1[a]) || !axis_in_key_range(nb[a])) {
-          if (ok) err_report(A.err, ERR_KEY_RANGE, pidv);
-          ok = false;
+          tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = 0.f;
         }
-      }
-      if (ok) {
-        ab[0] = nb[0] - (4 * B0 - 1);
-        ab[1] = nb[1] - (4 * B1 - 1);
-        ab[2] = nb[2] - (4 * B2 - 1);
-        far = ab[0] < 0 || ab[0] > 5 || ab[1] < 0 || ab[1] > 5 || ab[2] < 0 || ab[2] > 5;
-        const int nbx = nb[0] >> 2;
-        mig = nbx < A.bx0 ? 0 : (nbx >= A.bx1 ? 1 : -1);
-        if (mig >= 0) {
-          // leaves this rank's slab: still scattered here (P2G belongs to the
-          // step that moved it), binned by the neighbour
-          const uint32_t slot = atomicAdd(&A.mig_count[mig], 1u);
-          if (slot < A.mig_cap) {
-            const float4* src4 = A.dst.rec + size_t(pos) * 8;
-            float4* o4 = A.mig[mig] + size_t(slot) * 8;
 #pragma unroll
-            for (int c8 = 0; c8 < 8; ++c8) o4[c8] = src4[c8];
-          } else {
-            err_report(A.err, ERR_CAPACITY, pidv);
-          }
+        for (int q = 0; q < 6; ++q) M[q] = V0 * tau[q];
+        // ---- write the particle record at its sorted position
+        if (!A.measure) {
+          float4* o = A.dst.rec + size_t(pos) * 8;
+          int2 x0 = make_int2(__double2loint(xn[0]), __double2hiint(xn[0]));
+          int2 x1 = make_int2(__double2loint(xn[1]), __double2hiint(xn[1]));
+          int2 x2 = make_int2(__double2loint(xn[2]), __double2hiint(xn[2]));
+          o[0] = make_float4(__int_as_float(x0.x), __int_as_float(x0.y), __int_as_float(x1.x), __int_as_float(x1.y));
+          o[1] = make_float4(__int_as_float(x2.x), __int_as_float(x2.y), m, V0);
+          o[2] = make_float4(F[0], F[1], F[2], F[3]);
+          o[3] = make_float4(F[4], F[5], F[6], F[7]);
+          o[4] = make_float4(F[8], __uint_as_float(pm), vn[0], vn[1]);
+          o[5] = make_float4(vn[2], Cn[0], Cn[1], Cn[2]);
+          o[6] = make_float4(Cn[3], Cn[4], Cn[5], Cn[6]);
+          o[7] = make_float4(Cn[7], Cn[8], 0.f, 0.f);
         }
-        // contribution bounds: |w| <= prod_a max_o w_a(o); |grad w_a| <= max|g_a| prod_{b!=a} max w_b / h;
-        // |dx_a| <= h * max(d_a, 2 - d_a)
-        float wmax[3], gmax[3], dxm[3];
+        const float vv = vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2];
+        vmax2_local = max(vmax2_local, __float_as_uint(vv));
+        // ---- next step's keys
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          const float dd = d1[a];
-          const float w0 = 0.5f * (1.5f - dd) * (1.5f - dd), w1 = 0.75f - (dd - 1.f) * (dd - 1.f),
-                      w2 = 0.5f * (dd - 0.5f) * (dd - 0.5f);
-          wmax[a] = fmaxf(w0, fmaxf(w1, w2));
-          gmax[a] = fmaxf(fabsf(dd - 1.5f), fmaxf(fabsf(2.f * (dd - 1.f)), fabsf(dd - 0.5f)));
-          dxm[a] = hf_ * fmaxf(dd, 2.f - dd);
+          if (!isfinite(xn[a])) {
+            if (ok && !A.measure) err_report(A.err, ERR_NONFINITE_X, pidv);
+            ok = false;
+          } else if (!axis_base(xn[a], A.inv_h, nb[a], d1[a]) || !axis_in_key_range(nb[a])) {
+            if (ok && !A.measure) err_report(A.err, ERR_KEY_RANGE, pidv);
+            ok = false;
+          }
         }
-        const float W = wmax[0] * wmax[1] * wmax[2];
-        const float G0 = gmax[0] * wmax[1] * wmax[2] * ih, G1 = wmax[0] * gmax[1] * wmax[2] * ih,
-                    G2 = wmax[0] * wmax[1] * gmax[2] * ih;
-        float cm = 0.f;
+        if (ok) {
+          ab[0] = nb[0] - (4 * B0 - 1);
+          ab[1] = nb[1] - (4 * B1 - 1);
+          ab[2] = nb[2] - (4 * B2 - 1);
+          far = ab[0] < 0 || ab[0] > 5 || ab[1] < 0 || ab[1] > 5 || ab[2] < 0 || ab[2] > 5;
+          const int nbx = nb[0] >> 2;
+          mig = nbx < A.bx0 ? 0 : (nbx >= A.bx1 ? 1 : -1);
+          if (mig >= 0 && !A.measure) {
+            // leaves this rank's slab: still scattered here (P2G belongs to the
+            // step that moved it), binned by the neighbour
+            const uint32_t slot = atomicAdd(&A.mig_count[mig], 1u);
+            if (slot < A.mig_cap) {
+              const float4* src4 = A.dst.rec + size_t(pos) * 8;
+              float4* o4 = A.mig[mig] + size_t(slot) * 8;
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
-          cm = fmaxf(cm, fabsf(vn[a]) + fabsf(Cn[3 * a]) * dxm[0] + fabsf(Cn[3 * a + 1]) * dxm[1] +
-                             fabsf(Cn[3 * a + 2]) * dxm[2]);
-        const float fm = fmaxf(fabsf(M[0]) * G0 + fabsf(M[3]) * G1 + fabsf(M[4]) * G2,
-                               fmaxf(fabsf(M[3]) * G0 + fabsf(M[1]) * G1 + fabsf(M[5]) * G2,
-                                     fabsf(M[4]) * G0 + fabsf(M[5]) * G1 + fabsf(M[2]) * G2));
-        if (!far) {
-          bm = m * W * 1.0001f;
-          bp = m * W * cm * 1.0001f;
-          bf = fm * 1.0001f;
-          tmask = touched27(axis_blocks(ab[0]), axis_blocks(ab[1]), axis_blocks(ab[2]));
-          if (mig < 0) atomicAdd(&sm.cnt[p][aaddr(ab[0], ab[1], ab[2])], 1u);
+              for (int c8 = 0; c8 < 8; ++c8) o4[c8] = src4[c8];
+            } else {
+              err_report(A.err, ERR_CAPACITY, pidv);
+            }
+          }
+          // contribution bounds: |w| <= prod_a max_o w_a(o); |grad w_a| <= max|g_a| prod_{b!=a} max w_b / h;
+          // |dx_a| <= h * max(d_a, 2 - d_a)
+          float wmax[3], gmax[3], dxm[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const float dd = d1[a];
+            const float w0 = 0.5f * (1.5f - dd) * (1.5f - dd), w1 = 0.75f - (dd - 1.f) * (dd - 1.f),
+                        w2 = 0.5f * (dd - 0.5f) * (dd - 0.5f);
+            wmax[a] = fmaxf(w0, fmaxf(w1, w2));
+            gmax[a] = fmaxf(fabsf(dd - 1.5f), fmaxf(fabsf(2.f * (dd - 1.f)), fabsf(dd - 0.5f)));
+            dxm[a] = hf_ * fmaxf(dd, 2.f - dd);
+          }
+          const float W = wmax[0] * wmax[1] * wmax[2];
+          const float G0 = gmax[0] * wmax[1] * wmax[2] * ih, G1 = wmax[0] * gmax[1] * wmax[2] * ih,
+                      G2 = wmax[0] * wmax[1] * gmax[2] * ih;
+          float cm = 0.f;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            cm = fmaxf(cm, fabsf(vn[a]) + fabsf(Cn[3 * a]) * dxm[0] + fabsf(Cn[3 * a + 1]) * dxm[1] +
+                               fabsf(Cn[3 * a + 2]) * dxm[2]);
+          const float fm = fmaxf(fabsf(M[0]) * G0 + fabsf(M[3]) * G1 + fabsf(M[4]) * G2,
+                                 fmaxf(fabsf(M[3]) * G0 + fabsf(M[1]) * G1 + fabsf(M[5]) * G2,
+                                       fabsf(M[4]) * G0 + fabsf(M[5]) * G1 + fabsf(M[2]) * G2));
+          const float bm = m * W * 1.0001f, bp = m * W * cm * 1.0001f, bf = fm * 1.0001f;
+          mx_m = fmaxf(mx_m, bm);
+          mx_p = fmaxf(mx_p, bp);
+          mx_f = fmaxf(mx_f, bf);
+          if (!A.measure && !far && (bm * Sm > FX_LIM || bp * Sp > FX_LIM || bf * Sf > FX_LIM)) {
+            scale_ovf = true;  // the step's P2G is replayed from the records with measured scales
+            sovf = true;
+          }
+        }
+        if (sovf) {
+          binv = OVF_KEY;  // live: re-binned by the replay
+        } else if (!A.measure && ok && !far) {
+          // ---- P2G of the next step into the fixed-point arena X[p]; packed
+          // fp32x2 where two fields share an operation, the magic add folded
+          // into each product
+          float w[3][3], g[3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) bspline(d1[a], w[a], g[a]);
+          const int ad0 = aaddr(ab[0], ab[1], ab[2]);
+          const float2 mS = make_float2(m * Sm, m * Sp);
+          // force: f = -(M grad w); grad w = (g0 w1 w2, w0 g1 w2, w0 w1 g2)/h
+          const float fs = -Sf * ih;
+          const float Mh[6] = {M[0] * fs, M[1] * fs, M[2] * fs, M[3] * fs, M[4] * fs, M[5] * fs};
+          const float2 MhA = make_float2(Mh[0], Mh[3]), MhB = make_float2(Mh[3], Mh[1]),
+                       MhC = make_float2(Mh[4], Mh[5]);
+          const float2 V01 = make_float2(vn[0], vn[1]), C03 = make_float2(Cn[0], Cn[3]),
+                       C14 = make_float2(Cn[1], Cn[4]);
+          float2 cz01[3];  // h (C_02, C_12) (k - d2)
+          float cz2[3];    // h C_22 (k - d2)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const float dz = (float(k) - d1[2]) * hf_;
+            cz01[k] = __fmul2_rn(make_float2(Cn[2], Cn[5]), make_float2(dz, dz));
+            cz2[k] = Cn[8] * dz;
+          }
+          const float2 MG2 = make_float2(MAGIC, MAGIC), M0 = make_float2(MAGIC, 0.f);
+          int* a0 = &sm.acc[p][0][ad0];
+#pragma unroll
+          for (int oi = 0; oi < 3; ++oi) {
+            const float dx = (float(oi) - d1[0]) * hf_;
+#pragma unroll
+            for (int oj = 0; oj < 3; ++oj) {
+              const float dy = (float(oj) - d1[1]) * hf_;
+              const float wij = w[0][oi] * w[1][oj];
+              const float2 q01 = __ffma2_rn(C14, make_float2(dy, dy), __ffma2_rn(C03, make_float2(dx, dx), V01));
+              const float q2 = vn[2] + Cn[6] * dx + Cn[7] * dy;
+              const float Ax = g[0][oi] * w[1][oj], Ay = w[0][oi] * g[1][oj];
+              const float2 r01 = __ffma2_rn(MhB, make_float2(Ay, Ay), __fmul2_rn(MhA, make_float2(Ax, Ax)));
+              const float2 s01 = __fmul2_rn(MhC, make_float2(wij, wij));
+              const float r2 = Mh[4] * Ax + Mh[5] * Ay, s2 = Mh[2] * wij;
+              const float2 wm = __fmul2_rn(mS, make_float2(wij, wij));  // (wij m Sm, wij m Sp)
+#pragma unroll
+              for (int ok2 = 0; ok2 < 3; ++ok2) {
+                const int o = aaddr(oi, oj, ok2);
+                const float wz = w[2][ok2], gz = g[2][ok2];
+                const float2 mc = __ffma2_rn(wm, make_float2(wz, wz), M0);  // (mass + MAGIC, momentum weight)
+                const float2 m01 = __ffma2_rn(make_float2(mc.y, mc.y), __fadd2_rn(q01, cz01[ok2]), MG2);
+                const float m2 = fmaf(mc.y, q2 + cz2[ok2], MAGIC);
+                const float2 f01 = __ffma2_rn(make_float2(wz, wz), r01, __ffma2_rn(make_float2(gz, gz), s01, MG2));
+                const float f2 = fmaf(wz, r2, fmaf(gz, s2, MAGIC));
+                sred(a0 + o, magic_q(mc.x));
+                sred(a0 + 1 * SCAT_N + o, magic_q(m01.x));
+                sred(a0 + 2 * SCAT_N + o, magic_q(m01.y));
+                sred(a0 + 3 * SCAT_N + o, magic_q(m2));
+                sred(a0 + 4 * SCAT_N + o, magic_q(f01.x));
+                sred(a0 + 5 * SCAT_N + o, magic_q(f01.y));
+                sred(a0 + 6 * SCAT_N + o, magic_q(f2));
+                sred(a0 + 7 * SCAT_N + o, 1);
+              }
+            }
+          }
+          tmask |= touched27(axis_blocks(ab[0]), axis_blocks(ab[1]), axis_blocks(ab[2]));
+          if (mig < 0) {
+            atomicAdd(&sm.cnt[p][aaddr(ab[0], ab[1], ab[2])], 1u);
+            binv = BIN_ARENA | uint32_t((ab[0] << 6) | (ab[1] << 3) | ab[2]);
+          } else {
+            binv = BAD_KEY;
+          }
+        } else if (!A.measure && ok && far) {
+          scatter_global(A, nb, d1, m, vn, Cn, M, binv, mig < 0);
+        } else {
+          binv = BAD_KEY;
         }
       }
+      if (!A.measure) sm.binr[p][kk][tid] = valid ? binv : BIN_SKIP;
     }
     {
-      const uint32_t um = warp_max(__float_as_uint(bm)), up = warp_max(__float_as_uint(bp)),
-                     uf = warp_max(__float_as_uint(bf));
       const uint32_t tm = __reduce_or_sync(0xffffffffu, tmask);
-      if ((tid & 31) == 0) {
-        atomicMax(&sm.bmax[p][0], um);
-        atomicMax(&sm.bmax[p][1], up);
-        atomicMax(&sm.bmax[p][2], uf);
-        if (tm) atomicOr(&sm.touched[p], tm);
-      }
+      if ((tid & 31) == 0 && tm) atomicOr(&sm.touched[p], tm);
     }
-    __syncthreads();  // [B2] bounds, touched blocks and bin counts of item i
+    __syncthreads();  // [B2] touched blocks and bin counts of item i
     if (GATHER && nxt.r() != BAD_KEY) prefetch_arena(sm, A, nxt, buf ^ 1, tid);
     // item i+3's metadata goes into this item's ring slot (its fields are in
     // registers; nobody reads the slot after [B2])
     if (tid == 0) fetch_item(A, n_items, kf, sm.info[c], true);
     cp_async_commit();
-    // item i+2: raw index loads now, consumed after the scatter
+    // item i+2: index loads now, consumed after the flush
     const uint32_t nnr = nn.r();
-    const uint32_t key2 = nnr == BAD_KEY ? 0u : nnr * 64 + (tid & 63);
-    const uint32_t slot2 = nn.g() * SLOTS + (tid >> 6);
     uint32_t cnt2 = 0, off2 = 0;
     if (nnr != BAD_KEY) {
-      cnt2 = A.B.cell_count[key2];
-      off2 = A.B.cell_off[key2];
+      cnt2 = A.B.cell_count[nnr * 64 + cell];
+      off2 = A.B.cell_off[nnr * 64 + cell];
     }
     // warp 0: probe the home slot of each touched block of the next table;
-    // the probe latency overlaps the scatter, the insert resolves after it
+    // the probe latency overlaps the flush, the insert resolves after it
     const uint32_t tmask_all = sm.touched[p];
     uint64_t ins_key = 0, probe_key = 0;
     uint32_t probe_val = EMPTY_VAL;
-    const bool inserter = tid < 27 && ((tmask_all >> tid) & 1u);
+    const bool inserter = !A.measure && tid < 27 && ((tmask_all >> tid) & 1u);
     if (inserter) {
       const int di = tid / 9 - 1, dj = (tid / 3) % 3 - 1, dk = tid % 3 - 1;
       ins_key = pack_key(B0 + di, B1 + dj, B2 + dk);
@@ -960,80 +1089,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
       probe_key = ld_volatile_u64(&A.S.hv.keys[sl]);
       probe_val = ld_volatile_u32(&A.S.hv.vals[sl]);
     }
-    float iSm, iSp, iSf;
-    const float Sm = fx_scale(__uint_as_float(sm.bmax[p][0]), iSm);
-    const float Sp = fx_scale(__uint_as_float(sm.bmax[p][1]), iSp);
-    const float Sf = fx_scale(__uint_as_float(sm.bmax[p][2]), iSf);
-    int kind = 0;
-    uint32_t binv = BAD_KEY;
-    if (valid) kind = 1;
-    if (ok && !far) {
-      // ---- P2G of the next step into the fixed-point arena X[p]
-      float w[3][3], g[3][3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) bspline(d1[a], w[a], g[a]);
-      const int ad0 = aaddr(ab[0], ab[1], ab[2]);
-      // packed fp32x2 where two fields share an operation (FFMA2, scalar
-      // operands broadcast); the magic add is folded into each product
-      const float2 mS = make_float2(m * Sm, m * Sp);
-      // force: f = -(M grad w); grad w = (g0 w1 w2, w0 g1 w2, w0 w1 g2)/h
-      const float fs = -Sf * ih;
-      const float Mh[6] = {M[0] * fs, M[1] * fs, M[2] * fs, M[3] * fs, M[4] * fs, M[5] * fs};
-      const float2 MhA = make_float2(Mh[0], Mh[3]), MhB = make_float2(Mh[3], Mh[1]), MhC = make_float2(Mh[4], Mh[5]);
-      const float2 V01 = make_float2(vn[0], vn[1]), C03 = make_float2(Cn[0], Cn[3]), C14 = make_float2(Cn[1], Cn[4]);
-      float2 cz01[3];  // h (C_02, C_12) (k - d2)
-      float cz2[3];    // h C_22 (k - d2)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const float dz = (float(k) - d1[2]) * hf_;
-        cz01[k] = __fmul2_rn(make_float2(Cn[2], Cn[5]), make_float2(dz, dz));
-        cz2[k] = Cn[8] * dz;
-      }
-      const float2 MG2 = make_float2(MAGIC, MAGIC), M0 = make_float2(MAGIC, 0.f);
-      int* a0 = &sm.acc[p][0][ad0];
-#pragma unroll
-      for (int oi = 0; oi < 3; ++oi) {
-        const float dx = (float(oi) - d1[0]) * hf_;
-#pragma unroll
-        for (int oj = 0; oj < 3; ++oj) {
-          const float dy = (float(oj) - d1[1]) * hf_;
-          const float wij = w[0][oi] * w[1][oj];
-          const float2 q01 = __ffma2_rn(C14, make_float2(dy, dy), __ffma2_rn(C03, make_float2(dx, dx), V01));
-          const float q2 = vn[2] + Cn[6] * dx + Cn[7] * dy;
-          const float Ax = g[0][oi] * w[1][oj], Ay = w[0][oi] * g[1][oj];
-          const float2 r01 = __ffma2_rn(MhB, make_float2(Ay, Ay), __fmul2_rn(MhA, make_float2(Ax, Ax)));
-          const float2 s01 = __fmul2_rn(MhC, make_float2(wij, wij));
-          const float r2 = Mh[4] * Ax + Mh[5] * Ay, s2 = Mh[2] * wij;
-          const float2 wm = __fmul2_rn(mS, make_float2(wij, wij));  // (wij m Sm, wij m Sp)
-#pragma unroll
-          for (int ok2 = 0; ok2 < 3; ++ok2) {
-            const int o = aaddr(oi, oj, ok2);
-            const float wz = w[2][ok2], gz = g[2][ok2];
-            const float2 mc = __ffma2_rn(wm, make_float2(wz, wz), M0);  // (mass + MAGIC, momentum weight)
-            const float2 m01 = __ffma2_rn(make_float2(mc.y, mc.y), __fadd2_rn(q01, cz01[ok2]), MG2);
-            const float m2 = fmaf(mc.y, q2 + cz2[ok2], MAGIC);
-            const float2 f01 = __ffma2_rn(make_float2(wz, wz), r01, __ffma2_rn(make_float2(gz, gz), s01, MG2));
-            const float f2 = fmaf(wz, r2, fmaf(gz, s2, MAGIC));
-            sred(a0 + o, magic_q(mc.x));
-            sred(a0 + 1 * SCAT_N + o, magic_q(m01.x));
-            sred(a0 + 2 * SCAT_N + o, magic_q(m01.y));
-            sred(a0 + 3 * SCAT_N + o, magic_q(m2));
-            sred(a0 + 4 * SCAT_N + o, magic_q(f01.x));
-            sred(a0 + 5 * SCAT_N + o, magic_q(f01.y));
-            sred(a0 + 6 * SCAT_N + o, magic_q(f2));
-            sred(a0 + 7 * SCAT_N + o, 1);
-          }
-        }
-      }
-      if (mig < 0) {
-        kind = 2;
-        binv = uint32_t((ab[0] << 6) | (ab[1] << 3) | ab[2]);
-      }
-    } else if (ok && far) {
-      scatter_global(A, nb, d1, m, vn, Cn, M, binv, mig < 0);
-    }
     // ---- flush item i-1 (its ranks were resolved before [B1])
-    if (have_prev) flush(p ^ 1);
+    if (have_prev && !A.measure) flush(p ^ 1, c2r);
     // ---- warp 0: ranks of item i's touched blocks
     if (tid < 27) {
       uint32_t rk = BAD_KEY;
@@ -1043,33 +1100,31 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
       }
       sm.rank[p][tid] = rk;
     }
-    // item i+2's sorted position and source index (consumed one item later)
-    uint32_t pos2 = 0, src2 = 0;
-    const bool valid2 = nnr != BAD_KEY && slot2 < cnt2;
-    if (valid2) {
-      pos2 = off2 - cnt2 + slot2;  // k_bin advanced cell_off to the cell's end
-      src2 = A.perm[pos2];
+    // item i+2's sorted positions (ring slot of item i-1, flushed above) and
+    // source indices (consumed one item later)
+    slots(nn, cnt2, off2, c2r);
+    {
+      const uint32_t pa = sm.posr[c2r][0][tid], pb = sm.posr[c2r][1][tid];
+      src1a = pa != NOPOS ? A.perm[pa] : 0u;
+      src1b = pb != NOPOS ? A.perm[pb] : 0u;
     }
     ++kf;
     have_prev = true;
-    prev_kind = kind;
-    prev_pos = pos;
-    prev_bin = binv;
-    piSm = iSm;
-    piSp = iSp;
-    piSf = iSf;
-    pos = pos1;
-    valid = valid1;
-    pos1 = pos2;
-    valid1 = valid2;
-    src1 = src2;
     buf ^= 1;
     p ^= 1;
-    c = c == 2 ? 0 : c + 1;
+    c = c1r;
   }
-  if (have_prev) flush(p ^ 1);
+  if (have_prev && !A.measure) flush(p ^ 1, c == 0 ? 2 : c - 1);
   vmax2_local = warp_max(vmax2_local);
-  if ((tid & 31) == 0 && vmax2_local) atomicMax(&A.stS->vmax2_bits, vmax2_local);
+  const uint32_t um = warp_max(__float_as_uint(mx_m)), up = warp_max(__float_as_uint(mx_p)),
+                 uf = warp_max(__float_as_uint(mx_f));
+  if ((tid & 31) == 0) {
+    if (vmax2_local && !A.measure) atomicMax(&A.stS->vmax2_bits, vmax2_local);
+    if (um) atomicMax(&A.bnd_dst[0], um);
+    if (up) atomicMax(&A.bnd_dst[1], up);
+    if (uf) atomicMax(&A.bnd_dst[2], uf);
+  }
+  if (scale_ovf) atomicOr(&A.stS->scale_ovf, 1u);
 }
 
 // ------------------------------------------------------- state transfer
@@ -1301,6 +1356,7 @@ struct smpm_sim {
   int bx0 = INT32_MIN, bx1 = INT32_MAX;
   int64_t pid_base = 0;
   uint32_t n_store = 0;   // storage slots of the current buffer (incl. holes)
+  int64_t n_replays = 0;  // P2G replays after a fixed-point scale overflow
   float4* mig[2] = {nullptr, nullptr};
   uint32_t* mig_count = nullptr;
   uint32_t mig_cap = 0;
@@ -1412,6 +1468,9 @@ FusedArgs fused_args(smpm_sim* s, int B, int dstbuf, int project) {
   A.stS = s->dstats + (1 - B);
   A.err = s->derr;
   A.project = project;
+  A.measure = 0;
+  A.scale_src = s->dstats[B].bnd_bits;
+  A.bnd_dst = s->dstats[1 - B].bnd_bits;
   A.bx0 = s->bx0;
   A.bx1 = s->bx1;
   A.mig[0] = s->mig[0];
@@ -1450,6 +1509,15 @@ int launch_fused(smpm_sim* s, bool gather, int project) {
   if (s->mig_count) CK(cudaMemsetAsync(s->mig_count, 0, 8, s->stream));
   FusedArgs A = fused_args(s, s->S, dstbuf, project);
   size_t smem = smem_bytes();
+  if (!gather) {
+    // P2G-only pass (prologue / replay): first measure the contribution
+    // bounds the fixed-point scales derive from (nothing is written)
+    FusedArgs Mz = A;
+    Mz.measure = 1;
+    Mz.bnd_dst = s->dstats[s->S].bnd_bits;
+    k_g2p2g<false><<<s->persist_blocks, CTA, smem, s->stream>>>(Mz);
+    CK(cudaGetLastError());
+  }
   if (gather)
     k_g2p2g<true><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
   else
@@ -1503,9 +1571,9 @@ int grow_grid(smpm_sim* s, uint32_t need) {
   }
   s->allocs = keep;
   uint64_t nc = std::max<uint64_t>(uint64_t(s->cap_b) * 2, next_pow2(uint64_t(need) + need / 4));
-  if (nc > (1ull << 28)) return set_err(SMPM_ERR_CAPACITY, "block capacity exceeds 2^28");
+  if (nc > (1ull << 25)) return set_err(SMPM_ERR_CAPACITY, "block capacity exceeds 2^25");  // bins: rank * 64 + cell < 2^31
   s->cap_b = uint32_t(nc);
-  s->cap_items = uint32_t(std::min<uint64_t>(uint64_t(s->cap_p) / SLOTS + s->cap_b + 1024, 0xFFFFFFF0ull));
+  s->cap_items = uint32_t(std::min<uint64_t>(uint64_t(s->cap_p) / ISLOTS + s->cap_b + 1024, 0xFFFFFFF0ull));
   return alloc_grid(s);
 }
 
@@ -1665,8 +1733,8 @@ int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
   // grid
   uint64_t cb = cfg->block_capacity > 0 ? uint64_t(cfg->block_capacity)
                                         : next_pow2(std::max<uint64_t>(4096, uint64_t(s->cap_p) / 96));
-  s->cap_b = uint32_t(std::min<uint64_t>(cb, 1ull << 30));
-  s->cap_items = uint32_t(std::min<uint64_t>(uint64_t(s->cap_p) / SLOTS + s->cap_b + 1024, 0xFFFFFFF0ull));
+  s->cap_b = uint32_t(std::min<uint64_t>(cb, 1ull << 25));
+  s->cap_items = uint32_t(std::min<uint64_t>(uint64_t(s->cap_p) / ISLOTS + s->cap_b + 1024, 0xFFFFFFF0ull));
   rc = alloc_grid(s);
   if (rc) return rc;
   rc = dalloc(s, &s->dstats, 2);
@@ -1873,6 +1941,12 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
       if (rc) return rc;
       s->need_prologue = true;
       s->prologue_project = false;
+    } else if (nx.scale_ovf) {
+      // a P2G contribution outgrew the fixed-point scale derived from the
+      // previous step: redo this step's P2G from the records with measured bounds
+      s->need_prologue = true;
+      s->prologue_project = false;
+      s->n_replays += 1;
     }
     s->last = r;
   }
