@@ -519,12 +519,34 @@ __device__ inline void coulomb_project(double& v0, double& v1, double& v2, doubl
   v2 = scale * t2;
 }
 
+// Terrain under one node column (nx, ny): the heightfield sample depends
+// only on the node's x, y, so it is evaluated once per column of a block.
+struct Column {
+  double zs, n0, n1, n2;  // terrain height and unit normal (-zx, -zy, 1)/len
+};
+__device__ inline void column_terrain(const GridParams& gp, int nx, int ny, Column& col) {
+  col.zs = 0.0;
+  col.n0 = col.n1 = 0.0;
+  col.n2 = 1.0;
+  for (int b = 0; b < gp.n_bc; ++b) {
+    if (gp.bc[b].kind != 1) continue;
+    double zx, zy;
+    hf_sample(gp.hf, __dmul_rn(double(nx), gp.h), __dmul_rn(double(ny), gp.h), col.zs, zx, zy);
+    const double il = 1.0 / sqrt(zx * zx + zy * zy + 1.0);
+    col.n0 = -zx * il;
+    col.n1 = -zy * il;
+    col.n2 = il;
+  }
+}
+
 // One node of _grid_update (solver.py:578-625).  `force` excludes gravity
 // here; gravity enters as m*g (the scatter's sum_p w m g equals m_node g).
 // Node position and boundary predicates are fp64 and contraction-free, so the
-// plane / terrain decisions match the reference for the same node.
-__device__ inline void grid_node(const GridParams& gp, int nx, int ny, int nz, double m, double p0, double p1,
-                                 double p2, double f0, double f1, double f2, float& o0, float& o1, float& o2) {
+// plane / terrain decisions match the reference for the same node.  `col` is
+// the node column's terrain (column_terrain).
+__device__ inline void grid_node_col(const GridParams& gp, const Column& col, int nx, int ny, int nz, double m,
+                                     double p0, double p1, double p2, double f0, double f1, double f2, float& o0,
+                                     float& o1, float& o2) {
   if (m <= gp.mass_floor) {
     o0 = o1 = o2 = 0.0f;
     return;
@@ -542,19 +564,20 @@ __device__ inline void grid_node(const GridParams& gp, int nx, int ny, int nz, d
                                         __dmul_rn(__dadd_rn(x1, -bc.point[1]), bc.normal[1])),
                               __dmul_rn(__dadd_rn(x2, -bc.point[2]), bc.normal[2]));
         if (sd <= 0.0) coulomb_project(v0, v1, v2, bc.normal[0], bc.normal[1], bc.normal[2], bc.mu);
-      } else {
-        double zs, zx, zy;
-        hf_sample(gp.hf, x0, x1, zs, zx, zy);
-        if (__dadd_rn(x2, -zs) <= 0.0) {
-          double il = 1.0 / sqrt(zx * zx + zy * zy + 1.0);
-          coulomb_project(v0, v1, v2, -zx * il, -zy * il, il, bc.mu);
-        }
+      } else if (__dadd_rn(x2, -col.zs) <= 0.0) {
+        coulomb_project(v0, v1, v2, col.n0, col.n1, col.n2, bc.mu);
       }
     }
   }
   o0 = float(v0);
   o1 = float(v1);
   o2 = float(v2);
+}
+__device__ inline void grid_node(const GridParams& gp, int nx, int ny, int nz, double m, double p0, double p1,
+                                 double p2, double f0, double f1, double f2, float& o0, float& o1, float& o2) {
+  Column col;
+  column_terrain(gp, nx, ny, col);
+  grid_node_col(gp, col, nx, ny, nz, m, p0, p1, p2, f0, f1, f2, o0, o1, o2);
 }
 
 __device__ inline void err_report(unsigned long long* err, uint32_t code, uint64_t particle) {

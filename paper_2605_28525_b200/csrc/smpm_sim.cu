@@ -299,31 +299,54 @@ __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, u
 
 // grid update over the active nodes of S (+ accumulator zeroing, clearing of
 // table T for reuse by the next P2G).
-__global__ void __launch_bounds__(256) k_grid(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
-                                              float4* __restrict__ acc, float4* __restrict__ gv, GridParams gp,
-                                              int record, int bx0, int bx1) {
+__global__ void __launch_bounds__(256, 2) k_grid(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
+                                                 float4* __restrict__ acc, float4* __restrict__ gv, GridParams gp,
+                                                 int record, int bx0, int bx1) {
+  __shared__ Boundary sbc[8];
+  if (threadIdx.x < gp.n_bc && threadIdx.x < 8) sbc[threadIdx.x] = gp.bc[threadIdx.x];
+  __syncthreads();
+  gp.bc = sbc;  // boundary table read per node: keep it on chip
   const uint32_t nb = stS->n_blocks;
   gp.dt = stS->dt;
-  const size_t nn = size_t(nb) * 64;
   double msum = 0, p0s = 0, p1s = 0, p2s = 0;
   uint32_t act = 0;
-  for (size_t c = blockIdx.x * size_t(blockDim.x) + threadIdx.x; c < nn; c += size_t(gridDim.x) * blockDim.x) {
-    uint32_t r = uint32_t(c >> 6), l = uint32_t(c & 63);
-    float4 a = acc[2 * c], b = acc[2 * c + 1];
-    acc[2 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
-    acc[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  // a half-warp per block, a lane per node column (terrain sampled once per
+  // column), the column's four nodes (128 contiguous bytes) loaded up front
+  const int lane = threadIdx.x & 31;
+  const size_t hw = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 4;
+  const size_t nhw = (size_t(gridDim.x) * blockDim.x) >> 4;
+  const int li = (lane >> 2) & 3, lj = lane & 3;
+  for (size_t r = hw; r < nb; r += nhw) {
+    const uint64_t key = S.hv.active_keys[r];
+    const size_t c0 = size_t(r) * 64 + (li << 4) + (lj << 2);
+    float4 a[4], b[4];
+#pragma unroll
+    for (int lk = 0; lk < 4; ++lk) {
+      a[lk] = __ldcs(&acc[2 * (c0 + lk)]);
+      b[lk] = __ldcs(&acc[2 * (c0 + lk) + 1]);
+    }
     int bi, bj, bk;
-    unpack_key(S.hv.active_keys[r], bi, bj, bk);
-    float o0, o1, o2;
-    grid_node(gp, bi * 4 + int(l >> 4), bj * 4 + int((l >> 2) & 3), bk * 4 + int(l & 3), a.x, a.y, a.z, a.w, b.x,
-              b.y, b.z, o0, o1, o2);
-    gv[c] = make_float4(o0, o1, o2, 0.f);
-    act += (b.w > 0.f && bi >= bx0 && bi < bx1) ? 1u : 0u;
-    if (record) {
-      msum += a.x;
-      p0s += a.y;
-      p1s += a.z;
-      p2s += a.w;
+    unpack_key(key, bi, bj, bk);
+    const int nx = bi * 4 + li, ny = bj * 4 + lj;
+    Column col;
+    column_terrain(gp, nx, ny, col);
+    const bool own = bi >= bx0 && bi < bx1;
+#pragma unroll
+    for (int lk = 0; lk < 4; ++lk) {
+      const size_t c = c0 + lk;
+      acc[2 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      float o0, o1, o2;
+      grid_node_col(gp, col, nx, ny, bk * 4 + lk, a[lk].x, a[lk].y, a[lk].z, a[lk].w, b[lk].x, b[lk].y, b[lk].z, o0,
+                    o1, o2);
+      gv[c] = make_float4(o0, o1, o2, 0.f);
+      act += (b[lk].w > 0.f && own) ? 1u : 0u;
+      if (record) {
+        msum += a[lk].x;
+        p0s += a[lk].y;
+        p1s += a[lk].z;
+        p2s += a[lk].w;
+      }
     }
   }
   act = warp_sum(act);
