@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "../../include/smpm.h"
@@ -1175,6 +1176,33 @@ __global__ void k_upload(Particles P, int64_t off, int64_t pid_base, int64_t n, 
   }
 }
 
+// Inverse permutation of the current buffer: inv[pid - lo] = storage index.
+__global__ void k_invperm(Particles P, int64_t n_store, int64_t lo, int64_t n, const uint32_t* __restrict__ bin,
+                          uint32_t* __restrict__ inv) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_store;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if (bin && bin[i] == BAD_KEY) continue;
+    const int64_t p = int64_t(__float_as_uint(reinterpret_cast<const float*>(P.rec + i * 8)[W_PM]) & PID_MASK) - lo;
+    if (p >= 0 && p < n) inv[p] = uint32_t(i);
+  }
+}
+
+// Gather x and v of pids [lo, lo + c) in reference layout (fp64) into one
+// staging block: x[3c] then v[3c].
+__global__ void k_gather_xv(Particles P, const uint32_t* __restrict__ inv, int64_t lo, int64_t c,
+                            double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < c; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4* r4 = P.rec + size_t(inv[lo + i]) * 8;
+    const float4 c0 = r4[0], c1 = r4[1], c4 = r4[4], c5 = r4[5];
+    out[3 * i] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
+    out[3 * i + 1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
+    out[3 * i + 2] = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
+    out[3 * c + 3 * i] = c4.z;
+    out[3 * c + 3 * i + 1] = c4.w;
+    out[3 * c + 3 * i + 2] = c5.x;
+  }
+}
+
 // Download: un-permute by pid into reference layout.  sigma/jac from F.
 __global__ void k_download(Particles P, int64_t n, int64_t lo, int64_t hi, double* x, double* v, double* C,
                            double* F, double* sigma, double* jac, const Material* mats, int n_mat) {
@@ -1386,6 +1414,11 @@ struct smpm_sim {
   bool in_flight = false; // a step was launched and not yet synced
   uint32_t* hcount = nullptr;  // pinned: counter/overflow of the table just filled
   std::vector<smpm_material> host_mats;
+  // host <-> device transfer pipeline (pinned double buffer, host threads)
+  unsigned char* pin[2] = {nullptr, nullptr};
+  size_t pin_bytes = 0;
+  cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+  int host_threads = 1;
 };
 
 namespace {
@@ -1674,6 +1707,125 @@ int run_prologue(smpm_sim* s, int project) {
   return set_err(SMPM_ERR_CAPACITY, "capacity growth did not converge");
 }
 
+// ------------------------------------------------- host transfer pipeline
+// Host arrays (the caller's numpy buffers are pageable) move through two
+// pinned buffers: host threads pack / unpack one chunk while the copy engine
+// moves the other, so the transfer runs at PCIe rate instead of the driver's
+// pageable-staging rate.
+bool is_host_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+int ensure_pinned(smpm_sim* s) {
+  if (s->pin[0]) return SMPM_OK;
+  s->pin_bytes = size_t(192) << 20;
+  for (int b = 0; b < 2; ++b) {
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&s->pin[b]), s->pin_bytes, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&s->pin_ev[b], cudaEventDisableTiming));
+  }
+  s->host_threads = std::max(1, std::min(32, int(std::thread::hardware_concurrency())));
+  return SMPM_OK;
+}
+
+template <class Fn>
+void parallel_range(int nt, int64_t n, Fn fn) {
+  if (nt <= 1 || n < 65536) {
+    fn(int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t per = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t a = t * per, b = std::min(n, a + per);
+    if (a < b) th.emplace_back(fn, a, b);
+  }
+  for (auto& t : th) t.join();
+}
+
+// Host twin of k_upload: reference-layout fp64 arrays -> 128-byte records.
+void pack_records(float* out, int64_t off, int64_t pid_base, int64_t a, int64_t b, const double* x, const double* v,
+                  const double* C, const double* F, const double* m, const double* V0, const int64_t* mat) {
+  for (int64_t i = a; i < b; ++i) {
+    const int64_t j = off + i;
+    float* w = out + i * REC_W;
+    std::memcpy(w, x + 3 * j, 24);
+    w[W_M] = float(m[j]);
+    w[W_V0] = float(V0[j]);
+    for (int q = 0; q < 9; ++q) w[W_F + q] = float(F[9 * j + q] - ((q == 0 || q == 4 || q == 8) ? 1.0 : 0.0));
+    const uint32_t pm = (uint32_t(pid_base + j) & PID_MASK) | (uint32_t(mat[j]) << 29);
+    std::memcpy(&w[W_PM], &pm, 4);
+    for (int a3 = 0; a3 < 3; ++a3) w[W_V + a3] = float(v[3 * j + a3]);
+    for (int q = 0; q < 9; ++q) w[W_C + q] = float(C[9 * j + q]);
+    w[30] = w[31] = 0.f;
+  }
+}
+
+int upload_host(smpm_sim* s, int64_t n, const double* x, const double* v, const double* C, const double* F,
+                const double* m, const double* V0, const int64_t* mat) {
+  int rc = ensure_pinned(s);
+  if (rc) return rc;
+  const int64_t CH = int64_t(s->pin_bytes / 128);
+  for (int64_t k = 0, off = 0; off < n; ++k, off += CH) {
+    const int b = int(k & 1);
+    const int64_t c = std::min(CH, n - off);
+    if (k >= 2) CK(cudaEventSynchronize(s->pin_ev[b]));
+    float* dst = reinterpret_cast<float*>(s->pin[b]);
+    parallel_range(s->host_threads, c, [&](int64_t a, int64_t e) {
+      pack_records(dst, off, s->pid_base, a, e, x, v, C, F, m, V0, mat);
+    });
+    CK(cudaMemcpyAsync(s->state[0].rec + off * 8, dst, size_t(c) * 128, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaEventRecord(s->pin_ev[b], s->stream));
+  }
+  return SMPM_OK;
+}
+
+// x and v of every particle, in pid order, into host arrays.
+int download_xv_host(smpm_sim* s, double* x, double* v) {
+  int rc = ensure_pinned(s);
+  if (rc) return rc;
+  const int64_t n = s->n;
+  const int64_t CH = int64_t(s->pin_bytes / 48);
+  uint32_t* inv = nullptr;
+  double* dst[2] = {nullptr, nullptr};
+  CK(cudaMallocAsync(&inv, size_t(n) * 4, s->stream));
+  CK(cudaMemsetAsync(inv, 0, size_t(n) * 4, s->stream));
+  for (int b = 0; b < 2; ++b) CK(cudaMallocAsync(&dst[b], size_t(CH) * 48, s->stream));
+  k_invperm<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n_store, s->pid_base, n, s->bin, inv);
+  CK(cudaGetLastError());
+  const int64_t nch = (n + CH - 1) / CH;
+  auto issue = [&](int64_t k) -> int {
+    const int b = int(k & 1);
+    const int64_t lo = k * CH, c = std::min(CH, n - lo);
+    k_gather_xv<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], inv, lo, c, dst[b]);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->pin[b], dst[b], size_t(c) * 48, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaEventRecord(s->pin_ev[b], s->stream));
+    return SMPM_OK;
+  };
+  for (int64_t k = 0; k < std::min<int64_t>(2, nch); ++k)
+    if ((rc = issue(k))) return rc;
+  for (int64_t k = 0; k < nch; ++k) {
+    const int b = int(k & 1);
+    const int64_t lo = k * CH, c = std::min(CH, n - lo);
+    CK(cudaEventSynchronize(s->pin_ev[b]));
+    const double* src = reinterpret_cast<const double*>(s->pin[b]);
+    parallel_range(s->host_threads, c, [&](int64_t a, int64_t e) {
+      if (x) std::memcpy(x + 3 * (lo + a), src + 3 * a, size_t(e - a) * 24);
+      if (v) std::memcpy(v + 3 * (lo + a), src + 3 * c + 3 * a, size_t(e - a) * 24);
+    });
+    if (k + 2 < nch && (rc = issue(k + 2))) return rc;
+  }
+  CK(cudaFreeAsync(inv, s->stream));
+  for (int b = 0; b < 2; ++b) CK(cudaFreeAsync(dst[b], s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return SMPM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1786,6 +1938,10 @@ int smpm_sim_destroy(smpm_sim* s) {
   if (s->hstats) cudaFreeHost(s->hstats);
   if (s->herr) cudaFreeHost(s->herr);
   if (s->hcount) cudaFreeHost(s->hcount);
+  for (int b = 0; b < 2; ++b) {
+    if (s->pin[b]) cudaFreeHost(s->pin[b]);
+    if (s->pin_ev[b]) cudaEventDestroy(s->pin_ev[b]);
+  }
   for (int i = 0; i < 5; ++i) cudaEventDestroy(s->ev[i]);
   if (s->own_stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -1806,6 +1962,14 @@ int smpm_sim_set_particles(smpm_sim* s, int64_t n, const double* x, const double
   s->n_store = uint32_t(n);
   s->cur = 0;
   CK(cudaMemsetAsync(s->bin, 0, size_t(n) * 4, s->stream));  // live (non-BAD) marker
+  if (is_host_ptr(x)) {
+    int rc = upload_host(s, n, x, v, C, F, m, V0, mat_id);
+    if (rc) return rc;
+    s->need_prologue = true;
+    s->prologue_project = true;
+    s->pending_err = 0;
+    return SMPM_OK;
+  }
   // staged chunks (inputs may be host or device memory)
   const int64_t CH = 1 << 22;
   double *sx, *sv, *sC, *sF, *sm, *sV;
@@ -1849,6 +2013,7 @@ int smpm_sim_get_particles(smpm_sim* s, double* x, double* v, double* C, double*
     int rc = smpm_sim_sync(s, nullptr);
     if (rc) return rc;
   }
+  if (!C && !F && !sigma && !jac && (x || v) && is_host_ptr(x ? x : v)) return download_xv_host(s, x, v);
   const int64_t CH = 1 << 22;
   const int64_t n = s->n;
   double *sx = nullptr, *sv = nullptr, *sC = nullptr, *sF = nullptr, *ss = nullptr, *sj = nullptr;

@@ -522,8 +522,8 @@ class Simulation:
     def _upload(self, ps):
         arrs = [np.ascontiguousarray(getattr(ps, k), dtype=np.float64) for k in ("x", "v", "C", "F", "m", "V0")]
         mid = np.ascontiguousarray(ps.mat_id, dtype=np.int64)
-        if not np.all(np.isfinite(arrs[0])):
-            raise SimulationError("non-finite particle position")
+        # non-finite positions are detected on the device while the first
+        # step bins the particles and raised by that step (solver.py:1005-1006)
         _lib.check(_lib.load().smpm_sim_set_particles(self._h, ps.n, *(a.ctypes.data for a in arrs),
                                                       mid.ctypes.data), "set particles")
         self._exported = None
