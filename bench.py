@@ -143,7 +143,7 @@ def reference_arm(args):
     base = run_cpu_port(args.config, max(1, min(args.steps, 3)))
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": METRIC, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["ms_per_step"],
-            "higher_is_better": True, "scaling": "weak" if args.gpus > 1 else "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIG_NAMES[args.config], "config": args.config},
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -260,14 +260,14 @@ def ours(args):
         sim2.local_particles()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     stats_bytes = args.steps * (2 * 128 + 24)
-    h2d = n * (24 + 24 + 72 + 72 + 8 + 8 + 8)
-    d2h = n * 48
+    h2d = n * 128  # host-packed 128-B particle records (smpm_sim_set_particles, include/smpm.h)
+    d2h = n * 48   # x, v (fp64) of every particle
     e2e_value = n * args.steps / e2e_s
     del sim2
     line = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": CONFIG_NAMES[args.config], "config": args.config if world == 1 else "C5",
                    "n_particles": n, "h": sc.config.h, "ppc": 2, "mean_allocated_nodes": float(np.mean(nalloc)),
