@@ -193,6 +193,13 @@ int64_t smpm_sim_num_particles(const smpm_sim* s);
 double smpm_sim_vmax(smpm_sim* s);
 int smpm_sim_launch_count(const smpm_sim* s, int64_t* kernels_per_step);
 
+/* Dense allocation mode, the comparison baseline of bench.compare
+ * (replaces build_dense_grid, grid_index.py:256-277, for
+ * SimConfig.backend == "dense"): every block of the inclusive block box
+ * [bmin, bmax] is allocated each step (ranks in row-major order), so
+ * n_allocated = n_dense and the grid update runs over the whole domain. */
+int smpm_sim_set_dense_domain(smpm_sim* s, const int32_t* bmin, const int32_t* bmax);
+
 /* ---------------------------------------------------- slab decomposition
  * Multi-GPU (the reference is single-process, PAPER.md:335-337
  * lists multi-GPU as future work).  A rank owns the particles whose base

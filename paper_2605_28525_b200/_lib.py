@@ -107,6 +107,7 @@ _SIGS = {
     "smpm_sim_launch_count": (ctypes.c_int, [P, P]),
     "smpm_sim_grid_size": (ctypes.c_int, [P, P]),
     "smpm_sim_set_slab": (ctypes.c_int, [P, I32, I32, I64, I64]),
+    "smpm_sim_set_dense_domain": (ctypes.c_int, [P, P, P]),
     "smpm_sim_exchange_pack": (ctypes.c_int, [P, ctypes.c_int, P, I64, P]),
     "smpm_sim_exchange_unpack": (ctypes.c_int, [P, P, I64, ctypes.c_int]),
     "smpm_sim_migrants": (ctypes.c_int, [P, ctypes.c_int, P, I64, P]),

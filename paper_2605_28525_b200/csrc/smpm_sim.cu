@@ -378,6 +378,35 @@ __global__ void __launch_bounds__(256, 2) k_grid(TableDev S, TableDev T, DevStat
     T.cell_count[c] = 0;
 }
 
+// ----------------------------------------------------------- dense mode
+// Dense allocation (the comparison baseline of bench.compare): every block of
+// the domain's block box is allocated each step with rank = row-major index,
+// like build_dense_grid (grid_index.py:256-277); blocks touched outside the
+// box are appended by the fused kernel after them.  The table is empty when
+// this runs, so each key is inserted once and takes its index as rank.
+__global__ void k_dense_insert(TableDev T, int b0, int b1, int b2, int s0, int s1, int s2) {
+  const uint32_t nd = uint32_t(s0) * uint32_t(s1) * uint32_t(s2);
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
+    const int i = int(r / uint32_t(s1 * s2)), j = int((r / uint32_t(s2)) % uint32_t(s1)), k = int(r % uint32_t(s2));
+    const uint64_t key = pack_key(b0 + i, b1 + j, b2 + k);
+    uint32_t sl = uint32_t(mix64(key)) & T.hv.mask;
+    for (uint32_t it = 0; it <= T.hv.mask; ++it, sl = (sl + 1) & T.hv.mask) {
+      if (atomicCAS(reinterpret_cast<unsigned long long*>(&T.hv.keys[sl]), (unsigned long long)EMPTY_KEY,
+                    (unsigned long long)key) == EMPTY_KEY) {
+        if (r < T.hv.cap_blocks) {
+          T.hv.active_keys[r] = key;
+          T.hv.slot_of_rank[r] = sl;
+        } else {
+          atomicExch(T.hv.overflow, 1u);
+        }
+        atomicExch(&T.hv.vals[sl], r);
+        break;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(T.hv.counter, nd);
+}
+
 // --------------------------------------------------------- prologue keys
 // Bins particles (arbitrary storage order) by the block of their base cell.
 __global__ void k_prologue_keys(Particles P, int64_t n, TableDev B, uint32_t* __restrict__ bin, double inv_h,
@@ -1408,6 +1437,9 @@ struct smpm_sim {
   int64_t pid_base = 0;
   uint32_t n_store = 0;   // storage slots of the current buffer (incl. holes)
   int64_t n_replays = 0;  // P2G replays after a fixed-point scale overflow
+  // dense allocation mode (bench.compare baseline): block box [dbmin, dbmin + dbshape)
+  bool dense = false;
+  int dbmin[3] = {0, 0, 0}, dbshape[3] = {0, 0, 0};
   float4* mig[2] = {nullptr, nullptr};
   uint32_t* mig_count = nullptr;
   uint32_t mig_cap = 0;
@@ -1550,6 +1582,14 @@ StepParams step_params(smpm_sim* s, double dt) {
   return sp;
 }
 
+int dense_insert(smpm_sim* s, int t) {
+  if (!s->dense) return SMPM_OK;
+  k_dense_insert<<<148 * 4, 256, 0, s->stream>>>(s->tab[t], s->dbmin[0], s->dbmin[1], s->dbmin[2], s->dbshape[0],
+                                                 s->dbshape[1], s->dbshape[2]);
+  CK(cudaGetLastError());
+  return SMPM_OK;
+}
+
 int scan_and_bin(smpm_sim* s, int Sx, double dt) {
   StepParams sp = step_params(s, dt);
   int grid = std::max(1, std::min<int>(s->max_tiles, 148 * 8));
@@ -1656,6 +1696,10 @@ int run_prologue(smpm_sim* s, int project) {
     CK(cudaMemsetAsync(s->dstats, 0, 2 * sizeof(DevStats), s->stream));
     CK(cudaMemsetAsync(s->derr, 0xFF, 8, s->stream));
     s->S = 0;
+    for (int t = 0; t < 2; ++t) {
+      int rcd = dense_insert(s, t);
+      if (rcd) return rcd;
+    }
     k_prologue_keys<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n_store, s->tab[0], s->bin, s->inv_h,
                                                     s->derr);
     CK(cudaGetLastError());
@@ -2081,6 +2125,8 @@ int smpm_sim_step(smpm_sim* s, double dt) {
   k_grid<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
                                          s->gv, gp, s->record, s->bx0, s->bx1);
   CK(cudaGetLastError());
+  rc = dense_insert(s, 1 - Sx);
+  if (rc) return rc;
   CK(cudaEventRecord(s->ev[2], s->stream));
   rc = launch_fused(s, true, 1);
   if (rc) return rc;
@@ -2203,6 +2249,31 @@ int smpm_sim_grid_size(smpm_sim* s, int64_t* n_blocks) {
 }
 
 int64_t smpm_sim_num_particles(const smpm_sim* s) { return s ? s->n : 0; }
+
+int smpm_sim_set_dense_domain(smpm_sim* s, const int32_t* bmin, const int32_t* bmax) {
+  if (!s || !bmin || !bmax) return set_err(SMPM_ERR_ARG, "null argument");
+  uint64_t nd = 1;
+  for (int a = 0; a < 3; ++a) {
+    if (bmax[a] < bmin[a]) return set_err(SMPM_ERR_CONFIG, "dense domain: node_max must be >= node_min on every axis");
+    if (bmin[a] < COORD_MIN || bmax[a] > COORD_MAX) return set_err(SMPM_ERR_KEY_RANGE, "dense domain outside the key range");
+    s->dbmin[a] = bmin[a];
+    s->dbshape[a] = bmax[a] - bmin[a] + 1;
+    nd *= uint64_t(s->dbshape[a]);
+  }
+  if (nd > (1ull << 25)) return set_err(SMPM_ERR_CAPACITY, "dense domain exceeds 2^25 blocks");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  s->dense = true;
+  if (nd + nd / 4 + 1024 > s->cap_b) {
+    int rc = grow_grid(s, uint32_t(nd + nd / 4 + 1024));
+    if (rc) return rc;
+  }
+  s->need_prologue = true;
+  return SMPM_OK;
+}
 
 int smpm_sim_set_slab(smpm_sim* s, int32_t bx0, int32_t bx1, int64_t pid_base, int64_t migrant_capacity) {
   if (!s || bx1 <= bx0) return set_err(SMPM_ERR_ARG, "invalid slab");

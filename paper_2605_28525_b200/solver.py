@@ -13,7 +13,11 @@ Differences a caller can observe:
   bit-exact with the reference);
 * ``Simulation`` evaluates the next step's stress at the end of ``step`` (in
   the fused kernel), so ``particles.F`` after a step is already return-mapped;
-* ``block_size`` must be 4 and ``backend`` must be ``"hash"``.
+* ``block_size`` must be 4.  ``backend`` takes the reference's names:
+  ``"hash"`` and ``"scan"`` both run the GPU hash-grid pipeline (the two CPU
+  constructions produce the same active set and bitwise-equal results in the
+  reference, test_acceptance.py:98-137); ``"dense"`` allocates every block of
+  the domain each step (the comparison baseline of ``bench.compare``).
 """
 
 import hashlib
@@ -27,7 +31,7 @@ from .errors import ConfigError, InactiveNodeError, KeyRangeError, SimulationErr
 from .grid_index import ActiveIndexMap
 from .materials import _degenerate_message, material_tables  # noqa: F401
 
-BACKENDS = ("hash",)
+BACKENDS = ("dense", "scan", "hash")
 BC_PLANE = 0
 BC_HEIGHTFIELD = 1
 NODE_BYTES = 8 * (1 + 3 + 3)  # reference accounting (solver.py:29-30)
@@ -221,7 +225,7 @@ class SimConfig:
         if not 0.0 < self.cfl <= 1.0:
             raise ConfigError(f"cfl must lie in (0, 1], got {self.cfl}")
         if self.backend not in BACKENDS:
-            raise ConfigError(f"unknown backend {self.backend!r}; the B200 build implements {list(BACKENDS)}")
+            raise ConfigError(f"unknown backend {self.backend!r}; expected one of {sorted(BACKENDS)}")
         if self.block_size != 4:
             raise ConfigError(f"block size must be 4 on the GPU grid (one u64 node mask per block), "
                               f"got {self.block_size}")
@@ -505,6 +509,11 @@ class Simulation:
         self._h = h
         if slab is not None:  # (bx0, bx1, pid_base, migrant_capacity): see slabs.py
             _lib.check(lib.smpm_sim_set_slab(h, *[int(v) for v in slab]), "set slab")
+        if config.backend == "dense":
+            bs = int(config.block_size)
+            bmin = (ctypes.c_int32 * 3)(*[int(v) // bs for v in config.node_min])
+            bmax = (ctypes.c_int32 * 3)(*[int(v) // bs for v in config.node_max])
+            _lib.check(lib.smpm_sim_set_dense_domain(h, bmin, bmax), "dense domain")
         self._upload(particles)
         self.t = 0.0
         self.step_count = 0

@@ -1,0 +1,101 @@
+"""Scenario runs, the dense baseline and the CLI on the GPU (cases follow the
+reference's T/test_bench.py and T/test_scenarios_io.py).  The shipped scenes
+(tests/golden/scenarios/, copied from the reference package) load unchanged
+and run on the GPU step; the active-node series and the dense allocation are
+checked bit-exactly against the oracle."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+from click.testing import CliRunner
+
+from paper_2605_28525_b200 import bench, scenarios
+from paper_2605_28525_b200.cli import main as cli_main
+
+pytestmark = pytest.mark.gpu
+SCEN = Path(__file__).resolve().parent / "golden" / "scenarios"
+STEMS = ("granular_collapse", "localized_flow", "sliding_box", "terrain_demo")
+
+
+def _oracle_run(o, sc, backend, dts):
+    ps = scenarios.build_particles(sc)
+    cfg = sc.sim
+    sim = o.OracleSimulation(ps, cfg.h, cfg.gravity, [r.model for r in sc.materials], sc.boundaries,
+                             backend=backend, deterministic=True, node_min=cfg.node_min, node_max=cfg.node_max)
+    return [(r["n_active"], r["n_allocated"]) for r in (sim.step(dt) for dt in dts)]
+
+
+@pytest.mark.parametrize("stem", STEMS)
+def test_shipped_scene_runs_like_oracle(oracle, stem):
+    sc = scenarios.load_config(SCEN / f"{stem}.yaml")
+    m = bench.run(sc, backend="hash", max_steps=4)
+    assert m.n_steps == 4 and m.backend == "hash" and m.n_particles == scenarios.build_particles(sc).n
+    dts = [s.dt for s in m.steps]
+    ref = _oracle_run(oracle, sc, "hash", dts)
+    assert [(s.n_active, s.n_allocated) for s in m.steps] == ref
+    assert m.r_active == bench.sparsity_ratio([r[0] for r in ref], m.n_dense)
+
+
+def test_dense_baseline_allocates_the_domain(oracle):
+    sc = scenarios.load_config(SCEN / "terrain_demo.yaml")
+    dense = bench.run(sc, backend="dense", max_steps=3)
+    sparse = bench.run(sc, backend="hash", max_steps=3)
+    dts = [s.dt for s in dense.steps]
+    ref = _oracle_run(oracle, sc, "dense", dts)
+    assert [(s.n_active, s.n_allocated) for s in dense.steps] == ref
+    assert all(s.n_allocated == dense.n_dense for s in dense.steps)
+    assert dense.n_active_series == sparse.n_active_series
+    rep = bench.compare(dense, sparse)
+    assert rep.memory_reduction == dense.n_dense / sparse.peak_alloc_nodes
+    assert rep.speedup > 0 and set(rep.phase_table()) == set(bench.PHASES)
+
+
+def test_dense_and_hash_trajectories_agree():
+    sc = scenarios.load_config(SCEN / "granular_collapse.yaml")
+    a = scenarios.build_simulation(sc, backend="dense")
+    b = scenarios.build_simulation(sc, backend="hash")
+    for _ in range(5):
+        dt = 0.8 * b.dt_bound()
+        sa, sb = a.step(dt), b.step(dt)
+        assert sa.n_active == sb.n_active
+    xa, xb = a.particles.x, b.particles.x
+    assert np.abs(xa - xb).max() <= 1e-6 * np.abs(xb).max()
+
+
+def test_frames_and_metrics_output(tmp_path):
+    sc = scenarios.load_config(SCEN / "terrain_demo.yaml")
+    m = bench.run(sc, max_steps=6, out_dir=tmp_path, record_conservation=True)
+    frames = sorted(tmp_path.glob("frame_*.csv"))
+    assert frames and frames[0].name == "frame_000000.csv"
+    pos, vel = scenarios.read_particles(frames[0])
+    assert pos.shape == (m.n_particles, 3)
+    rows, summary = scenarios.read_metrics(tmp_path / "metrics.csv")
+    assert len(rows) == m.n_steps and summary["physics_hash"] == sc.physics_hash()
+    assert "mass_sum_kg" in rows[0] and float(rows[0]["mass_sum_kg"]) > 0
+
+
+def test_compare_rejections():
+    sc = scenarios.load_config(SCEN / "terrain_demo.yaml")
+    a = bench.run(sc, backend="hash", max_steps=2)
+    b = bench.run(sc, backend="scan", max_steps=3)
+    with pytest.raises(ValueError):
+        bench.compare(a, b)
+    d = bench.run(sc, backend="dense", max_steps=2)
+    with pytest.raises(ValueError):
+        bench.compare(d, d)
+    with pytest.raises(ValueError):
+        bench.compare(d, b)
+
+
+def test_cli_run_and_compare(tmp_path):
+    cfg = str(SCEN / "sliding_box.yaml")
+    r = CliRunner().invoke(cli_main, ["run", cfg, "--backend", "hash", "--max-steps", "3", "--out", str(tmp_path)])
+    assert r.exit_code == 0, r.output
+    assert "sparsity ratio:" in r.output and (tmp_path / "metrics.csv").exists()
+    out = tmp_path / "cmp.csv"
+    r = CliRunner().invoke(cli_main, ["compare", cfg, "--sparse-backend", "hash", "--max-steps", "3",
+                                      "--out", str(out)])
+    assert r.exit_code == 0, r.output
+    rows, summary = scenarios.read_metrics(out)
+    assert {row["phase"] for row in rows} == set(bench.PHASES) and float(summary["memory_reduction"]) > 1

@@ -29,8 +29,10 @@ def test_config_validation():
     SimConfig(**base)
     with pytest.raises(ConfigError):
         SimConfig(**{**base, "h": 0.0})
+    for backend in ("dense", "scan", "hash"):  # the reference's backend names (solver.py:24)
+        assert SimConfig(**{**base, "backend": backend}).backend == backend
     with pytest.raises(ConfigError):
-        SimConfig(**{**base, "backend": "dense"})
+        SimConfig(**{**base, "backend": "octree"})
     with pytest.raises(ConfigError):
         SimConfig(**{**base, "block_size": 8})
     with pytest.raises(ConfigError):
