@@ -1696,10 +1696,8 @@ int run_prologue(smpm_sim* s, int project) {
     CK(cudaMemsetAsync(s->dstats, 0, 2 * sizeof(DevStats), s->stream));
     CK(cudaMemsetAsync(s->derr, 0xFF, 8, s->stream));
     s->S = 0;
-    for (int t = 0; t < 2; ++t) {
-      int rcd = dense_insert(s, t);
-      if (rcd) return rcd;
-    }
+    int rcd = dense_insert(s, 0);
+    if (rcd) return rcd;
     k_prologue_keys<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n_store, s->tab[0], s->bin, s->inv_h,
                                                     s->derr);
     CK(cudaGetLastError());
@@ -1721,6 +1719,8 @@ int run_prologue(smpm_sim* s, int project) {
       continue;
     }
     rc = scan_and_bin(s, 0, 0.0);
+    if (rc) return rc;
+    rc = dense_insert(s, 1);  // after scan1 reset table 1, before the P2G fills it
     if (rc) return rc;
     // every binned particle is copied to the other buffer, so the swap in
     // launch_fused keeps the full particle set even if the scatter overflows
