@@ -26,6 +26,8 @@ from .solver import (
     p2g,
 )
 from .sparse_hash import BlockHashTable, build_hash_sparse_grid
+from .scenarios import load_config, load_heightfield, sample_box
+from .bench import compare, run, sliding_box_oracle, sparsity_ratio
 
 __version__ = "0.1.0"
 
@@ -34,5 +36,6 @@ __all__ = [
     "KeyRangeError", "MaterialModel", "NodalFields", "ParticleSet", "SimConfig", "Simulation", "SimulationError",
     "SparseMpmError", "StepStats", "apply_friction_boundary", "block_of", "bspline_weights",
     "build_hash_sparse_grid", "count_active_nodes", "g2p", "grid_forces", "grid_update", "local_offset", "mix64",
-    "node_index", "p2g", "pack_key", "unpack_key", "update_stress",
+    "node_index", "p2g", "pack_key", "unpack_key", "update_stress", "load_config", "load_heightfield", "sample_box",
+    "compare", "run", "sliding_box_oracle", "sparsity_ratio",
 ]
