@@ -235,7 +235,7 @@ def ours(args):
     step_bytes = 204.0 * n + 80.0 * float(np.mean(nalloc))
     traffic = None
     tf = ROOT / "profiles" / "fused_traffic.json"
-    if tf.exists():
+    if tf.exists() and world == 1 and args.scale == 1.0:  # the ncu capture is of the full 1-GPU workload
         try:
             traffic = json.loads(tf.read_text()).get(args.config)
         except Exception:  # noqa: BLE001

@@ -145,6 +145,17 @@ class _Transport:
             torch.cuda.synchronize()  # the library consumes these on its own stream
         return out_l, out_r
 
+    def gather(self, arr):
+        """Every rank's float64 vector, stacked (one collective)."""
+        import torch
+
+        dist = self.dist
+        dev = self.device if self.nccl else torch.device("cpu")
+        t = torch.tensor(np.asarray(arr, dtype=np.float64), device=dev)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return np.stack([o.cpu().numpy() for o in out])
+
     def allreduce(self, arr, op="sum"):
         import torch
 
@@ -179,6 +190,7 @@ class DistributedSimulation:
         self.step_count = 0
         self.migrated = 0  # particles received from neighbours so far
         self._torch = torch
+        self._gvmax = None  # global max |v| after the last step (next dt bound)
         # step 0: P2G of the initial state on every rank, then the halo exchange
         nb = ctypes.c_int64(0)
         _lib.check(self.lib.smpm_sim_grid_size(self._h, ctypes.byref(nb)), "prologue")
@@ -211,40 +223,61 @@ class DistributedSimulation:
         _lib.check(self.lib.smpm_sim_migrants(self._h, side, _lib.ptr(out), n.value, ctypes.byref(n)), "migrants")
         return out
 
+    def _frame(self, blocks, parts):
+        """One message: a 16-byte header (int64 byte count of the block
+        records, pad) keeping the records 16-byte aligned, the block records
+        (BLOCK_REC_BYTES each), then particle records."""
+        torch = self._torch
+        if blocks is None and parts is None:
+            return None
+        nbytes = 0 if blocks is None else blocks.numel()
+        head = torch.tensor([nbytes, 0], dtype=torch.int64, device="cuda").view(torch.uint8)
+        return torch.cat([head] + [b for b in (blocks, parts) if b is not None])
+
+    def _unframe(self, msg):
+        if msg is None or msg.numel() == 0:
+            return None, None
+        nbytes = int(msg[:8].view(self._torch.int64).item())
+        blocks = msg[16:16 + nbytes].to("cuda")
+        parts = msg[16 + nbytes:].to("cuda")
+        return (blocks if nbytes else None), (parts if parts.numel() else None)
+
     def _exchange(self):
-        self._torch.cuda.synchronize()
-        # 1. partial sums of blocks outside the slab -> owners
-        from_l, from_r = self.tr.exchange(self._pack(0), self._pack(1))
-        self._unpack(from_l, False)
-        self._unpack(from_r, False)
+        """Two neighbour rounds per step: (1) partial sums of halo blocks and
+        departing particles, (2) the owners' boundary-layer sums back to the
+        left neighbour (which needs (1) applied first)."""
         self._torch.cuda.synchronize()
         self.sim.stream.synchronize()
-        # 2. owner's first layer (full sums) -> left neighbour
+        to_l = self._frame(self._pack(0), self._migrants(0))
+        to_r = self._frame(self._pack(1), self._migrants(1))
+        for msg in self.tr.exchange(to_l, to_r):
+            blocks, parts = self._unframe(msg)
+            self._unpack(blocks, False)
+            if parts is not None:
+                self.migrated += parts.numel() // PARTICLE_REC_BYTES
+                _lib.check(self.lib.smpm_sim_accept(self._h, _lib.ptr(parts), parts.numel() // PARTICLE_REC_BYTES),
+                           "accept")
+        self.sim.stream.synchronize()
         _, from_r = self.tr.exchange(self._pack(2), None)
         self._unpack(from_r, True)
-        self.sim.stream.synchronize()
-        # 3. departing particles
-        from_l, from_r = self.tr.exchange(self._migrants(0), self._migrants(1))
-        for buf in (from_l, from_r):
-            if buf is not None:
-                self.migrated += buf.numel() // PARTICLE_REC_BYTES
-                _lib.check(self.lib.smpm_sim_accept(self._h, _lib.ptr(buf), buf.numel() // PARTICLE_REC_BYTES),
-                           "accept")
         self.sim.stream.synchronize()
 
     # -- API ------------------------------------------------------------------
     def dt_bound(self):
-        vmax = float(self.lib.smpm_sim_vmax(self._h))
-        vmax = float(self.tr.allreduce([vmax], "max")[0])
-        return self.config.cfl * self.config.h / (self.sim._wave_speed + vmax)
+        if self._gvmax is None:
+            self._gvmax = float(self.tr.allreduce([float(self.lib.smpm_sim_vmax(self._h))], "max")[0])
+        return self.config.cfl * self.config.h / (self.sim._wave_speed + self._gvmax)
 
     def step(self, dt=None):
         cfg = self.config
         if dt is None:
             dt = cfg.dt if cfg.dt is not None else self.dt_bound()
         st = self.sim.step(float(dt))
-        red = self.tr.allreduce([st.n_active, st.n_allocated, st.mass_sum or 0.0,
-                                 *(st.mom_sum if st.mom_sum is not None else (0.0, 0.0, 0.0))])
+        # one collective for the step's global stats and the next dt bound
+        rows = self.tr.gather([float(self.lib.smpm_sim_vmax(self._h)), st.n_active, st.n_allocated,
+                               st.mass_sum or 0.0, *(st.mom_sum if st.mom_sum is not None else (0.0, 0.0, 0.0))])
+        self._gvmax = float(rows[:, 0].max())
+        red = rows[:, 1:].sum(axis=0)
         self._exchange()
         self.t += st.dt
         self.step_count += 1
