@@ -177,6 +177,7 @@ def ours(args):
         per_col = sc.particles.n // max(1, slab[3] - slab[2])
     else:
         sc = make_scene(args.config, args.scale)
+    sc.config.deterministic = bool(args.deterministic)
     n_local = sc.particles.n
 
     def make_sim(ps):
@@ -272,7 +273,8 @@ def ours(args):
         "config": {"workload": CONFIG_NAMES[args.config], "config": args.config if world == 1 else "C5",
                    "n_particles": n, "h": sc.config.h, "ppc": 2, "mean_allocated_nodes": float(np.mean(nalloc)),
                    "l2": "inputs larger than L2 (state %.1f GB)" % (n * 242 / 1e9),
-                   "dt": "CFL bound (cfl=0.4)", "parallelism": f"slab{world}" if world > 1 else "single"},
+                   "dt": "CFL bound (cfl=0.4)", "parallelism": f"slab{world}" if world > 1 else "single",
+                   "deterministic": bool(args.deterministic)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_g2p2g (G2P+F+return map+next P2G)",
                      "peak_kind": peak_kind, "kernel_ms": ph["fused"],
@@ -303,6 +305,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(CONFIG_NAMES))
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of the C4 release columns")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bitwise run-to-run reproducible mode (int64 fixed-point grid sums)")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

@@ -102,6 +102,8 @@ struct DevStats {
   unsigned long long n_active;
   uint32_t bnd_bits[3];     // maxima of the P2G contribution bounds (mass, momentum, force) into this table
   uint32_t scale_ovf;       // a contribution exceeded the fixed-point scale: replay the P2G
+  float scale_inv[3];       // inverse fixed-point scales of the P2G into this table (deterministic mode)
+  uint32_t pad3;
   double dt;
   double mass_sum, mom_sum[3];
 };
@@ -302,7 +304,7 @@ __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, u
 // table T for reuse by the next P2G).
 __global__ void __launch_bounds__(256, 2) k_grid(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
                                                  float4* __restrict__ acc, float4* __restrict__ gv, GridParams gp,
-                                                 int record, int bx0, int bx1) {
+                                                 int record, int bx0, int bx1, unsigned long long* acc_fx) {
   __shared__ Boundary sbc[8];
   if (threadIdx.x < gp.n_bc && threadIdx.x < 8) sbc[threadIdx.x] = gp.bc[threadIdx.x];
   __syncthreads();
@@ -321,10 +323,30 @@ __global__ void __launch_bounds__(256, 2) k_grid(TableDev S, TableDev T, DevStat
     const uint64_t key = S.hv.active_keys[r];
     const size_t c0 = size_t(r) * 64 + (li << 4) + (lj << 2);
     float4 a[4], b[4];
+    if (acc_fx) {
+      // deterministic mode: exact int64 fixed-point sums -> values (the scales
+      // are powers of two, the sums < 2^53: the conversion is exact)
+      const double iSm = stS->scale_inv[0], iSp = stS->scale_inv[1], iSf = stS->scale_inv[2];
 #pragma unroll
-    for (int lk = 0; lk < 4; ++lk) {
-      a[lk] = __ldcs(&acc[2 * (c0 + lk)]);
-      b[lk] = __ldcs(&acc[2 * (c0 + lk) + 1]);
+      for (int lk = 0; lk < 4; ++lk) {
+        unsigned long long* q = acc_fx + 8 * (c0 + lk);
+        long long v[8];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          v[f] = (long long)__ldcs(q + f);
+          q[f] = 0ull;
+        }
+        a[lk] = make_float4(float(double(v[0]) * iSm), float(double(v[1]) * iSp), float(double(v[2]) * iSp),
+                            float(double(v[3]) * iSp));
+        b[lk] = make_float4(float(double(v[4]) * iSf), float(double(v[5]) * iSf), float(double(v[6]) * iSf),
+                            float(v[7]));
+      }
+    } else {
+#pragma unroll
+      for (int lk = 0; lk < 4; ++lk) {
+        a[lk] = __ldcs(&acc[2 * (c0 + lk)]);
+        b[lk] = __ldcs(&acc[2 * (c0 + lk) + 1]);
+      }
     }
     int bi, bj, bk;
     unpack_key(key, bi, bj, bk);
@@ -455,6 +477,7 @@ struct FusedArgs {
   TableDev S;                 // table receiving the next P2G
   const float4* gv;           // grid velocity of B (float4 per node)
   float4* acc;                // accumulators of S (2 float4 per node)
+  unsigned long long* acc_fx; // deterministic mode: int64 fixed-point accumulators (8 per node), else null
   uint32_t* bin_out;          // cell keys (rank*64+cell) of dst particles in S
   const Material* mats;
   int n_mat;
@@ -553,7 +576,8 @@ __device__ __forceinline__ uint32_t touched27(uint32_t mx, uint32_t my, uint32_t
 // Global (slow-path) scatter of a particle that moved outside its block's
 // 8^3 arena: direct inserts and float atomics (rare: |dx| > 1 cell/step).
 __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float d[3], float m, const float v[3],
-                               const float C[9], const float M[6], uint32_t& binv, bool bin) {
+                               const float C[9], const float M[6], uint32_t& binv, bool bin, float Sm, float Sp,
+                               float Sf) {
   float w[3][3], g[3][3];
   for (int a = 0; a < 3; ++a) bspline(d[a], w[a], g[a]);
   const float h = float(A.h), ih = float(A.inv_h);
@@ -576,6 +600,13 @@ __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float 
         float f1 = -(M[3] * gx + M[1] * gy + M[5] * gz);
         float f2 = -(M[4] * gx + M[5] * gy + M[2] * gz);
         size_t node = size_t(r) * 64 + l;
+        if (A.acc_fx) {  // deterministic mode: the launch's fixed-point scales
+          const float fv[NF] = {wm * Sm, wm * mv0 * Sp, wm * mv1 * Sp, wm * mv2 * Sp, f0 * Sf, f1 * Sf, f2 * Sf};
+          unsigned long long* o = A.acc_fx + 8 * node;
+          for (int f = 0; f < NF; ++f) atomicAdd(o + f, (unsigned long long)(long long)__float2int_rn(fv[f]));
+          atomicAdd(o + 7, 1ull);
+          continue;
+        }
         red_v4(&A.acc[2 * node], wm, wm * mv0, wm * mv1, wm * mv2);
         red_v4(&A.acc[2 * node + 1], f0, f1, f2, 1.f);  // .w: contribution count K (n_active)
       }
@@ -760,6 +791,15 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
 #pragma unroll
       for (int f = 0; f < NF; ++f) vals[f] = float(int(uint32_t(sm.acc[q][f][ad]) - bias));
       const size_t node = size_t(rk) * 64 + l;
+      if (A.acc_fx) {
+        // deterministic mode: integer sums are order-independent
+        unsigned long long* o = A.acc_fx + 8 * node;
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+          atomicAdd(o + f, (unsigned long long)(long long)int(uint32_t(sm.acc[q][f][ad]) - bias));
+        atomicAdd(o + 7, (unsigned long long)K);
+        continue;
+      }
       red_v4(&A.acc[2 * node], vals[0] * iSm, vals[1] * iSp, vals[2] * iSp, vals[3] * iSp);
       red_v4(&A.acc[2 * node + 1], vals[4] * iSf, vals[5] * iSf, vals[6] * iSf, float(K));
     }
@@ -1030,7 +1070,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
           mx_m = fmaxf(mx_m, bm);
           mx_p = fmaxf(mx_p, bp);
           mx_f = fmaxf(mx_f, bf);
-          if (!A.measure && !far && (bm * Sm > FX_LIM || bp * Sp > FX_LIM || bf * Sf > FX_LIM)) {
+          if (!A.measure && (!far || A.acc_fx) && (bm * Sm > FX_LIM || bp * Sp > FX_LIM || bf * Sf > FX_LIM)) {
             scale_ovf = true;  // the step's P2G is replayed from the records with measured scales
             sovf = true;
           }
@@ -1105,7 +1145,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
             binv = BAD_KEY;
           }
         } else if (!A.measure && ok && far) {
-          scatter_global(A, nb, d1, m, vn, Cn, M, binv, mig < 0);
+          scatter_global(A, nb, d1, m, vn, Cn, M, binv, mig < 0, Sm, Sp, Sf);
         } else {
           binv = BAD_KEY;
         }
@@ -1178,6 +1218,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     if (uf) atomicMax(&A.bnd_dst[2], uf);
   }
   if (scale_ovf) atomicOr(&A.stS->scale_ovf, 1u);
+  if (blockIdx.x == 0 && tid < 3 && !A.measure) A.stS->scale_inv[tid] = sm.sc[3 + tid];
 }
 
 // ------------------------------------------------------- state transfer
@@ -1411,6 +1452,7 @@ struct smpm_sim {
   int S = 0;  // table holding the current particles' bins
   float4* acc = nullptr;
   float4* gv = nullptr;
+  unsigned long long* acc_fx = nullptr;  // deterministic mode accumulators
   DevStats* dstats = nullptr;  // [2]
   unsigned long long* derr = nullptr;
   Material* dmats = nullptr;
@@ -1533,6 +1575,10 @@ int alloc_grid(smpm_sim* s) {
   DA(s->acc, size_t(cb) * 64 * 2);
   DA(s->gv, size_t(cb) * 64);
   CK(cudaMemsetAsync(s->acc, 0, size_t(cb) * 64 * 32, s->stream));
+  if (s->deterministic) {
+    DA(s->acc_fx, size_t(cb) * 64 * 8);
+    CK(cudaMemsetAsync(s->acc_fx, 0, size_t(cb) * 64 * 64, s->stream));
+  }
   return SMPM_OK;
 }
 
@@ -1547,6 +1593,7 @@ FusedArgs fused_args(smpm_sim* s, int B, int dstbuf, int project) {
   A.S = s->tab[1 - B];
   A.gv = s->gv;
   A.acc = s->acc;
+  A.acc_fx = s->acc_fx;
   A.bin_out = s->bin;
   A.mats = s->dmats;
   A.n_mat = s->n_mat;
@@ -1657,6 +1704,7 @@ int grow_grid(smpm_sim* s, uint32_t need) {
     for (void* p : ps) grid_ptrs.push_back(p);
   }
   grid_ptrs.push_back(s->acc);
+  grid_ptrs.push_back(s->acc_fx);
   grid_ptrs.push_back(s->gv);
   std::vector<void*> keep;
   for (void* p : s->allocs) {
@@ -1693,6 +1741,7 @@ int run_prologue(smpm_sim* s, int project) {
       CK(cudaMemsetAsync(T.cell_count, 0, size_t(s->cap_b) * 64 * 4, s->stream));
     }
     CK(cudaMemsetAsync(s->acc, 0, size_t(s->cap_b) * 64 * 32, s->stream));
+    if (s->acc_fx) CK(cudaMemsetAsync(s->acc_fx, 0, size_t(s->cap_b) * 64 * 64, s->stream));
     CK(cudaMemsetAsync(s->dstats, 0, 2 * sizeof(DevStats), s->stream));
     CK(cudaMemsetAsync(s->derr, 0xFF, 8, s->stream));
     s->S = 0;
@@ -2123,7 +2172,7 @@ int smpm_sim_step(smpm_sim* s, double dt) {
   CK(cudaEventRecord(s->ev[1], s->stream));
   GridParams gp = grid_params(s);
   k_grid<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
-                                         s->gv, gp, s->record, s->bx0, s->bx1);
+                                         s->gv, gp, s->record, s->bx0, s->bx1, s->acc_fx);
   CK(cudaGetLastError());
   rc = dense_insert(s, 1 - Sx);
   if (rc) return rc;
@@ -2208,7 +2257,18 @@ int smpm_sim_query_grid(smpm_sim* s, int32_t* blocks, float* mass, float* mom, f
   std::vector<uint64_t> keys(nb);
   std::vector<float> a(size_t(nb) * 64 * 8);
   CK(cudaMemcpy(keys.data(), T.hv.active_keys, size_t(nb) * 8, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(a.data(), s->acc, a.size() * 4, cudaMemcpyDeviceToHost));
+  if (s->acc_fx) {  // deterministic mode: convert the int64 sums with the P2G's scales
+    std::vector<long long> fx(size_t(nb) * 64 * 8);
+    CK(cudaMemcpy(fx.data(), s->acc_fx, fx.size() * 8, cudaMemcpyDeviceToHost));
+    DevStats st;
+    CK(cudaMemcpy(&st, s->dstats + s->S, sizeof(DevStats), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < size_t(nb) * 64; ++i)
+      for (int f = 0; f < 8; ++f)
+        a[8 * i + f] = f == 7 ? float(fx[8 * i + 7])
+                              : float(double(fx[8 * i + f]) * st.scale_inv[f == 0 ? 0 : (f < 4 ? 1 : 2)]);
+  } else {
+    CK(cudaMemcpy(a.data(), s->acc, a.size() * 4, cudaMemcpyDeviceToHost));
+  }
   for (uint32_t r = 0; r < nb; ++r) {
     int bi, bj, bk;
     unpack_key(keys[r], bi, bj, bk);
@@ -2277,6 +2337,7 @@ int smpm_sim_set_dense_domain(smpm_sim* s, const int32_t* bmin, const int32_t* b
 
 int smpm_sim_set_slab(smpm_sim* s, int32_t bx0, int32_t bx1, int64_t pid_base, int64_t migrant_capacity) {
   if (!s || bx1 <= bx0) return set_err(SMPM_ERR_ARG, "invalid slab");
+  if (s->deterministic) return set_err(SMPM_ERR_CONFIG, "deterministic mode is single-GPU");
   CK(cudaSetDevice(s->device));
   s->bx0 = bx0;
   s->bx1 = bx1;

@@ -69,9 +69,10 @@ def compare_grid(oracle, sim, cfg, mats, ref_state):
     return dict(mass=normwise(mg, mr), mom=normwise(pg, pr), force=normwise(fg, frr))
 
 
-@pytest.mark.parametrize("bcs", ["mixed", "none"])
-def test_steps_match_oracle(oracle, bcs):
+@pytest.mark.parametrize("bcs,det", [("mixed", False), ("none", False), ("mixed", True)])
+def test_steps_match_oracle(oracle, bcs, det):
     ps, cfg, mats, bc = column_scene(bcs=bcs)
+    cfg.deterministic = det  # deterministic mode: int64 fixed-point grid sums
     sim = Simulation(ps, cfg, mats, bc)
     worst = {}
     for s in range(8):
@@ -96,6 +97,26 @@ def test_steps_match_oracle(oracle, bcs):
     print("worst per-step errors:", {k: f"{v:.2e}" for k, v in worst.items()})
     for k, e in worst.items():
         assert e <= TOL[k], (k, e)
+
+
+def test_deterministic_mode_is_bitwise_reproducible():
+    """deterministic=True: node sums are int64 fixed point (order-independent),
+    so two runs agree bit for bit whatever the hash ranks and atomic order."""
+    ps, cfg, mats, bc = column_scene(vx=3.0)
+    cfg.deterministic = True
+    runs = []
+    for _ in range(2):
+        sim = Simulation(ps.copy(), cfg, mats, bc, block_capacity=64)  # growth + replay on the way
+        for s in range(12):
+            sim.step(2e-4)
+        p = sim.particles
+        runs.append((p.x.copy(), p.v.copy(), p.C.copy(), p.F.copy()))
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)
+    ref = Simulation(ps.copy(), SimConfig(**{**cfg.__dict__, "deterministic": False}), mats, bc)
+    for s in range(12):
+        ref.step(2e-4)
+    assert np.abs(ref.particles.x - runs[0][0]).max() < 1e-6 * np.abs(runs[0][0]).max()
 
 
 def test_capacity_growth_replays_exactly(oracle):
