@@ -234,11 +234,12 @@ def ours(args):
     fused_bytes = 204.0 * n_local + 40.0 * n_alloc_local  # SURVEY 8d per-unit figures
     achieved = fused_bytes / (ph["fused"] * 1e-3) / 1e9
     step_bytes = 204.0 * n + 80.0 * float(np.mean(nalloc))
-    traffic = None
+    traffic, atomics = None, None
     tf = ROOT / "profiles" / "fused_traffic.json"
     if tf.exists() and world == 1 and args.scale == 1.0:  # the ncu capture is of the full 1-GPU workload
         try:
-            traffic = json.loads(tf.read_text()).get(args.config)
+            prof = json.loads(tf.read_text())
+            traffic, atomics = prof.get(args.config), prof.get(f"{args.config}_atomics")
         except Exception:  # noqa: BLE001
             traffic = None
     del sim, inner
@@ -277,7 +278,7 @@ def ours(args):
                    "deterministic": bool(args.deterministic)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_g2p2g (G2P+F+return map+next P2G)",
-                     "peak_kind": peak_kind, "kernel_ms": ph["fused"],
+                     "peak_kind": peak_kind, "kernel_ms": ph["fused"], "atomics": atomics,
                      "step_frac": step_bytes / world / (ms / args.steps * 1e-3) / 1e9 / peak},
         "phases_ms": {"map_build(scan+bin)": ph["map"], "grid_update": ph["grid"], "fused": ph["fused"]},
         "e2e": {"value": e2e_value, "unit": METRIC,
