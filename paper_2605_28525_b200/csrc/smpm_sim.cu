@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -1814,11 +1815,22 @@ bool is_host_ptr(const void* p) {
   return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
 }
 
+// One process-wide pair of pinned buffers (cudaHostAlloc of 384 MB costs tens
+// of ms; simulations share them, one transfer at a time).
+std::mutex g_pin_mu;
+unsigned char* g_pin[2] = {nullptr, nullptr};
+constexpr size_t PIN_BYTES = size_t(192) << 20;
+
 int ensure_pinned(smpm_sim* s) {
   if (s->pin[0]) return SMPM_OK;
-  s->pin_bytes = size_t(192) << 20;
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (int b = 0; b < 2; ++b)
+      if (!g_pin[b]) CK(cudaHostAlloc(reinterpret_cast<void**>(&g_pin[b]), PIN_BYTES, cudaHostAllocPortable));
+  }
+  s->pin_bytes = PIN_BYTES;
   for (int b = 0; b < 2; ++b) {
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&s->pin[b]), s->pin_bytes, cudaHostAllocDefault));
+    s->pin[b] = g_pin[b];
     CK(cudaEventCreateWithFlags(&s->pin_ev[b], cudaEventDisableTiming));
   }
   s->host_threads = std::max(1, std::min(32, int(std::thread::hardware_concurrency())));
@@ -1862,6 +1874,7 @@ int upload_host(smpm_sim* s, int64_t n, const double* x, const double* v, const 
                 const double* m, const double* V0, const int64_t* mat) {
   int rc = ensure_pinned(s);
   if (rc) return rc;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
   const int64_t CH = int64_t(s->pin_bytes / 128);
   for (int64_t k = 0, off = 0; off < n; ++k, off += CH) {
     const int b = int(k & 1);
@@ -1874,6 +1887,8 @@ int upload_host(smpm_sim* s, int64_t n, const double* x, const double* v, const 
     CK(cudaMemcpyAsync(s->state[0].rec + off * 8, dst, size_t(c) * 128, cudaMemcpyHostToDevice, s->stream));
     CK(cudaEventRecord(s->pin_ev[b], s->stream));
   }
+  // the shared pinned buffers are free again only when the copies are done
+  for (int b = 0; b < 2; ++b) CK(cudaEventSynchronize(s->pin_ev[b]));
   return SMPM_OK;
 }
 
@@ -1881,6 +1896,7 @@ int upload_host(smpm_sim* s, int64_t n, const double* x, const double* v, const 
 int download_xv_host(smpm_sim* s, double* x, double* v) {
   int rc = ensure_pinned(s);
   if (rc) return rc;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
   const int64_t n = s->n;
   const int64_t CH = int64_t(s->pin_bytes / 48);
   uint32_t* inv = nullptr;
@@ -2031,10 +2047,8 @@ int smpm_sim_destroy(smpm_sim* s) {
   if (s->hstats) cudaFreeHost(s->hstats);
   if (s->herr) cudaFreeHost(s->herr);
   if (s->hcount) cudaFreeHost(s->hcount);
-  for (int b = 0; b < 2; ++b) {
-    if (s->pin[b]) cudaFreeHost(s->pin[b]);
+  for (int b = 0; b < 2; ++b)  // the pinned buffers are process-wide
     if (s->pin_ev[b]) cudaEventDestroy(s->pin_ev[b]);
-  }
   for (int i = 0; i < 5; ++i) cudaEventDestroy(s->ev[i]);
   if (s->own_stream) cudaStreamDestroy(s->stream);
   delete s;
