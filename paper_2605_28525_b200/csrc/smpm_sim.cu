@@ -2376,7 +2376,6 @@ int smpm_sim_exchange_pack(smpm_sim* s, int mode, void* out, int64_t cap_blocks,
     int rc = smpm_sim_sync(s, nullptr);
     if (rc) return rc;
   }
-  uint32_t* cnt = s->mig_count ? s->mig_count : nullptr;
   uint32_t* dcnt = nullptr;
   CK(cudaMallocAsync(&dcnt, 4, s->stream));
   CK(cudaMemsetAsync(dcnt, 0, 4, s->stream));
@@ -2387,7 +2386,6 @@ int smpm_sim_exchange_pack(smpm_sim* s, int mode, void* out, int64_t cap_blocks,
   CK(cudaMemcpyAsync(&h, dcnt, 4, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaFreeAsync(dcnt, s->stream));
   CK(cudaStreamSynchronize(s->stream));
-  (void)cnt;
   *n_out = int64_t(h);
   if (int64_t(h) > cap_blocks) return set_err(SMPM_ERR_CAPACITY, "exchange buffer too small");
   return SMPM_OK;
