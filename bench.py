@@ -166,7 +166,10 @@ def ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     dist = None
-    if world > 1:
+    # SMPM_FORCE_DIST=1 runs the slab code path at world size 1 (exercises the
+    # NCCL plumbing on a 1-GPU box: init, all_gather, empty neighbour rounds)
+    distributed = world > 1 or os.environ.get("SMPM_FORCE_DIST") == "1"
+    if distributed:
         import torch.distributed as dist
 
         dist.init_process_group(os.environ.get("SMPM_DIST_BACKEND", "nccl"))
@@ -181,7 +184,7 @@ def ours(args):
     n_local = sc.particles.n
 
     def make_sim(ps):
-        if world == 1:
+        if not distributed:
             return Simulation(ps, sc.config, sc.materials, sc.boundaries)
         from paper_2605_28525_b200.slabs import DistributedSimulation
 
@@ -189,14 +192,14 @@ def ours(args):
                                      pid_base=slab[2] * per_col)
 
     def max_over_ranks(x):
-        if world == 1:
+        if not distributed:
             return x
         t = torch.tensor([x], device="cuda" if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x):
-        if world == 1:
+        if not distributed:
             return x
         t = torch.tensor([x], device="cuda" if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t)
@@ -205,14 +208,14 @@ def ours(args):
     n = int(sum_over_ranks(n_local))
     # ---- value: device-resident state, K steps timed on the sim's stream
     sim = make_sim(sc.particles)
-    inner = sim if world == 1 else sim.sim
+    inner = sim.sim if distributed else sim
     stream = inner.stream
     for _ in range(args.warmup):
         sim.step()
     hist = {"map": [], "grid": [], "fused": []}
     nalloc = []
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local % max(1, torch.cuda.device_count())) as clk:
@@ -247,13 +250,13 @@ def ours(args):
     # ---- e2e: public API from host buffers (upload + K steps + download x,v)
     host = sc.particles
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     t0 = time.perf_counter()
     sim2 = make_sim(host)
     for _ in range(args.steps):
         sim2.step()
-    if world == 1:
+    if not distributed:
         out_x = np.empty_like(host.x)
         out_v = np.empty_like(host.v)
         _lib.check(_lib.load().smpm_sim_get_particles(sim2._h, out_x.ctypes.data, out_v.ctypes.data, None, None,
@@ -292,7 +295,7 @@ def ours(args):
                                 if k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -1488,6 +1488,8 @@ struct smpm_sim {
   uint32_t mig_cap = 0;
   bool in_flight = false; // a step was launched and not yet synced
   uint32_t* hcount = nullptr;  // pinned: counter/overflow of the table just filled
+  uint32_t* xcount = nullptr;  // device: block count of an exchange pack (per call, no allocation)
+  uint32_t* hxcount = nullptr; // pinned host copy
   std::vector<smpm_material> host_mats;
   // host <-> device transfer pipeline (pinned double buffer, host threads)
   unsigned char* pin[2] = {nullptr, nullptr};
@@ -2028,6 +2030,9 @@ int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
   CK(cudaMallocHost(&s->hstats, 2 * sizeof(DevStats)));
   CK(cudaMallocHost(&s->herr, sizeof(unsigned long long)));
   CK(cudaMallocHost(&s->hcount, 2 * sizeof(uint32_t)));
+  CK(cudaMallocHost(&s->hxcount, 4 * sizeof(uint32_t)));
+  rc = dalloc(s, &s->xcount, 4);
+  if (rc) return rc;
   CK(cudaFuncSetAttribute(k_g2p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes())));
   CK(cudaFuncSetAttribute(k_g2p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes())));
   int occ = 0, sms = 0;
@@ -2047,6 +2052,7 @@ int smpm_sim_destroy(smpm_sim* s) {
   if (s->hstats) cudaFreeHost(s->hstats);
   if (s->herr) cudaFreeHost(s->herr);
   if (s->hcount) cudaFreeHost(s->hcount);
+  if (s->hxcount) cudaFreeHost(s->hxcount);
   for (int b = 0; b < 2; ++b)  // the pinned buffers are process-wide
     if (s->pin_ev[b]) cudaEventDestroy(s->pin_ev[b]);
   for (int i = 0; i < 5; ++i) cudaEventDestroy(s->ev[i]);
@@ -2376,16 +2382,13 @@ int smpm_sim_exchange_pack(smpm_sim* s, int mode, void* out, int64_t cap_blocks,
     int rc = smpm_sim_sync(s, nullptr);
     if (rc) return rc;
   }
-  uint32_t* dcnt = nullptr;
-  CK(cudaMallocAsync(&dcnt, 4, s->stream));
-  CK(cudaMemsetAsync(dcnt, 0, 4, s->stream));
+  CK(cudaMemsetAsync(s->xcount, 0, 4, s->stream));
   k_pack_blocks<<<148 * 8, 256, 0, s->stream>>>(s->tab[s->S], s->acc, mode, s->bx0, s->bx1,
-                                                reinterpret_cast<BlockRec*>(out), dcnt, uint32_t(cap_blocks));
+                                                reinterpret_cast<BlockRec*>(out), s->xcount, uint32_t(cap_blocks));
   CK(cudaGetLastError());
-  uint32_t h = 0;
-  CK(cudaMemcpyAsync(&h, dcnt, 4, cudaMemcpyDeviceToHost, s->stream));
-  CK(cudaFreeAsync(dcnt, s->stream));
+  CK(cudaMemcpyAsync(s->hxcount, s->xcount, 4, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
+  const uint32_t h = *s->hxcount;
   *n_out = int64_t(h);
   if (int64_t(h) > cap_blocks) return set_err(SMPM_ERR_CAPACITY, "exchange buffer too small");
   return SMPM_OK;
@@ -2406,7 +2409,7 @@ int smpm_sim_migrants(smpm_sim* s, int side, void* out, int64_t cap, int64_t* n)
   CK(cudaSetDevice(s->device));
   *n = 0;
   if (!s->mig_count) return SMPM_OK;
-  uint32_t c[2];
+  uint32_t* c = s->hxcount;
   CK(cudaMemcpyAsync(c, s->mig_count, 8, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
   if (c[side] > s->mig_cap) return set_err(SMPM_ERR_CAPACITY, "migrant buffer overflow");

@@ -104,22 +104,23 @@ class _Transport:
         left = self.rank - 1 if self.rank > 0 else None
         right = self.rank + 1 if self.rank + 1 < self.world else None
         dev = self.device
-        # sizes first
+        # sizes first (one persistent int64[4] tensor: send l, send r, recv l, recv r)
         n_to = {"l": 0 if to_left is None else to_left.numel(), "r": 0 if to_right is None else to_right.numel()}
         sz_dev = dev if self.nccl else torch.device("cpu")
-        send_l = torch.tensor([n_to["l"]], dtype=torch.int64, device=sz_dev)
-        send_r = torch.tensor([n_to["r"]], dtype=torch.int64, device=sz_dev)
-        recv_l = torch.zeros(1, dtype=torch.int64, device=sz_dev)
-        recv_r = torch.zeros(1, dtype=torch.int64, device=sz_dev)
+        if left is None and right is None:
+            return None, None
+        if getattr(self, "_sz", None) is None:
+            self._sz = torch.zeros(4, dtype=torch.int64, device=sz_dev)
+        sz = self._sz
+        sz.copy_(torch.tensor([n_to["l"], n_to["r"], 0, 0], dtype=torch.int64))
         ops = []
         if left is not None:
-            ops += [dist.P2POp(dist.isend, send_l, left, self.group), dist.P2POp(dist.irecv, recv_l, left, self.group)]
+            ops += [dist.P2POp(dist.isend, sz[0:1], left, self.group), dist.P2POp(dist.irecv, sz[2:3], left, self.group)]
         if right is not None:
-            ops += [dist.P2POp(dist.isend, send_r, right, self.group), dist.P2POp(dist.irecv, recv_r, right, self.group)]
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-        nl, nr = int(recv_l.item()), int(recv_r.item())
+            ops += [dist.P2POp(dist.isend, sz[1:2], right, self.group), dist.P2POp(dist.irecv, sz[3:4], right, self.group)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        nl, nr = (int(v) for v in sz[2:].tolist())
         bufs = {}
         ops = []
         if left is not None:
@@ -191,6 +192,8 @@ class DistributedSimulation:
         self.migrated = 0  # particles received from neighbours so far
         self._torch = torch
         self._gvmax = None  # global max |v| after the last step (next dt bound)
+        self._xcap = [4096, 4096, 4096]  # halo exchange buffers (blocks) per pack mode
+        self._xbuf = [None, None, None]
         # step 0: P2G of the initial state on every rank, then the halo exchange
         nb = ctypes.c_int64(0)
         _lib.check(self.lib.smpm_sim_grid_size(self._h, ctypes.byref(nb)), "prologue")
@@ -198,14 +201,20 @@ class DistributedSimulation:
 
     # -- exchange -------------------------------------------------------------
     def _pack(self, mode):
+        """Halo block records of one kind into a persistent buffer (grown on
+        demand; the C call reports the count, and overflow as CAPACITY)."""
         torch = self._torch
-        nb = ctypes.c_int64(0)
-        _lib.check(self.lib.smpm_sim_grid_size(self._h, ctypes.byref(nb)), "grid size")
-        cap = max(int(nb.value), 1)
-        buf = torch.empty(cap * BLOCK_REC_BYTES, dtype=torch.uint8, device="cuda")
-        n = ctypes.c_int64(0)
-        _lib.check(self.lib.smpm_sim_exchange_pack(self._h, mode, _lib.ptr(buf), cap, ctypes.byref(n)), "pack")
-        return buf[: n.value * BLOCK_REC_BYTES] if n.value else None
+        while True:
+            cap, buf = self._xcap[mode], self._xbuf[mode]
+            if buf is None:
+                buf = self._xbuf[mode] = torch.empty(cap * BLOCK_REC_BYTES, dtype=torch.uint8, device="cuda")
+            n = ctypes.c_int64(0)
+            rc = self.lib.smpm_sim_exchange_pack(self._h, mode, _lib.ptr(buf), cap, ctypes.byref(n))
+            if rc == _lib.ERR_CAPACITY and n.value > cap:
+                self._xcap[mode], self._xbuf[mode] = 2 * int(n.value), None
+                continue
+            _lib.check(rc, "pack")
+            return buf[: n.value * BLOCK_REC_BYTES] if n.value else None
 
     def _unpack(self, buf, set_):
         if buf is None or buf.numel() == 0:
