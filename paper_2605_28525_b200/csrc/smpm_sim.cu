@@ -17,6 +17,7 @@
 // state G2P(n) writes, so they run in G2P(n)'s epilogue (a prologue kernel
 // does them for step 0 and after host-side edits).
 #include <cuda_runtime.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1835,7 +1836,12 @@ int ensure_pinned(smpm_sim* s) {
     s->pin[b] = g_pin[b];
     CK(cudaEventCreateWithFlags(&s->pin_ev[b], cudaEventDisableTiming));
   }
-  s->host_threads = std::max(1, std::min(32, int(std::thread::hardware_concurrency())));
+  // threads this process may run on (the affinity mask, not the machine size)
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  const int avail = sched_getaffinity(0, sizeof(set), &set) == 0 ? CPU_COUNT(&set)
+                                                                : int(std::thread::hardware_concurrency());
+  s->host_threads = std::max(1, std::min(32, avail));
   return SMPM_OK;
 }
 
