@@ -152,7 +152,8 @@ def check(rc, what="libsmpm call"):
     if rc == ERR_KEY_RANGE:
         raise KeyRangeError("particle stencil block outside packable coordinate range")
     if rc == ERR_INACTIVE:
-        raise InactiveNodeError("particle stencil node outside active grid")
+        raise InactiveNodeError("a particle stencil node is outside the active grid; with the dense backend this means "
+                                "a particle left the declared domain")
     if rc == ERR_CONFIG:
         raise ConfigError(msg)
     raise RuntimeError(f"{msg} (status {rc})")

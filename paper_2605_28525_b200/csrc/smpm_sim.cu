@@ -491,6 +491,7 @@ struct FusedArgs {
   unsigned long long* err;
   int project;
   int measure;                // 1: bounds only (prologue pass 1), nothing is written
+  int dbox_lo[3], dbox_hi[3]; // dense mode: the allocated block box (stencils leaving it -> ERR_INACTIVE)
   // slab decomposition (multi-GPU): this rank owns base blocks bx in [bx0, bx1)
   int bx0, bx1;
   float4* mig[2];        // departing particle records (left, right)
@@ -587,6 +588,9 @@ __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float 
     for (int oj = 0; oj < 3; ++oj)
       for (int ok = 0; ok < 3; ++ok) {
         int n0 = nb[0] + oi, n1 = nb[1] + oj, n2 = nb[2] + ok;
+        if ((n0 >> 2) < A.dbox_lo[0] || (n0 >> 2) > A.dbox_hi[0] || (n1 >> 2) < A.dbox_lo[1] ||
+            (n1 >> 2) > A.dbox_hi[1] || (n2 >> 2) < A.dbox_lo[2] || (n2 >> 2) > A.dbox_hi[2])
+          err_report(A.err, ERR_INACTIVE, 0);
         uint32_t r = hash_insert(A.S.hv, pack_key(n0 >> 2, n1 >> 2, n2 >> 2));
         if (r >= A.S.hv.cap_blocks) continue;
         uint32_t l = uint32_t(((n0 & 3) << 4) | ((n1 & 3) << 2) | (n2 & 3));
@@ -1180,6 +1184,10 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     if (inserter) {
       const int di = tid / 9 - 1, dj = (tid / 3) % 3 - 1, dk = tid % 3 - 1;
       ins_key = pack_key(B0 + di, B1 + dj, B2 + dk);
+      // dense backend: a stencil node outside the declared domain (solver.py:1053-1058)
+      if (B0 + di < A.dbox_lo[0] || B0 + di > A.dbox_hi[0] || B1 + dj < A.dbox_lo[1] || B1 + dj > A.dbox_hi[1] ||
+          B2 + dk < A.dbox_lo[2] || B2 + dk > A.dbox_hi[2])
+        err_report(A.err, ERR_INACTIVE, 0);
       const uint32_t sl = uint32_t(mix64(ins_key)) & A.S.hv.mask;
       probe_key = ld_volatile_u64(&A.S.hv.keys[sl]);
       probe_val = ld_volatile_u32(&A.S.hv.vals[sl]);
@@ -1608,6 +1616,10 @@ FusedArgs fused_args(smpm_sim* s, int B, int dstbuf, int project) {
   A.err = s->derr;
   A.project = project;
   A.measure = 0;
+  for (int a = 0; a < 3; ++a) {
+    A.dbox_lo[a] = s->dense ? s->dbmin[a] : INT32_MIN;
+    A.dbox_hi[a] = s->dense ? s->dbmin[a] + s->dbshape[a] - 1 : INT32_MAX;
+  }
   A.scale_src = s->dstats[B].bnd_bits;
   A.bnd_dst = s->dstats[1 - B].bnd_bits;
   A.bx0 = s->bx0;

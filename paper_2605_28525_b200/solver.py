@@ -315,7 +315,8 @@ def _scatter(particles, index_map, h, gravity, fields, want_mass_mom, want_force
                                     _lib.stream_ptr()), "p2g")
     code, _p = _host_err(err)
     if code == _lib.ERR_INACTIVE:
-        raise InactiveNodeError("particle stencil node outside active grid")
+        raise InactiveNodeError("a particle stencil node is outside the active grid; with the dense backend this means "
+                                "a particle left the declared domain")
     if code == _lib.ERR_KEY_RANGE:
         raise KeyRangeError("particle stencil block outside packable coordinate range")
     if want_mass_mom:
@@ -390,7 +391,8 @@ def g2p(particles, index_map, fields, h, dt):
                                     _lib.ptr(vel), _lib.ptr(err), _lib.stream_ptr()), "g2p")
     code, _p = _host_err(err)
     if code == _lib.ERR_INACTIVE:
-        raise InactiveNodeError("particle stencil node outside active grid")
+        raise InactiveNodeError("a particle stencil node is outside the active grid; with the dense backend this means "
+                                "a particle left the declared domain")
     for k in ("x", "v", "C", "F"):
         getattr(particles, k)[...] = dev[k].cpu().numpy().reshape(getattr(particles, k).shape)
     return particles

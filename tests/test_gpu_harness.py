@@ -8,6 +8,7 @@ from pathlib import Path
 
 import numpy as np
 import pytest
+import yaml
 from click.testing import CliRunner
 
 from paper_2605_28525_b200 import bench, scenarios
@@ -106,3 +107,22 @@ def test_cli_run_and_compare(tmp_path):
     assert r.exit_code == 0, r.output
     rows, summary = scenarios.read_metrics(out)
     assert {row["phase"] for row in rows} == set(bench.PHASES) and float(summary["memory_reduction"]) > 1
+
+
+def test_dense_backend_raises_when_a_particle_leaves_the_domain():
+    """The dense backend allocates only the declared domain: a stencil node
+    outside it raises InactiveNodeError (solver.py:1053-1058); hash does not."""
+    from paper_2605_28525_b200.errors import InactiveNodeError
+
+    doc = yaml.safe_load((SCEN / "terrain_demo.yaml").read_text())
+    doc["materials"][0]["region_min_m"] = [0.7, -0.15, 0.15]
+    doc["materials"][0]["region_max_m"] = [0.95, 0.15, 0.45]
+    doc["materials"][0]["initial_velocity_m_s"] = [20.0, 0.0, 0.0]
+    sc = scenarios.parse_config(doc, base_dir=SCEN)
+    sim = scenarios.build_simulation(sc, backend="dense")
+    with pytest.raises(InactiveNodeError, match="outside the active grid"):
+        for _ in range(200):
+            sim.step()
+    sim = scenarios.build_simulation(sc, backend="hash")
+    for _ in range(20):
+        sim.step()
