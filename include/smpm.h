@@ -27,7 +27,10 @@ enum {
   SMPM_ERR_CAPACITY = 6,      /* internal capacity overflow (handled by growth) */
   SMPM_ERR_CONFIG = 20,       /* ConfigError (solver.py:776-810) */
   SMPM_ERR_CUDA = 30,         /* CUDA runtime failure (message: smpm_last_error) */
-  SMPM_ERR_ARG = 31           /* invalid argument */
+  SMPM_ERR_ARG = 31,          /* invalid argument */
+  SMPM_NEED_BOUNDS = 40,      /* internal: prologue measured, waiting for the caller's bounds */
+  SMPM_RETRY = 41,            /* prologue capacity grew: call smpm_sim_prologue_begin again */
+  SMPM_NEED_PROLOGUE = 42     /* external-bounds mode: run the coordinated prologue first */
 };
 
 const char* smpm_last_error(void);
@@ -199,6 +202,29 @@ int smpm_sim_launch_count(const smpm_sim* s, int64_t* kernels_per_step);
  * [bmin, bmax] is allocated each step (ranks in row-major order), so
  * n_allocated = n_dense and the grid update runs over the whole domain. */
 int smpm_sim_set_dense_domain(smpm_sim* s, const int32_t* bmin, const int32_t* bmax);
+
+/* Deterministic mode across ranks: every rank must scale its fixed-point
+ * partial sums identically, so the prologue's bounds are agreed by the caller
+ * (max over ranks) between the measure and scatter passes:
+ *   smpm_sim_set_external_bounds(s, 1);
+ *   if (smpm_sim_prologue_needed(s)) {   -- on every rank, together
+ *     smpm_sim_prologue_begin(s, local);    allreduce(max) -> global;
+ *     rc = smpm_sim_prologue_finish(s, global);  -- SMPM_RETRY: begin again
+ *   }
+ * and after each step the bounds the next launch scales with are replaced by
+ * the max over ranks (smpm_sim_p2g_bounds get / set). */
+int smpm_sim_set_external_bounds(smpm_sim* s, int on);
+int smpm_sim_prologue_needed(smpm_sim* s);
+int smpm_sim_prologue_begin(smpm_sim* s, float* local_bounds);
+int smpm_sim_prologue_finish(smpm_sim* s, const float* global_bounds);
+int smpm_sim_p2g_bounds(smpm_sim* s, int set, float* bounds);
+/* Diagnostics: per table (n_blocks, n_binned, n_items, scale_ovf, overflow,
+ * n_owned) x 2, then S, n_store, need_prologue, migrants_sent, and the bin
+ * census of the stored particles (holes, in-flight migrants, overflowed,
+ * unresolved, binned): 21 int64. */
+int smpm_sim_debug_stats(smpm_sim* s, int64_t* out);
+/* Bytes per block record of smpm_sim_exchange_pack (2064 fp32, 4112 deterministic). */
+int64_t smpm_sim_exchange_record_bytes(const smpm_sim* s);
 
 /* ---------------------------------------------------- slab decomposition
  * Multi-GPU (the reference is single-process, PAPER.md:335-337

@@ -26,6 +26,7 @@ ERR_KEY_RANGE = 4
 ERR_INACTIVE = 5
 ERR_CAPACITY = 6
 ERR_CONFIG = 20
+RETRY = 41
 ERR_CUDA = 30
 ERR_ARG = 31
 
@@ -108,6 +109,13 @@ _SIGS = {
     "smpm_sim_grid_size": (ctypes.c_int, [P, P]),
     "smpm_sim_set_slab": (ctypes.c_int, [P, I32, I32, I64, I64]),
     "smpm_sim_set_dense_domain": (ctypes.c_int, [P, P, P]),
+    "smpm_sim_set_external_bounds": (ctypes.c_int, [P, ctypes.c_int]),
+    "smpm_sim_prologue_needed": (ctypes.c_int, [P]),
+    "smpm_sim_prologue_begin": (ctypes.c_int, [P, P]),
+    "smpm_sim_prologue_finish": (ctypes.c_int, [P, P]),
+    "smpm_sim_p2g_bounds": (ctypes.c_int, [P, ctypes.c_int, P]),
+    "smpm_sim_exchange_record_bytes": (I64, [P]),
+    "smpm_sim_debug_stats": (ctypes.c_int, [P, P]),
     "smpm_sim_exchange_pack": (ctypes.c_int, [P, ctypes.c_int, P, I64, P]),
     "smpm_sim_exchange_unpack": (ctypes.c_int, [P, P, I64, ctypes.c_int]),
     "smpm_sim_migrants": (ctypes.c_int, [P, ctypes.c_int, P, I64, P]),

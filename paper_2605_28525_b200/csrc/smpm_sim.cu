@@ -57,6 +57,7 @@ constexpr uint32_t MAGIC_BITS = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float MAGIC = 12582912.0f;
 constexpr uint32_t BAD_KEY = 0xFFFFFFFFu;  // bin of a hole (departed particle) or an invalid one
 constexpr uint32_t OVF_KEY = 0xFFFFFFFEu;  // live particle whose block did not fit (replayed after growth)
+constexpr uint32_t MIG_KEY = 0xFFFFFFFDu;  // left this rank's slab: live until the exchange hands it over
 // Gather arena: float4 velocity per node, nodes 4B .. 4B+5 per axis, address
 // (k ^ 4*(j&1)) + 8 j + 48 i in float4 units: each quarter-warp (2x4 cells)
 // reads 8 distinct 16-byte bank groups, so the 27 LDS.128 per particle are
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S) {
 __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     uint32_t key = bin[i];
-    if (key >= OVF_KEY) continue;
+    if (key >= MIG_KEY) continue;
     perm[atomicAdd(&S.cell_off[key], 1u)] = uint32_t(i);
   }
 }
@@ -434,9 +435,11 @@ __global__ void k_dense_insert(TableDev T, int b0, int b1, int b2, int s0, int s
 // --------------------------------------------------------- prologue keys
 // Bins particles (arbitrary storage order) by the block of their base cell.
 __global__ void k_prologue_keys(Particles P, int64_t n, TableDev B, uint32_t* __restrict__ bin, double inv_h,
-                                unsigned long long* err) {
+                                unsigned long long* err, int mig_live) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    if (bin[i] == BAD_KEY) continue;  // hole left by a particle that moved to another rank
+    // holes: invalid particles and departed ones; migrants not yet handed over
+    // are re-scattered by a replay (their P2G belongs to this rank's step)
+    if (bin[i] == BAD_KEY || (bin[i] == MIG_KEY && !mig_live)) continue;
     const double* xr = reinterpret_cast<const double*>(&P.rec[i * 8]);
     const uint32_t pid = __float_as_uint(reinterpret_cast<const float*>(&P.rec[i * 8])[W_PM]) & PID_MASK;
     int base[3];
@@ -511,7 +514,7 @@ struct __align__(16) ItemInfo {
 
 constexpr int GCH = 5;                      // record chunks G2P reads (x, m, V0, H, pid|mat)
 constexpr uint32_t NOPOS = 0xFFFFFFFFu;     // thread has no particle in this slot
-constexpr uint32_t BIN_SKIP = 0xFFFFFFFDu;  // no bin to write
+constexpr uint32_t BIN_SKIP = 0xFFFFFFFCu;  // no bin to write (distinct from BAD / OVF / MIG_KEY)
 constexpr uint32_t BIN_ARENA = 0x80000000u; // | packed arena cell: resolved with the item's ranks
 constexpr float FX_LIM = 4194304.0f;        // 2^22: |contribution| * S (exact magic-add conversion)
 
@@ -617,7 +620,7 @@ __device__ void scatter_global(const FusedArgs& A, const int nb[3], const float 
         red_v4(&A.acc[2 * node + 1], f0, f1, f2, 1.f);  // .w: contribution count K (n_active)
       }
   if (!bin) {
-    binv = BAD_KEY;
+    binv = MIG_KEY;
     return;
   }
   uint32_t r = hash_insert(A.S.hv, pack_key(nb[0] >> 2, nb[1] >> 2, nb[2] >> 2));
@@ -1148,7 +1151,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
             atomicAdd(&sm.cnt[p][aaddr(ab[0], ab[1], ab[2])], 1u);
             binv = BIN_ARENA | uint32_t((ab[0] << 6) | (ab[1] << 3) | ab[2]);
           } else {
-            binv = BAD_KEY;
+            binv = MIG_KEY;
           }
         } else if (!A.measure && ok && far) {
           scatter_global(A, nb, d1, m, vn, Cn, M, binv, mig < 0, Sm, Sp, Sf);
@@ -1261,7 +1264,7 @@ __global__ void k_invperm(Particles P, int64_t n_store, int64_t lo, int64_t n, c
                           uint32_t* __restrict__ inv) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_store;
        i += int64_t(gridDim.x) * blockDim.x) {
-    if (bin && bin[i] == BAD_KEY) continue;
+    if (bin && (bin[i] == BAD_KEY || bin[i] == MIG_KEY)) continue;
     const int64_t p = int64_t(__float_as_uint(reinterpret_cast<const float*>(P.rec + i * 8)[W_PM]) & PID_MASK) - lo;
     if (p >= 0 && p < n) inv[p] = uint32_t(i);
   }
@@ -1391,6 +1394,59 @@ __global__ void k_unpack_blocks(TableDev S, float4* acc, const BlockRec* __restr
   }
 }
 
+// Deterministic mode: the same exchange on the int64 fixed-point sums (all
+// ranks use the same scales, so partial sums add exactly).
+struct BlockRecFx {
+  unsigned long long key, pad;
+  unsigned long long v[64 * 8];
+};
+
+__global__ void k_pack_blocks_fx(TableDev S, const unsigned long long* __restrict__ acc_fx, int mode, int x0, int x1,
+                                 BlockRecFx* out, uint32_t* count, uint32_t cap) {
+  const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nb; r += nw) {
+    const uint64_t key = S.hv.active_keys[r];
+    int bi, bj, bk;
+    unpack_key(key, bi, bj, bk);
+    const bool sel = mode == 0 ? bi < x0 : (mode == 1 ? bi >= x1 : bi == x0);
+    if (!sel) continue;
+    uint32_t slot = 0;
+    if (lane == 0) slot = atomicAdd(count, 1u);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (slot >= cap) continue;
+    BlockRecFx& o = out[slot];
+    if (lane == 0) {
+      o.key = key;
+      o.pad = 0;
+    }
+    for (int q = lane; q < 512; q += 32) o.v[q] = acc_fx[size_t(r) * 512 + q];
+  }
+}
+
+__global__ void k_unpack_blocks_fx(TableDev S, unsigned long long* acc_fx, const BlockRecFx* __restrict__ in,
+                                   uint32_t n, int set, unsigned long long* err) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    uint32_t r = 0;
+    if (lane == 0) r = hash_insert(S.hv, in[i].key);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= S.hv.cap_blocks) {
+      if (lane == 0) err_report(err, ERR_CAPACITY, 0);
+      continue;
+    }
+    for (int q = lane; q < 512; q += 32) {
+      unsigned long long* d = &acc_fx[size_t(r) * 512 + q];
+      if (set)
+        *d = in[i].v[q];
+      else
+        atomicAdd(d, in[i].v[q]);
+    }
+  }
+}
+
 // Arriving particles: append their records at dst[off..] and bin them in S.
 // Their P2G was done by the sender, so only the bin (and cell count) is new.
 __global__ void k_accept(const float4* __restrict__ in, uint32_t n, Particles dst, uint32_t off, TableDev S,
@@ -1422,7 +1478,7 @@ __global__ void k_accept(const float4* __restrict__ in, uint32_t n, Particles ds
 __global__ void k_download_local(Particles P, const uint32_t* __restrict__ bin, uint32_t n_store, uint32_t* count,
                                  int64_t* pid, double* x, double* v) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_store; i += gridDim.x * blockDim.x) {
-    if (bin[i] == BAD_KEY) continue;
+    if (bin[i] == BAD_KEY || bin[i] == MIG_KEY) continue;
     const uint32_t o = atomicAdd(count, 1u);
     const float4* r4 = P.rec + size_t(i) * 8;
     const float4 c0 = r4[0], c1 = r4[1], c4 = r4[4], c5 = r4[5];
@@ -1492,9 +1548,15 @@ struct smpm_sim {
   // dense allocation mode (bench.compare baseline): block box [dbmin, dbmin + dbshape)
   bool dense = false;
   int dbmin[3] = {0, 0, 0}, dbshape[3] = {0, 0, 0};
+  // multi-GPU deterministic mode: the prologue's fixed-point bounds come from
+  // the caller (max over ranks) between its measure and scatter passes
+  bool ext_bounds = false;
+  int prologue_phase = 0;  // 1: measured, waiting for smpm_sim_prologue_finish
+  int prologue_proj = 0;
   float4* mig[2] = {nullptr, nullptr};
   uint32_t* mig_count = nullptr;
   uint32_t mig_cap = 0;
+  bool mig_sent = true;   // the migrants of the last launch were handed to the caller
   bool in_flight = false; // a step was launched and not yet synced
   uint32_t* hcount = nullptr;  // pinned: counter/overflow of the table just filled
   uint32_t* xcount = nullptr;  // device: block count of an exchange pack (per call, no allocation)
@@ -1666,9 +1728,10 @@ int scan_and_bin(smpm_sim* s, int Sx, double dt) {
 int launch_fused(smpm_sim* s, bool gather, int project) {
   int dstbuf = 1 - s->cur;
   if (s->mig_count) CK(cudaMemsetAsync(s->mig_count, 0, 8, s->stream));
+  s->mig_sent = false;
   FusedArgs A = fused_args(s, s->S, dstbuf, project);
   size_t smem = smem_bytes();
-  if (!gather) {
+  if (!gather && s->prologue_phase != 2) {
     // P2G-only pass (prologue / replay): first measure the contribution
     // bounds the fixed-point scales derive from (nothing is written)
     FusedArgs Mz = A;
@@ -1676,6 +1739,11 @@ int launch_fused(smpm_sim* s, bool gather, int project) {
     Mz.bnd_dst = s->dstats[s->S].bnd_bits;
     k_g2p2g<false><<<s->persist_blocks, CTA, smem, s->stream>>>(Mz);
     CK(cudaGetLastError());
+    if (s->ext_bounds && s->prologue_phase == 0) {
+      s->prologue_phase = 1;
+      s->prologue_proj = project;
+      return SMPM_NEED_BOUNDS;
+    }
   }
   if (gather)
     k_g2p2g<true><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
@@ -1747,6 +1815,33 @@ int decode_err(unsigned long long w, int64_t* particle) {
 // bin the current particles by block (keys -> scan -> bin) and run the P2G-only
 // variant of the fused kernel.  Synchronous; grows the grid until it fits.
 // Returns an error code (KeyRange / non-finite / degenerate) if detected.
+// After the prologue's P2G pass: errors, capacity (grow -> SMPM_RETRY), stats.
+int prologue_tail(smpm_sim* s) {
+  CK(cudaMemcpyAsync(s->hstats, s->dstats, 2 * sizeof(DevStats), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->herr, s->derr, 8, cudaMemcpyDeviceToHost, s->stream));
+  uint32_t need = 0;
+  bool over = false;
+  int rc = table_state(s, s->S, &need, &over);
+  if (rc) return rc;
+  s->n_store = s->hstats[0].n_binned;  // the P2G pass wrote every binned particle at its sorted position
+  int64_t p = 0;
+  const int code = decode_err(*s->herr, &p);
+  if (code) {
+    s->pending_err = code;
+    s->pending_particle = p;
+    return code;
+  }
+  if (over) {
+    rc = grow_grid(s, need);
+    if (rc) return rc;
+    s->prologue_project = false;
+    return SMPM_RETRY;
+  }
+  s->vmax = std::sqrt(double(__uint_as_float_host(s->hstats[s->S].vmax2_bits)));
+  s->need_prologue = false;
+  return SMPM_OK;
+}
+
 int run_prologue(smpm_sim* s, int project) {
   for (int attempt = 0; attempt < 24; ++attempt) {
     for (int t = 0; t < 2; ++t) {
@@ -1764,7 +1859,7 @@ int run_prologue(smpm_sim* s, int project) {
     int rcd = dense_insert(s, 0);
     if (rcd) return rcd;
     k_prologue_keys<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n_store, s->tab[0], s->bin, s->inv_h,
-                                                    s->derr);
+                                                    s->derr, s->mig_sent ? 0 : 1);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(s->herr, s->derr, 8, cudaMemcpyDeviceToHost, s->stream));
     uint32_t need = 0;
@@ -1790,28 +1885,13 @@ int run_prologue(smpm_sim* s, int project) {
     // every binned particle is copied to the other buffer, so the swap in
     // launch_fused keeps the full particle set even if the scatter overflows
     rc = launch_fused(s, false, project);
-    if (rc) return rc;
-    CK(cudaMemcpyAsync(s->hstats, s->dstats, 2 * sizeof(DevStats), cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaMemcpyAsync(s->herr, s->derr, 8, cudaMemcpyDeviceToHost, s->stream));
-    need = 0;
-    rc = table_state(s, s->S, &need, &over);
-    if (rc) return rc;
-    s->n_store = s->hstats[0].n_binned;  // the P2G pass wrote every binned particle at its sorted position
-    code = decode_err(*s->herr, &p);
-    if (code) {
-      s->pending_err = code;
-      s->pending_particle = p;
-      return code;
-    }
-    if (over) {
-      rc = grow_grid(s, need);
-      if (rc) return rc;
+    if (rc) return rc;  // SMPM_NEED_BOUNDS: the caller finishes with smpm_sim_prologue_finish
+    rc = prologue_tail(s);
+    if (rc == SMPM_RETRY) {
       project = 0;  // F is already return-mapped
       continue;
     }
-    s->vmax = std::sqrt(double(__uint_as_float_host(s->hstats[s->S].vmax2_bits)));
-    s->need_prologue = false;
-    return SMPM_OK;
+    return rc;
   }
   return set_err(SMPM_ERR_CAPACITY, "capacity growth did not converge");
 }
@@ -2186,6 +2266,7 @@ int smpm_sim_step(smpm_sim* s, double dt) {
     return s->pending_err;
   }
   if (s->need_prologue) {
+    if (s->ext_bounds) return set_err(SMPM_NEED_PROLOGUE, "externally coordinated prologue pending");
     int rc = run_prologue(s, s->prologue_project ? 1 : 0);
     if (rc) {
       s->last.status = rc;
@@ -2341,6 +2422,7 @@ int smpm_sim_grid_size(smpm_sim* s, int64_t* n_blocks) {
     s->prologue_project = false;
   }
   uint32_t nb;
+  CK(cudaStreamSynchronize(s->stream));
   CK(cudaMemcpy(&nb, s->tab[s->S].hv.counter, 4, cudaMemcpyDeviceToHost));
   *n_blocks = std::min(nb, s->cap_b);
   return SMPM_OK;
@@ -2373,9 +2455,107 @@ int smpm_sim_set_dense_domain(smpm_sim* s, const int32_t* bmin, const int32_t* b
   return SMPM_OK;
 }
 
+int smpm_sim_debug_stats(smpm_sim* s, int64_t* out) {
+  if (!s || !out) return set_err(SMPM_ERR_ARG, "null argument");
+  CK(cudaSetDevice(s->device));
+  CK(cudaStreamSynchronize(s->stream));
+  DevStats st[2];
+  CK(cudaMemcpy(st, s->dstats, sizeof(st), cudaMemcpyDeviceToHost));
+  for (int t = 0; t < 2; ++t) {
+    out[6 * t + 0] = st[t].n_blocks;
+    out[6 * t + 1] = st[t].n_binned;
+    out[6 * t + 2] = st[t].n_items;
+    out[6 * t + 3] = st[t].scale_ovf;
+    out[6 * t + 4] = st[t].overflow;
+    out[6 * t + 5] = st[t].n_owned;
+  }
+  out[12] = s->S;
+  out[13] = s->n_store;
+  out[14] = s->need_prologue;
+  out[15] = s->mig_sent;
+  std::vector<uint32_t> b(s->n_store);
+  CK(cudaMemcpy(b.data(), s->bin, size_t(s->n_store) * 4, cudaMemcpyDeviceToHost));
+  int64_t c[5] = {0, 0, 0, 0, 0};
+  for (uint32_t v : b) c[v == BAD_KEY ? 0 : v == MIG_KEY ? 1 : v == OVF_KEY ? 2 : v >= 0x80000000u ? 3 : 4]++;
+  for (int k = 0; k < 5; ++k) out[16 + k] = c[k];
+  return SMPM_OK;
+}
+
+int smpm_sim_set_external_bounds(smpm_sim* s, int on) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  s->ext_bounds = on != 0;
+  return SMPM_OK;
+}
+
+int smpm_sim_prologue_needed(smpm_sim* s) {
+  if (!s) return 0;
+  if (s->in_flight && smpm_sim_sync(s, nullptr)) return 0;
+  return s->need_prologue && !s->pending_err ? 1 : 0;
+}
+
+int smpm_sim_prologue_begin(smpm_sim* s, float* local_bounds) {
+  if (!s || !local_bounds) return set_err(SMPM_ERR_ARG, "null argument");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  if (s->pending_err) return s->pending_err;
+  s->need_prologue = true;
+  s->prologue_phase = 0;
+  int rc = run_prologue(s, s->prologue_project ? 1 : 0);
+  if (rc == SMPM_NEED_BOUNDS) {
+    uint32_t b[3];
+    // the measure pass ran on s->stream (non-blocking): wait for it first
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaMemcpy(b, s->dstats[s->S].bnd_bits, 12, cudaMemcpyDeviceToHost));
+    for (int a = 0; a < 3; ++a) local_bounds[a] = __uint_as_float_host(b[a]);
+    return SMPM_OK;
+  }
+  return rc ? rc : set_err(SMPM_ERR_ARG, "prologue_begin needs external-bounds mode");
+}
+
+int smpm_sim_prologue_finish(smpm_sim* s, const float* global_bounds) {
+  if (!s || !global_bounds) return set_err(SMPM_ERR_ARG, "null argument");
+  if (s->prologue_phase != 1) return set_err(SMPM_ERR_ARG, "no measured prologue to finish");
+  CK(cudaSetDevice(s->device));
+  uint32_t b[3];
+  for (int a = 0; a < 3; ++a) std::memcpy(&b[a], &global_bounds[a], 4);
+  CK(cudaMemcpyAsync(s->dstats[s->S].bnd_bits, b, 12, cudaMemcpyHostToDevice, s->stream));
+  s->prologue_phase = 2;  // the scatter pass now runs
+  int rc = launch_fused(s, false, s->prologue_proj);
+  s->prologue_phase = 0;
+  if (rc) return rc;
+  rc = prologue_tail(s);
+  if (rc == SMPM_OK) s->prologue_project = false;
+  return rc;  // SMPM_RETRY: capacity grew, begin again (all ranks)
+}
+
+int smpm_sim_p2g_bounds(smpm_sim* s, int set, float* bounds) {
+  if (!s || !bounds) return set_err(SMPM_ERR_ARG, "null argument");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  uint32_t b[3];
+  CK(cudaStreamSynchronize(s->stream));
+  if (set) {
+    for (int a = 0; a < 3; ++a) std::memcpy(&b[a], &bounds[a], 4);
+    CK(cudaMemcpy(s->dstats[s->S].bnd_bits, b, 12, cudaMemcpyHostToDevice));
+  } else {
+    CK(cudaMemcpy(b, s->dstats[s->S].bnd_bits, 12, cudaMemcpyDeviceToHost));
+    for (int a = 0; a < 3; ++a) bounds[a] = __uint_as_float_host(b[a]);
+  }
+  return SMPM_OK;
+}
+
+int64_t smpm_sim_exchange_record_bytes(const smpm_sim* s) {
+  return s && s->deterministic ? int64_t(sizeof(BlockRecFx)) : int64_t(sizeof(BlockRec));
+}
+
 int smpm_sim_set_slab(smpm_sim* s, int32_t bx0, int32_t bx1, int64_t pid_base, int64_t migrant_capacity) {
   if (!s || bx1 <= bx0) return set_err(SMPM_ERR_ARG, "invalid slab");
-  if (s->deterministic) return set_err(SMPM_ERR_CONFIG, "deterministic mode is single-GPU");
   CK(cudaSetDevice(s->device));
   s->bx0 = bx0;
   s->bx1 = bx1;
@@ -2401,8 +2581,13 @@ int smpm_sim_exchange_pack(smpm_sim* s, int mode, void* out, int64_t cap_blocks,
     if (rc) return rc;
   }
   CK(cudaMemsetAsync(s->xcount, 0, 4, s->stream));
-  k_pack_blocks<<<148 * 8, 256, 0, s->stream>>>(s->tab[s->S], s->acc, mode, s->bx0, s->bx1,
-                                                reinterpret_cast<BlockRec*>(out), s->xcount, uint32_t(cap_blocks));
+  if (s->acc_fx)
+    k_pack_blocks_fx<<<148 * 8, 256, 0, s->stream>>>(s->tab[s->S], s->acc_fx, mode, s->bx0, s->bx1,
+                                                     reinterpret_cast<BlockRecFx*>(out), s->xcount,
+                                                     uint32_t(cap_blocks));
+  else
+    k_pack_blocks<<<148 * 8, 256, 0, s->stream>>>(s->tab[s->S], s->acc, mode, s->bx0, s->bx1,
+                                                  reinterpret_cast<BlockRec*>(out), s->xcount, uint32_t(cap_blocks));
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(s->hxcount, s->xcount, 4, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
@@ -2416,8 +2601,13 @@ int smpm_sim_exchange_unpack(smpm_sim* s, const void* in, int64_t n, int set) {
   if (!s) return set_err(SMPM_ERR_ARG, "null sim");
   if (n <= 0) return SMPM_OK;
   CK(cudaSetDevice(s->device));
-  k_unpack_blocks<<<148 * 4, 256, 0, s->stream>>>(s->tab[s->S], s->acc, reinterpret_cast<const BlockRec*>(in),
-                                                  uint32_t(n), set, s->derr);
+  if (s->acc_fx)
+    k_unpack_blocks_fx<<<148 * 4, 256, 0, s->stream>>>(s->tab[s->S], s->acc_fx,
+                                                       reinterpret_cast<const BlockRecFx*>(in), uint32_t(n), set,
+                                                       s->derr);
+  else
+    k_unpack_blocks<<<148 * 4, 256, 0, s->stream>>>(s->tab[s->S], s->acc, reinterpret_cast<const BlockRec*>(in),
+                                                    uint32_t(n), set, s->derr);
   CK(cudaGetLastError());
   return SMPM_OK;
 }
@@ -2426,6 +2616,7 @@ int smpm_sim_migrants(smpm_sim* s, int side, void* out, int64_t cap, int64_t* n)
   if (!s || !n || side < 0 || side > 1) return set_err(SMPM_ERR_ARG, "invalid argument");
   CK(cudaSetDevice(s->device));
   *n = 0;
+  if (out) s->mig_sent = true;  // handed over: their storage slots become holes
   if (!s->mig_count) return SMPM_OK;
   uint32_t* c = s->hxcount;
   CK(cudaMemcpyAsync(c, s->mig_count, 8, cudaMemcpyDeviceToHost, s->stream));
@@ -2488,7 +2679,8 @@ int64_t smpm_sim_num_stored(const smpm_sim* s) { return s ? int64_t(s->n_store) 
 double smpm_sim_vmax(smpm_sim* s) {
   if (!s) return 0;
   if (s->in_flight) smpm_sim_sync(s, nullptr);
-  if (s->need_prologue && !s->pending_err) run_prologue(s, s->prologue_project ? 1 : 0), s->prologue_project = false;
+  if (s->need_prologue && !s->pending_err && !s->ext_bounds)
+    run_prologue(s, s->prologue_project ? 1 : 0), s->prologue_project = false;
   return s->vmax;
 }
 

@@ -27,7 +27,7 @@ import numpy as np
 from . import _lib
 from .solver import PHASES, Simulation, StepStats
 
-BLOCK_REC_BYTES = 2064  # key, node mask, 64 nodes x 8 floats
+BLOCK_REC_BYTES = 2064  # key, node mask, 64 nodes x 8 floats (deterministic mode: 4112, int64 sums)
 PARTICLE_REC_BYTES = 128
 INT32_MIN = -(1 << 31)
 INT32_MAX = (1 << 31) - 1
@@ -194,10 +194,39 @@ class DistributedSimulation:
         self._gvmax = None  # global max |v| after the last step (next dt bound)
         self._xcap = [4096, 4096, 4096]  # halo exchange buffers (blocks) per pack mode
         self._xbuf = [None, None, None]
-        # step 0: P2G of the initial state on every rank, then the halo exchange
-        nb = ctypes.c_int64(0)
-        _lib.check(self.lib.smpm_sim_grid_size(self._h, ctypes.byref(nb)), "prologue")
+        self._rec = int(self.lib.smpm_sim_exchange_record_bytes(self._h))
+        # Prologues (step 0, and replays after a rank's P2G outgrew its
+        # fixed-point scales or grid capacity) run on all ranks together and
+        # before the halo exchange; the fixed-point bounds are the max over
+        # ranks, so in deterministic mode every rank scales its int64 partial
+        # sums alike and they add exactly.
+        self.det = bool(config.deterministic)
+        self._replay = False
+        _lib.check(self.lib.smpm_sim_set_external_bounds(self._h, 1), "external bounds")
+        self._coordinated_prologue()
         self._exchange()
+
+    def _coordinated_prologue(self):
+        """P2G of the current particles on every rank with the max over ranks
+        of the fixed-point bounds (collective; deterministic mode)."""
+        while True:
+            local = (ctypes.c_float * 3)()
+            _lib.check(self.lib.smpm_sim_prologue_begin(self._h, local), "prologue")
+            glob = self.tr.gather(list(local)).max(axis=0)
+            rc = self.lib.smpm_sim_prologue_finish(self._h, (ctypes.c_float * 3)(*glob))
+            if rc not in (0, _lib.RETRY):
+                _lib.check(rc, "prologue")
+            if not self.tr.gather([float(rc == _lib.RETRY)]).max():
+                break
+        self._agree_bounds()
+
+    def _agree_bounds(self):
+        """The next launch scales its P2G with the max over ranks of the
+        contribution bounds each rank just measured (collective)."""
+        b = (ctypes.c_float * 3)()
+        _lib.check(self.lib.smpm_sim_p2g_bounds(self._h, 0, b), "bounds")
+        glob = self.tr.gather(list(b)).max(axis=0)
+        _lib.check(self.lib.smpm_sim_p2g_bounds(self._h, 1, (ctypes.c_float * 3)(*glob)), "bounds")
 
     # -- exchange -------------------------------------------------------------
     def _pack(self, mode):
@@ -207,19 +236,19 @@ class DistributedSimulation:
         while True:
             cap, buf = self._xcap[mode], self._xbuf[mode]
             if buf is None:
-                buf = self._xbuf[mode] = torch.empty(cap * BLOCK_REC_BYTES, dtype=torch.uint8, device="cuda")
+                buf = self._xbuf[mode] = torch.empty(cap * self._rec, dtype=torch.uint8, device="cuda")
             n = ctypes.c_int64(0)
             rc = self.lib.smpm_sim_exchange_pack(self._h, mode, _lib.ptr(buf), cap, ctypes.byref(n))
             if rc == _lib.ERR_CAPACITY and n.value > cap:
                 self._xcap[mode], self._xbuf[mode] = 2 * int(n.value), None
                 continue
             _lib.check(rc, "pack")
-            return buf[: n.value * BLOCK_REC_BYTES] if n.value else None
+            return buf[: n.value * self._rec] if n.value else None
 
     def _unpack(self, buf, set_):
         if buf is None or buf.numel() == 0:
             return
-        _lib.check(self.lib.smpm_sim_exchange_unpack(self._h, _lib.ptr(buf), buf.numel() // BLOCK_REC_BYTES,
+        _lib.check(self.lib.smpm_sim_exchange_unpack(self._h, _lib.ptr(buf), buf.numel() // self._rec,
                                                      int(set_)), "unpack")
 
     def _migrants(self, side):
@@ -235,7 +264,7 @@ class DistributedSimulation:
     def _frame(self, blocks, parts):
         """One message: a 16-byte header (int64 byte count of the block
         records, pad) keeping the records 16-byte aligned, the block records
-        (BLOCK_REC_BYTES each), then particle records."""
+        (exchange_record_bytes each), then particle records."""
         torch = self._torch
         if blocks is None and parts is None:
             return None
@@ -281,13 +310,26 @@ class DistributedSimulation:
         cfg = self.config
         if dt is None:
             dt = cfg.dt if cfg.dt is not None else self.dt_bound()
+        if self._replay:  # a rank's P2G outgrew its scales / capacity: all ranks redo it
+            self._coordinated_prologue()
+            self._exchange()
+            self._replay = False
         st = self.sim.step(float(dt))
-        # one collective for the step's global stats and the next dt bound
+        # one collective for the step's global stats, the next dt bound and,
+        # in deterministic mode, the next launch's bounds and replay flags
+        b = (ctypes.c_float * 3)()
+        _lib.check(self.lib.smpm_sim_p2g_bounds(self._h, 0, b), "bounds")
+        extra = [*b, float(self.lib.smpm_sim_prologue_needed(self._h))]
         rows = self.tr.gather([float(self.lib.smpm_sim_vmax(self._h)), st.n_active, st.n_allocated,
-                               st.mass_sum or 0.0, *(st.mom_sum if st.mom_sum is not None else (0.0, 0.0, 0.0))])
+                               st.mass_sum or 0.0, *(st.mom_sum if st.mom_sum is not None else (0.0, 0.0, 0.0)),
+                               *extra])
         self._gvmax = float(rows[:, 0].max())
-        red = rows[:, 1:].sum(axis=0)
-        self._exchange()
+        red = rows[:, 1:7].sum(axis=0)
+        glob = rows[:, 7:10].max(axis=0)
+        _lib.check(self.lib.smpm_sim_p2g_bounds(self._h, 1, (ctypes.c_float * 3)(*glob)), "bounds")
+        self._replay = bool(rows[:, 10].max())
+        if not self._replay:
+            self._exchange()
         self.t += st.dt
         self.step_count += 1
         return StepStats(step=self.step_count, t=self.t, dt=st.dt, n_active=int(red[0]), n_allocated=int(red[1]),
