@@ -332,13 +332,16 @@ __global__ void __launch_bounds__(256, 2) k_grid(TableDev S, TableDev T, DevStat
       const double iSm = stS->scale_inv[0], iSp = stS->scale_inv[1], iSf = stS->scale_inv[2];
 #pragma unroll
       for (int lk = 0; lk < 4; ++lk) {
-        unsigned long long* q = acc_fx + 8 * (c0 + lk);
+        ulonglong2* q = reinterpret_cast<ulonglong2*>(acc_fx + 8 * (c0 + lk));
         long long v[8];
 #pragma unroll
-        for (int f = 0; f < 8; ++f) {
-          v[f] = (long long)__ldcs(q + f);
-          q[f] = 0ull;
+        for (int f = 0; f < 4; ++f) {
+          const ulonglong2 u = __ldcs(q + f);
+          v[2 * f] = (long long)u.x;
+          v[2 * f + 1] = (long long)u.y;
         }
+#pragma unroll
+        for (int f = 0; f < 4; ++f) q[f] = make_ulonglong2(0ull, 0ull);
         a[lk] = make_float4(float(double(v[0]) * iSm), float(double(v[1]) * iSp), float(double(v[2]) * iSp),
                             float(double(v[3]) * iSp));
         b[lk] = make_float4(float(double(v[4]) * iSf), float(double(v[5]) * iSf), float(double(v[6]) * iSf),
