@@ -1956,10 +1956,16 @@ void parallel_range(int nt, int64_t n, Fn fn) {
 }
 
 // Host twin of k_upload: reference-layout fp64 arrays -> 128-byte records.
+// Also returns max m and the material-id range of the chunk (validation and the
+// mass floor come for free while the arrays stream through the cache).
 void pack_records(float* out, int64_t off, int64_t pid_base, int64_t a, int64_t b, const double* x, const double* v,
-                  const double* C, const double* F, const double* m, const double* V0, const int64_t* mat) {
+                  const double* C, const double* F, const double* m, const double* V0, const int64_t* mat,
+                  double& m_max, int64_t& mat_lo, int64_t& mat_hi) {
   for (int64_t i = a; i < b; ++i) {
     const int64_t j = off + i;
+    m_max = std::max(m_max, m[j]);
+    mat_lo = std::min(mat_lo, mat[j]);
+    mat_hi = std::max(mat_hi, mat[j]);
     float* w = out + i * REC_W;
     std::memcpy(w, x + 3 * j, 24);
     w[W_M] = float(m[j]);
@@ -1979,19 +1985,30 @@ int upload_host(smpm_sim* s, int64_t n, const double* x, const double* v, const 
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(g_pin_mu);
   const int64_t CH = int64_t(s->pin_bytes / 128);
+  double m_max = 0.0;
+  int64_t mat_lo = INT64_MAX, mat_hi = INT64_MIN;
   for (int64_t k = 0, off = 0; off < n; ++k, off += CH) {
     const int b = int(k & 1);
     const int64_t c = std::min(CH, n - off);
     if (k >= 2) CK(cudaEventSynchronize(s->pin_ev[b]));
     float* dst = reinterpret_cast<float*>(s->pin[b]);
+    std::mutex red_mu;
     parallel_range(s->host_threads, c, [&](int64_t a, int64_t e) {
-      pack_records(dst, off, s->pid_base, a, e, x, v, C, F, m, V0, mat);
+      double mm = 0.0;
+      int64_t lo = INT64_MAX, hi = INT64_MIN;
+      pack_records(dst, off, s->pid_base, a, e, x, v, C, F, m, V0, mat, mm, lo, hi);
+      std::lock_guard<std::mutex> lk(red_mu);
+      m_max = std::max(m_max, mm);
+      mat_lo = std::min(mat_lo, lo);
+      mat_hi = std::max(mat_hi, hi);
     });
     CK(cudaMemcpyAsync(s->state[0].rec + off * 8, dst, size_t(c) * 128, cudaMemcpyHostToDevice, s->stream));
     CK(cudaEventRecord(s->pin_ev[b], s->stream));
   }
   // the shared pinned buffers are free again only when the copies are done
   for (int b = 0; b < 2; ++b) CK(cudaEventSynchronize(s->pin_ev[b]));
+  if (mat_lo < 0 || mat_hi >= s->n_mat) return set_err(SMPM_ERR_CONFIG, "particle material id out of range");
+  if (s->mass_floor < 0) s->mass_floor = 1e-12 * m_max;  // MASS_FLOOR_SCALE * max m (solver.py:952)
   return SMPM_OK;
 }
 

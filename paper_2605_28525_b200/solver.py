@@ -469,12 +469,15 @@ class Simulation:
             raise ConfigError("simulation needs at least one material")
         if len(self.materials) > 8:
             raise ConfigError("at most 8 materials are supported on the GPU")
-        if particles.mat_id.min() < 0 or particles.mat_id.max() >= len(self.materials):
+        # large host sets: the material-id range and max mass are checked / taken
+        # by the library's threaded upload (mass floor < 0: "from the particles")
+        in_lib = particles.n >= 1 << 20 and isinstance(particles.x, np.ndarray)
+        if not in_lib and (particles.mat_id.min() < 0 or particles.mat_id.max() >= len(self.materials)):
             raise ConfigError("particle material id out of range")
         if sum(1 for b in self.boundaries if b.kind == "heightfield") > 1:
             raise ConfigError("at most one heightfield boundary is supported")
         self._wave_speed = max(m.wave_speed for m in self.materials)
-        self._mass_floor = MASS_FLOOR_SCALE * float(particles.m.max())
+        self._mass_floor = -1.0 if in_lib else MASS_FLOOR_SCALE * float(particles.m.max())
         torch = _lib.torch_cuda()
         lib = _lib.load()
         # every kernel of this simulation runs on one torch-managed stream

@@ -204,3 +204,20 @@ def test_heightfield_slide_steps():
         st = sim.step()
     assert st.n_active > 0 and n0 > 0
     assert np.isfinite(sim.particles.x).all()
+
+
+def test_large_upload_validates_material_ids():
+    """Sets of >= 2^20 particles are validated inside the threaded upload
+    (material-id range, max mass for the mass floor) instead of numpy."""
+    from paper_2605_28525_b200.errors import ConfigError
+
+    pos, vol = scenes.sample_box((0, 0, 0), (1.3, 1.3, 0.65), 0.02, 2)
+    assert len(pos) >= 1 << 20
+    ps = scenes.rest_particles(pos, vol, 1500.0)
+    cfg = SimConfig(h=0.02, gravity=np.array([0.0, 0.0, -9.81]), total_time=1.0, domain_min=np.array([-1.0, -1, -1]),
+                    domain_max=np.array([2.0, 2.0, 2.0]))
+    sim = Simulation(ps, cfg, [scenes.SAND], [])
+    sim.step(1e-4)
+    ps.mat_id[12345] = 3
+    with pytest.raises(ConfigError, match="material id out of range"):
+        Simulation(ps, cfg, [scenes.SAND], [])
