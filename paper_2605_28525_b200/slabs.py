@@ -20,7 +20,6 @@ a GPU box; gloo with host staging in the CPU tests).
 """
 
 import ctypes
-import math
 
 import numpy as np
 
@@ -363,4 +362,3 @@ class DistributedSimulation:
 
 
 __all__ = ["DistributedSimulation", "partition", "slab_bounds", "subset", "base_block_x", "PHASES"]
-_ = math
