@@ -332,6 +332,127 @@ __device__ __forceinline__ void sym_mul(const float a[6], const float b[6], floa
   c[5] = a[3] * b[4] + a[1] * b[5] + a[5] * b[2];
 }
 
+// Same model for moderate elastic strain (spectral radius of
+// Z = (B - I)(B + I)^-1 up to 0.6, i.e. principal stretches^2 in [0.25, 4]),
+// still without an eigen-decomposition.  eps = 1/2 log B = atanh(Z) =
+// sum_k Z^(2k+1)/(2k+1); the return map is the tensor form of the series
+// path below; the update uses E = exp(eps' - eps) - I = sum_k D^k/k!.  Both
+// series are summed forward with a per-particle term count chosen from the
+// Frobenius norm (>= spectral radius) so the truncation stays below 1e-8;
+// the loop index is warp-uniform while any lane is still summing.  Returns 0
+// when Z is too large (caller takes the Jacobi path), -1 on a degenerate F.
+__device__ inline int hencky_dp_mid(float H[9], const float X[6], const Material& mat, bool project, float tau[6],
+                                    float& J) {
+  // M = B + I = 2I + X, Z = X M^-1 (X and M^-1 commute)
+  const float m00 = 2.f + X[0], m11 = 2.f + X[1], m22 = 2.f + X[2], m01 = X[3], m02 = X[4], m12 = X[5];
+  const float c00 = m11 * m22 - m12 * m12, c11 = m00 * m22 - m02 * m02, c22 = m00 * m11 - m01 * m01;
+  const float c01 = m02 * m12 - m01 * m22, c02 = m01 * m12 - m02 * m11, c12 = m01 * m02 - m00 * m12;
+  const float det = m00 * c00 + m01 * c01 + m02 * c02;
+  if (!(det > 0.0f) || !isfinite(det)) return -1;
+  const float id = 1.0f / det;
+  const float Mi[6] = {c00 * id, c11 * id, c22 * id, c01 * id, c02 * id, c12 * id};
+  float Z[6];
+  sym_mul(X, Mi, Z);
+  const float r2 = Z[0] * Z[0] + Z[1] * Z[1] + Z[2] * Z[2] + 2.f * (Z[3] * Z[3] + Z[4] * Z[4] + Z[5] * Z[5]);
+  if (!(r2 <= 0.36f)) return 0;
+  // eps = Z + Z^3/3 + Z^5/5 + ...; truncation after Z^(2K+1) <= r^(2K+3)/((2K+3)(1-r^2))
+  float W[6], T[6], eps[6];
+  sym_mul(Z, Z, W);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    eps[q] = Z[q];
+    T[q] = Z[q];
+  }
+  const float tol = 5e-9f * (1.0f - r2);
+  float bound = r2 * sqrtf(r2);  // r^(2k+1), k = 1
+#pragma unroll 1
+  for (int k = 1; k <= 16; ++k) {
+    if (bound * __fdividef(1.0f, (float)(2 * k + 1)) <= tol) break;  // next term negligible
+    float Tn[6];
+    sym_mul(T, W, Tn);
+    const float ck = __fdividef(1.0f, (float)(2 * k + 1));
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      T[q] = Tn[q];
+      eps[q] = fmaf(ck, Tn[q], eps[q]);
+    }
+    bound *= r2;
+  }
+  float e2[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) e2[q] = eps[q];
+  const float tr = eps[0] + eps[1] + eps[2];
+  bool changed = false;
+  if (mat.kind == 1) {
+    if (tr > 0.0f) {  // apex: no tensile strength
+      changed = (eps[0] != 0.f) || (eps[1] != 0.f) || (eps[2] != 0.f) || (eps[3] != 0.f) || (eps[4] != 0.f) ||
+                (eps[5] != 0.f);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) e2[q] = 0.f;
+    } else {
+      const float m = tr * (1.0f / 3.0f);
+      const float h0 = eps[0] - m, h1 = eps[1] - m, h2 = eps[2] - m;
+      const float en = sqrtf(h0 * h0 + h1 * h1 + h2 * h2 + 2.f * (eps[3] * eps[3] + eps[4] * eps[4] + eps[5] * eps[5]));
+      const float dg = en + mat.alpha * mat.ratio * tr;
+      if (dg > 0.0f && en > 0.0f) {
+        const float c = dg / en;
+        e2[0] = eps[0] - c * h0;
+        e2[1] = eps[1] - c * h1;
+        e2[2] = eps[2] - c * h2;
+        e2[3] = eps[3] - c * eps[3];
+        e2[4] = eps[4] - c * eps[4];
+        e2[5] = eps[5] - c * eps[5];
+        changed = true;
+      }
+    }
+  }
+  if (changed && project) {
+    // E = exp(D) - I = D + D^2/2! + ..., D = eps' - eps (a polynomial of eps)
+    float D[6], E[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      D[q] = e2[q] - eps[q];
+      E[q] = D[q];
+      T[q] = D[q];
+    }
+    const float d2 = D[0] * D[0] + D[1] * D[1] + D[2] * D[2] + 2.f * (D[3] * D[3] + D[4] * D[4] + D[5] * D[5]);
+    const float d = sqrtf(d2);
+    float bound_e = d;  // ||D^k / k!||
+#pragma unroll 1
+    for (int k = 2; k <= 20; ++k) {
+      bound_e *= d * __fdividef(1.0f, (float)k);
+      if (bound_e <= 5e-9f) break;
+      float Tn[6];
+      sym_mul(T, D, Tn);
+      const float ik = __fdividef(1.0f, (float)k);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        T[q] = Tn[q] * ik;
+        E[q] += T[q];
+      }
+    }
+    const float Ef[9] = {E[0], E[3], E[4], E[3], E[1], E[5], E[4], E[5], E[2]};
+    float Hn[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        Hn[3 * i + j] = H[3 * i + j] + (Ef[3 * i + j] + (Ef[3 * i] * H[j] + Ef[3 * i + 1] * H[3 + j] + Ef[3 * i + 2] * H[6 + j]));
+#pragma unroll
+    for (int q = 0; q < 9; ++q) H[q] = Hn[q];
+  }
+  const float tr2 = e2[0] + e2[1] + e2[2];
+  const float lt = mat.lam * tr2, m2u = 2.0f * mat.mu;
+  tau[0] = m2u * e2[0] + lt;
+  tau[1] = m2u * e2[1] + lt;
+  tau[2] = m2u * e2[2] + lt;
+  tau[3] = m2u * e2[3];
+  tau[4] = m2u * e2[4];
+  tau[5] = m2u * e2[5];
+  J = expf(tr2);
+  return 1;
+}
+
 // Same model without an eigen-decomposition, for small elastic strain
 // (||B - I||_inf <= 0.05, the normal case: Drucker-Prager keeps elastic
 // strains small).  Hencky strain eps = 1/2 log(B), B = F F^T = I + X, as a
@@ -340,6 +461,10 @@ __device__ __forceinline__ void sym_mul(const float a[6], const float b[6], floa
 // materials.py:147-166); tau = 2 mu eps' + lam tr(eps') I equals
 // sum_k t_k u_k u_k^T of materials.py:233-238; and since eps' is a polynomial
 // of eps, F' = U exp(e') V^T = exp(eps' - eps) F.
+// MID: strains beyond the series range take hencky_dp_mid before the Jacobi
+// path (chosen per kernel variant: the extra code costs the small-strain
+// regime ~1.5 %).
+template <bool MID = false>
 __device__ inline bool hencky_dp(float H[9], const Material& mat, bool project, float tau[6], float& J) {
   const float trH = H[0] + H[4] + H[8];
   const float m2 = (H[0] * H[4] - H[1] * H[3]) + (H[0] * H[8] - H[2] * H[6]) + (H[4] * H[8] - H[5] * H[7]);
@@ -357,7 +482,13 @@ __device__ inline bool hencky_dp(float H[9], const Material& mat, bool project, 
   X[5] = (H[5] + H[7]) + (H[3] * H[6] + H[4] * H[7] + H[5] * H[8]);
   const float nx = fmaxf(fabsf(X[0]) + fabsf(X[3]) + fabsf(X[4]),
                          fmaxf(fabsf(X[3]) + fabsf(X[1]) + fabsf(X[5]), fabsf(X[4]) + fabsf(X[5]) + fabsf(X[2])));
-  if (!(nx <= 0.05f)) return hencky_dp_eig(H, mat, project, tau, J);
+  if (!(nx <= 0.05f)) {
+    if (MID) {
+      const int mid = hencky_dp_mid(H, X, mat, project, tau, J);
+      if (mid != 0) return mid > 0;
+    }
+    return hencky_dp_eig(H, mat, project, tau, J);
+  }
   // log(I + X) = X (1 - X (1/2 - X (1/3 - X (1/4 - X/5))))  (Horner); for
   // ||X|| <= 0.05 the truncation is < 0.05^6/6 = 2.6e-9, below fp32 rounding
   // of the strains (~1e-8 absolute)

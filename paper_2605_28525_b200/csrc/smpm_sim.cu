@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -53,6 +54,8 @@ constexpr int NF = 7;            // m, p0..2, f0..2
 constexpr int NA = NF + 1;       // + contribution count K
 constexpr int CTA = 256;         // 64 cells x 4 slots
 constexpr int ISLOTS = 8;     // particle slots per cell per work item (2 per thread)
+constexpr int MAXKK = 3;      // wide layout: 3 particles per thread
+constexpr uint32_t WIDE_CAP = 768;  // wide layout: particles per work item (CTA * MAXKK)
 constexpr uint32_t MAGIC_BITS = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float MAGIC = 12582912.0f;
 constexpr uint32_t BAD_KEY = 0xFFFFFFFFu;  // bin of a hole (departed particle) or an invalid one
@@ -101,7 +104,7 @@ struct DevStats {
   uint32_t prev_blocks;     // snapshot of the other table's block count
   uint32_t n_binned;
   uint32_t n_owned;         // blocks inside this rank's slab
-  uint32_t pad2;
+  uint32_t n_items8;        // items the 8-slot layout needs (layout choice of the next step)
   unsigned long long n_active;
   uint32_t bnd_bits[3];     // maxima of the P2G contribution bounds (mass, momentum, force) into this table
   uint32_t scale_ovf;       // a contribution exceeded the fixed-point scale: replay the P2G
@@ -116,6 +119,7 @@ struct StepParams {
   int record_conservation;
   int project;
   int bx0, bx1;  // owned block-x range (n_active / n_owned count owned blocks only)
+  int wide;      // work-item layout (see k_g2p2g): 0 cell slots, 1 block ranges of WIDE_CAP
 };
 
 // ------------------------------------------------------------------ scan
@@ -170,13 +174,14 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
   const int ntiles = (nb + TB - 1) / TB;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    uint32_t s_tot = 0, s_items = 0, s_own = 0;
+    uint32_t s_tot = 0, s_items = 0, s_items8 = 0, s_own = 0;
     for (int b = w; b < TB; b += 8) {
       uint32_t r = tile * TB + b;
       if (r >= nb) break;
       uint32_t c0 = S.cell_count[size_t(r) * 64 + lane], c1 = S.cell_count[size_t(r) * 64 + 32 + lane];
       uint32_t tot = warp_sum(c0 + c1), mx = warp_max(max(c0, c1));
-      uint32_t items = (mx + ISLOTS - 1) / ISLOTS;
+      const uint32_t items8 = (mx + ISLOTS - 1) / ISLOTS;
+      const uint32_t items = sp.wide ? (tot + WIDE_CAP - 1) / WIDE_CAP : items8;
       // neighbour ranks for the gather arena of this block's work items
       if (lane < 8 && items) {
         int bi, bj, bk;
@@ -189,6 +194,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
         S.block_items[r] = items;
         s_tot += tot;
         s_items += items;
+        s_items8 += items8;
         int bi, bj, bk;
         unpack_key(S.hv.active_keys[r], bi, bj, bk);
         if (bi >= sp.bx0 && bi < sp.bx1) s_own += 1;
@@ -197,7 +203,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
     if (lane == 0) {
       red[0][w] = s_tot;
       red[1][w] = s_items;
-      red[2][w] = 0;
+      red[2][w] = s_items8;
       red[3][w] = s_own;
     }
     __syncthreads();
@@ -234,6 +240,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
     st->n_binned = carry[0];
     st->n_active = 0;  // counted by k_grid (nodes with a stencil contribution, acc .w > 0)
     st->n_owned = carry[3];
+    st->n_items8 = carry[2];
     st->overflow = *S.hv.overflow | (*S.hv.counter > S.hv.cap_blocks ? 1u : 0u);
     // dt is validated on the host against the CFL bound (solver.py:1021-1030)
     st->dt = sp.dt_req;
@@ -529,8 +536,8 @@ struct __align__(16) FusedSmem {
   float4 garena[2][GATH_N];     // double-buffered velocity arena
   int acc[2][NA][SCAT_N];       // fixed-point arenas (+ contribution count K)
   uint32_t cnt[2][SCAT_N];      // particles per arena base cell (bin sizes)
-  uint32_t posr[3][2][CTA];     // sorted positions of the thread's two particles, ring like info
-  uint32_t binr[2][2][CTA];     // bins of the item awaiting its ranks
+  uint32_t posr[3][MAXKK][CTA]; // sorted positions of the thread's particles, ring like info
+  uint32_t binr[2][MAXKK][CTA]; // bins of the item awaiting its ranks
   uint32_t touched[2];          // 27-bit masks of the neighbour blocks the item's stencils touch
   uint32_t rank[2][27];         // next-table ranks of those blocks
   float sc[6];                  // Sm, Sp, Sf and their inverses
@@ -663,10 +670,20 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
   }
 }
 
-// One persistent CTA works through items = (block, group of ISLOTS particles
-// per cell); thread t owns cell t & 63 and slots s, s + 4 (s = t >> 6) of the
-// group: two particles, processed one after the other.  A full block of
-// ppc^3 = 8 particles per cell is one item.  Item i, parity p = i & 1:
+// One persistent CTA works through work items.  Narrow layout (NKK = 2): an
+// item is (block, group of 8 particles per cell); thread t owns cell t & 63
+// and slots s, s + 4 (s = t >> 6) of the group: two particles, processed one
+// after the other, and a warp's lanes sit in 32 distinct cells.  A full block
+// of ppc^3 = 8 particles per cell is one item.  Once the particles of a block
+// disorder (late in a landslide most blocks have some cell with more than 8,
+// so the narrow layout needs a second, nearly empty item per block), the host
+// switches to the wide layout (NKK = 3): an item is a range of up to WIDE_CAP
+// of the block's cell-sorted particles, lane L = tid + 256 kk taking particle
+// (L & 31) * R + (L >> 5), R = ceil(n / 32), so a warp's lanes stay ~n/32
+// particles (several cells) apart; the particle's cell comes from its
+// position.  The third particle of a thread is read straight from global
+// memory (no staging), so the shared-memory footprint and the steady-state
+// pipeline stay those of NKK = 2.  MID selects the constitutive variant.  Item i, parity p = i & 1:
 //   [B1]  records / velocity arena of item i have landed; item i-1 is fully
 //         scattered into X[p^1] and its blocks are inserted (rank[p^1]).
 //   A     zero X[p]; per particle: G2P, F update, advection, stress of the
@@ -679,7 +696,7 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
 //         threads flush item i-1 from X[p^1] (red.global.add.v4.f32, .w = the
 //         contribution count K), write its bins and cell counts; warp 0
 //         resolves item i's ranks into rank[p].
-template <bool GATHER>
+template <bool GATHER, int NKK, bool MID>
 __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
   FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smraw);
@@ -709,11 +726,33 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   }
 
   // sorted positions of the thread's two particles of an item (NOPOS: none)
+  // (narrow: cnt / off = the thread's cell count and end offset; wide: the
+  // block's particle count and end offset)
   auto slots = [&](const ItemInfo& inf, uint32_t cnt, uint32_t off, int ring) {
+    if (NKK == 2) {
 #pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-      const uint32_t slot = inf.g() * ISLOTS + s0 + 4 * kk;
-      sm.posr[ring][kk][tid] = (inf.r() != BAD_KEY && slot < cnt) ? off - cnt + slot : NOPOS;
+      for (int kk = 0; kk < NKK; ++kk) {
+        const uint32_t slot = inf.g() * ISLOTS + s0 + 4 * kk;
+        sm.posr[ring][kk][tid] = (inf.r() != BAD_KEY && slot < cnt) ? off - cnt + slot : NOPOS;
+      }
+    } else {
+      const uint32_t first = inf.g() * WIDE_CAP;
+      const uint32_t n = inf.r() != BAD_KEY && cnt > first ? min(cnt - first, WIDE_CAP) : 0u;
+      const uint32_t R = (n + 31) >> 5;
+#pragma unroll
+      for (int kk = 0; kk < NKK; ++kk) {
+        const uint32_t L = uint32_t(tid) + CTA * kk, w = L >> 5, j = (L & 31) * R + w;
+        sm.posr[ring][kk][tid] = (w < R && j < n) ? off - cnt + first + j : NOPOS;
+      }
+    }
+  };
+  auto item_counts = [&](uint32_t r, uint32_t& cnt, uint32_t& off) {
+    if (NKK == 2) {
+      cnt = A.B.cell_count[r * 64 + cell];
+      off = A.B.cell_off[r * 64 + cell];  // k_bin advanced cell_off to the cell's end
+    } else {
+      cnt = A.B.block_total[r];
+      off = A.B.cell_off[r * 64 + 63];  // end of the block's last cell
     }
   };
   // ---- prime the pipeline: records of item 0, positions of item 1, metadata
@@ -729,14 +768,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     const ItemInfo& i1 = sm.info[1];
     if (GATHER && tid < 8 && i0.r() != BAD_KEY) sm.info[0].nbr[tid] = A.B.nbr8[size_t(i0.r()) * 8 + tid];
     uint32_t c0 = 0, o0 = 0, c1 = 0, o1 = 0;
-    if (i0.r() != BAD_KEY) {
-      c0 = A.B.cell_count[i0.r() * 64 + cell];
-      o0 = A.B.cell_off[i0.r() * 64 + cell];  // k_bin advanced cell_off to the cell's end
-    }
-    if (i1.r() != BAD_KEY) {
-      c1 = A.B.cell_count[i1.r() * 64 + cell];
-      o1 = A.B.cell_off[i1.r() * 64 + cell];
-    }
+    if (i0.r() != BAD_KEY) item_counts(i0.r(), c0, o0);
+    if (i1.r() != BAD_KEY) item_counts(i1.r(), c1, o1);
     slots(i0, c0, o0, 0);
     slots(i1, c1, o1, 1);
     if (GATHER) {
@@ -766,7 +799,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   auto flush = [&](int q, int rq) {
     const float iSm = sm.sc[3], iSp = sm.sc[4], iSf = sm.sc[5];
 #pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
+    for (int kk = 0; kk < NKK; ++kk) {
       const uint32_t bv = sm.binr[q][kk][tid];
       if (bv == BIN_SKIP) continue;
       uint32_t out = bv;
@@ -839,13 +872,13 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     uint32_t tmask = 0;
 
 #pragma unroll 1
-    for (int kk = 0; kk < 2; ++kk) {
+    for (int kk = 0; kk < NKK; ++kk) {
       const uint32_t pos = sm.posr[c][kk][tid];
       const bool valid = pos != NOPOS;
       // this item's record -> registers; the stage slot then takes item i+1's
       float4 c0, c1, c2, c3, c4, c5, c6, c7;
       if (valid) {
-        if (GATHER) {
+        if (GATHER && (NKK == 2 || kk < 2)) {
           c0 = sm.stage[kk][0][tid];
           c1 = sm.stage[kk][1][tid];
           c2 = sm.stage[kk][2][tid];
@@ -863,7 +896,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
           c7 = g[7];
         }
       }
-      if (GATHER) {
+      if (GATHER && (NKK == 2 || kk < 2)) {
         const uint32_t p1 = sm.posr[c1r][kk][tid];
         if (p1 != NOPOS) {
           const float4* g = A.src.rec + size_t(kk ? src1b : src1a) * 8;
@@ -890,13 +923,15 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
         if (GATHER) {
           // ---- G2P (solver.py:628-732) from the smem velocity arena.  The
           // particle is binned by its base cell, so the block-local base is
-          // the thread's cell.
-          const int lb[3] = {cell >> 4, (cell >> 2) & 3, cell & 3};
+          // the thread's cell (narrow layout) or follows from its position.
+          int lb[3] = {cell >> 4, (cell >> 2) & 3, cell & 3};
           float d[3], w[3][3], g[3][3];
+          const int Bb[3] = {B0, B1, B2};
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             int bs;
             axis_base(xn[a], A.inv_h, bs, d[a]);
+            if (NKK == 3) lb[a] = bs - 4 * Bb[a];
             bspline(d[a], w[a], g[a]);
           }
           // Packed fp32x2 (FFMA2, one issue slot for two FMAs; scalar operands
@@ -1000,7 +1035,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
         float tau[6], J;
         const Material& mat = sm.mats[mt];
         if ((SMPM_DIAG_SKIP & 1) ? (tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = F[0] * 1e-3f, false)
-                                 : !hencky_dp(F, mat, A.project != 0 && !A.measure, tau, J)) {
+                                 : !hencky_dp<MID>(F, mat, A.project != 0 && !A.measure, tau, J)) {
           if (!A.measure) err_report(A.err, ERR_DEGENERATE_F, pidv);
           ok = false;
           tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = 0.f;
@@ -1177,10 +1212,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     // item i+2: index loads now, consumed after the flush
     const uint32_t nnr = nn.r();
     uint32_t cnt2 = 0, off2 = 0;
-    if (nnr != BAD_KEY) {
-      cnt2 = A.B.cell_count[nnr * 64 + cell];
-      off2 = A.B.cell_off[nnr * 64 + cell];
-    }
+    if (nnr != BAD_KEY) item_counts(nnr, cnt2, off2);
     // warp 0: probe the home slot of each touched block of the next table;
     // the probe latency overlaps the flush, the insert resolves after it
     const uint32_t tmask_all = sm.touched[p];
@@ -1560,6 +1592,10 @@ struct smpm_sim {
   uint32_t* mig_count = nullptr;
   uint32_t mig_cap = 0;
   bool mig_sent = true;   // the migrants of the last launch were handed to the caller
+  // work-item layout (k_g2p2g NKK): 2 particles per thread (8 slots per cell),
+  // or 3 once cells hold more than 8; SMPM_ITEM_LAYOUT=narrow|wide pins it
+  int nkk = 2, nkk_scan = 2;
+  bool allow_wide = true, pin_wide = false;
   bool in_flight = false; // a step was launched and not yet synced
   uint32_t* hcount = nullptr;  // pinned: counter/overflow of the table just filled
   uint32_t* xcount = nullptr;  // device: block count of an exchange pack (per call, no allocation)
@@ -1707,6 +1743,7 @@ StepParams step_params(smpm_sim* s, double dt) {
   sp.project = 1;
   sp.bx0 = s->bx0;
   sp.bx1 = s->bx1;
+  sp.wide = s->nkk == 3;
   return sp;
 }
 
@@ -1720,12 +1757,26 @@ int dense_insert(smpm_sim* s, int t) {
 
 int scan_and_bin(smpm_sim* s, int Sx, double dt) {
   StepParams sp = step_params(s, dt);
+  s->nkk_scan = s->nkk;  // the items just built are laid out for this kernel variant
   int grid = std::max(1, std::min<int>(s->max_tiles, 148 * 8));
   k_scan1<<<grid, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp);
   k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx]);
   k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm);
   CK(cudaGetLastError());
   return SMPM_OK;
+}
+
+// kernel variant: layout of the scanned items; the moderate-strain
+// constitutive path with the wide layout (late, large-strain regime) and in
+// deterministic mode (bitwise results must not depend on the layout choice)
+template <bool GATHER>
+void launch_g2p2g(smpm_sim* s, const FusedArgs& A, size_t smem) {
+  if (s->nkk_scan == 3)
+    k_g2p2g<GATHER, 3, true><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+  else if (s->acc_fx)
+    k_g2p2g<GATHER, 2, true><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+  else
+    k_g2p2g<GATHER, 2, false><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
 }
 
 int launch_fused(smpm_sim* s, bool gather, int project) {
@@ -1740,7 +1791,7 @@ int launch_fused(smpm_sim* s, bool gather, int project) {
     FusedArgs Mz = A;
     Mz.measure = 1;
     Mz.bnd_dst = s->dstats[s->S].bnd_bits;
-    k_g2p2g<false><<<s->persist_blocks, CTA, smem, s->stream>>>(Mz);
+    launch_g2p2g<false>(s, Mz, smem);
     CK(cudaGetLastError());
     if (s->ext_bounds && s->prologue_phase == 0) {
       s->prologue_phase = 1;
@@ -1749,9 +1800,9 @@ int launch_fused(smpm_sim* s, bool gather, int project) {
     }
   }
   if (gather)
-    k_g2p2g<true><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+    launch_g2p2g<true>(s, A, smem);
   else
-    k_g2p2g<false><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+    launch_g2p2g<false>(s, A, smem);
   CK(cudaGetLastError());
   s->cur = dstbuf;
   s->S = 1 - s->S;
@@ -2068,6 +2119,10 @@ int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
   if (cfg->n_mat < 1 || cfg->n_mat > 8) return set_err(SMPM_ERR_CONFIG, "1..8 materials supported");
   smpm_sim* s = new smpm_sim();
   s->device = cfg->device;
+  if (const char* lay = std::getenv("SMPM_ITEM_LAYOUT")) {
+    if (!std::strcmp(lay, "narrow")) s->allow_wide = false;
+    if (!std::strcmp(lay, "wide")) s->pin_wide = true, s->nkk = 3;
+  }
   CK(cudaSetDevice(s->device));
   if (cfg->stream) {
     s->stream = (cudaStream_t)cfg->stream;
@@ -2151,10 +2206,17 @@ int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
   CK(cudaMallocHost(&s->hxcount, 4 * sizeof(uint32_t)));
   rc = dalloc(s, &s->xcount, 4);
   if (rc) return rc;
-  CK(cudaFuncSetAttribute(k_g2p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes())));
-  CK(cudaFuncSetAttribute(k_g2p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes())));
+  {
+    const int sb = int(smem_bytes());
+    CK(cudaFuncSetAttribute(k_g2p2g<true, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<false, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<true, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<true, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<false, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+  }
   int occ = 0, sms = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<true>, CTA, smem_bytes()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<true, 2, false>, CTA, smem_bytes()));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
   s->persist_blocks = std::max(1, occ) * sms;
   for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&s->ev[i]));
@@ -2341,6 +2403,13 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
     r.dt = st.dt;
     r.n_active = int64_t(st.n_active);
     r.n_blocks = int64_t(st.n_owned);
+    // work-item layout of the next step: wide (block ranges) while the
+    // 8-slot layout would need > 5 % extra items, back below 2 %
+    if (st.n_blocks) {
+      const double extra = double(st.n_items8) / double(st.n_blocks);
+      if (s->nkk == 2 && extra > 1.05 && s->allow_wide) s->nkk = 3;
+      else if (s->nkk == 3 && extra < 1.02 && !s->pin_wide) s->nkk = 2;
+    }
     s->n_store = st.n_binned;  // positions written by the fused kernel (holes included)
     s->vmax = std::sqrt(double(__uint_as_float_host(nx.vmax2_bits)));
     r.vmax = s->vmax;

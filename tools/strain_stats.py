@@ -10,9 +10,22 @@ from paper_2605_28525_b200 import scenes  # noqa: E402
 from paper_2605_28525_b200.solver import Simulation  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 600
+checkpoints = sorted({n} | {int(a) for a in sys.argv[2:]})
 sc = scenes.landslide(fraction=0.02)
 sim = Simulation(sc.particles, sc.config, sc.materials, sc.boundaries)
-for s in range(n):
+done = 0
+for cp in checkpoints:
+    for s in range(cp - done):
+        sim.step()
+    done = cp
+    lam = np.linalg.eigvalsh(sim.particles.F @ np.transpose(sim.particles.F, (0, 2, 1)))
+    qs = [0, 1e-4, 1e-3, 1e-2, 0.5, 0.99, 0.999, 0.9999, 1]
+    print(f"step {cp}: lambda_min(B) quantiles", np.quantile(lam[:, 0], qs).round(4))
+    print(f"step {cp}: lambda_max(B) quantiles", np.quantile(lam[:, 2], qs).round(4))
+    z = np.maximum(np.abs((lam[:, 0] - 1) / (lam[:, 0] + 1)), np.abs((lam[:, 2] - 1) / (lam[:, 2] + 1)))
+    for zt in (0.1, 0.2, 0.33, 0.5, 0.6, 0.8):
+        print(f"   |z| <= {zt}: {np.mean(z <= zt) * 100:7.3f} %")
+for s in range(n - done):
     sim.step()
 F = sim.particles.F
 B = F @ np.transpose(F, (0, 2, 1))
