@@ -462,10 +462,9 @@ __device__ inline int hencky_dp_mid(float H[9], const float X[6], const Material
 // sum_k t_k u_k u_k^T of materials.py:233-238; and since eps' is a polynomial
 // of eps, F' = U exp(e') V^T = exp(eps' - eps) F.
 // MID: strains beyond the series range take hencky_dp_mid before the Jacobi
-// path (chosen per kernel variant: the extra code costs the small-strain
-// regime ~1.5 %).
-template <bool MID = false>
-__device__ inline bool hencky_dp(float H[9], const Material& mat, bool project, float tau[6], float& J) {
+// path (chosen per kernel variant, see hencky_dp below).
+template <bool MID>
+__device__ inline bool hencky_dp_body(float H[9], const Material& mat, bool project, float tau[6], float& J) {
   const float trH = H[0] + H[4] + H[8];
   const float m2 = (H[0] * H[4] - H[1] * H[3]) + (H[0] * H[8] - H[2] * H[6]) + (H[4] * H[8] - H[5] * H[7]);
   const float dH = H[0] * (H[4] * H[8] - H[5] * H[7]) - H[1] * (H[3] * H[8] - H[5] * H[6]) +
@@ -713,6 +712,22 @@ __device__ inline void grid_node(const GridParams& gp, int nx, int ny, int nz, d
 
 __device__ inline void err_report(unsigned long long* err, uint32_t code, uint64_t particle) {
   atomicMin(err, (unsigned long long)err_word(code, particle));
+}
+
+
+// CV = 0: series + Jacobi, inlined (ordered regime); 1: series + moderate-
+// strain path + Jacobi, inlined; 2: the same compiled once, out of line, so
+// every deterministic kernel variant (both work-item layouts) runs the same
+// machine code and bitwise results do not depend on the layout choice
+// (inlined copies may contract multiply-adds differently).
+static __device__ __noinline__ bool hencky_dp_shared(float* H, const Material& mat, bool project, float* tau,
+                                                     float& J) {
+  return hencky_dp_body<true>(H, mat, project, tau, J);
+}
+template <int CV = 0>
+__device__ __forceinline__ bool hencky_dp(float H[9], const Material& mat, bool project, float tau[6], float& J) {
+  if (CV == 2) return hencky_dp_shared(H, mat, project, tau, J);
+  return hencky_dp_body<CV == 1>(H, mat, project, tau, J);
 }
 
 }  // namespace smpm

@@ -104,7 +104,7 @@ struct DevStats {
   uint32_t prev_blocks;     // snapshot of the other table's block count
   uint32_t n_binned;
   uint32_t n_owned;         // blocks inside this rank's slab
-  uint32_t n_items8;        // items the 8-slot layout needs (layout choice of the next step)
+  uint32_t n_items_alt;     // items the other work-item layout would need (layout choice)
   unsigned long long n_active;
   uint32_t bnd_bits[3];     // maxima of the P2G contribution bounds (mass, momentum, force) into this table
   uint32_t scale_ovf;       // a contribution exceeded the fixed-point scale: replay the P2G
@@ -174,14 +174,14 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
   const int ntiles = (nb + TB - 1) / TB;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    uint32_t s_tot = 0, s_items = 0, s_items8 = 0, s_own = 0;
+    uint32_t s_tot = 0, s_items = 0, s_alt = 0, s_own = 0;
     for (int b = w; b < TB; b += 8) {
       uint32_t r = tile * TB + b;
       if (r >= nb) break;
       uint32_t c0 = S.cell_count[size_t(r) * 64 + lane], c1 = S.cell_count[size_t(r) * 64 + 32 + lane];
       uint32_t tot = warp_sum(c0 + c1), mx = warp_max(max(c0, c1));
-      const uint32_t items8 = (mx + ISLOTS - 1) / ISLOTS;
-      const uint32_t items = sp.wide ? (tot + WIDE_CAP - 1) / WIDE_CAP : items8;
+      const uint32_t items8 = (mx + ISLOTS - 1) / ISLOTS, itemsw = (tot + WIDE_CAP - 1) / WIDE_CAP;
+      const uint32_t items = sp.wide ? itemsw : items8, items_alt = sp.wide ? items8 : itemsw;
       // neighbour ranks for the gather arena of this block's work items
       if (lane < 8 && items) {
         int bi, bj, bk;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
         S.block_items[r] = items;
         s_tot += tot;
         s_items += items;
-        s_items8 += items8;
+        s_alt += items_alt;
         int bi, bj, bk;
         unpack_key(S.hv.active_keys[r], bi, bj, bk);
         if (bi >= sp.bx0 && bi < sp.bx1) s_own += 1;
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
     if (lane == 0) {
       red[0][w] = s_tot;
       red[1][w] = s_items;
-      red[2][w] = s_items8;
+      red[2][w] = s_alt;
       red[3][w] = s_own;
     }
     __syncthreads();
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
     st->n_binned = carry[0];
     st->n_active = 0;  // counted by k_grid (nodes with a stencil contribution, acc .w > 0)
     st->n_owned = carry[3];
-    st->n_items8 = carry[2];
+    st->n_items_alt = carry[2];
     st->overflow = *S.hv.overflow | (*S.hv.counter > S.hv.cap_blocks ? 1u : 0u);
     // dt is validated on the host against the CFL bound (solver.py:1021-1030)
     st->dt = sp.dt_req;
@@ -683,7 +683,8 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
 // particles (several cells) apart; the particle's cell comes from its
 // position.  The third particle of a thread is read straight from global
 // memory (no staging), so the shared-memory footprint and the steady-state
-// pipeline stay those of NKK = 2.  MID selects the constitutive variant.  Item i, parity p = i & 1:
+// pipeline stay those of NKK = 2.  CV selects the constitutive variant
+// (hencky_dp).  Item i, parity p = i & 1:
 //   [B1]  records / velocity arena of item i have landed; item i-1 is fully
 //         scattered into X[p^1] and its blocks are inserted (rank[p^1]).
 //   A     zero X[p]; per particle: G2P, F update, advection, stress of the
@@ -696,7 +697,7 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
 //         threads flush item i-1 from X[p^1] (red.global.add.v4.f32, .w = the
 //         contribution count K), write its bins and cell counts; warp 0
 //         resolves item i's ranks into rank[p].
-template <bool GATHER, int NKK, bool MID>
+template <bool GATHER, int NKK, int CV>
 __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
   FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smraw);
@@ -1035,7 +1036,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
         float tau[6], J;
         const Material& mat = sm.mats[mt];
         if ((SMPM_DIAG_SKIP & 1) ? (tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = F[0] * 1e-3f, false)
-                                 : !hencky_dp<MID>(F, mat, A.project != 0 && !A.measure, tau, J)) {
+                                 : !hencky_dp<CV>(F, mat, A.project != 0 && !A.measure, tau, J)) {
           if (!A.measure) err_report(A.err, ERR_DEGENERATE_F, pidv);
           ok = false;
           tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = 0.f;
@@ -1771,12 +1772,18 @@ int scan_and_bin(smpm_sim* s, int Sx, double dt) {
 // deterministic mode (bitwise results must not depend on the layout choice)
 template <bool GATHER>
 void launch_g2p2g(smpm_sim* s, const FusedArgs& A, size_t smem) {
-  if (s->nkk_scan == 3)
-    k_g2p2g<GATHER, 3, true><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
-  else if (s->acc_fx)
-    k_g2p2g<GATHER, 2, true><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
-  else
-    k_g2p2g<GATHER, 2, false><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+  const bool wide = s->nkk_scan == 3;
+  if (s->acc_fx) {
+    if (wide)
+      k_g2p2g<GATHER, 3, 2><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+    else
+      k_g2p2g<GATHER, 2, 2><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+  } else {
+    if (wide)
+      k_g2p2g<GATHER, 3, 1><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+    else
+      k_g2p2g<GATHER, 2, 0><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
+  }
 }
 
 int launch_fused(smpm_sim* s, bool gather, int project) {
@@ -2208,15 +2215,17 @@ int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
   if (rc) return rc;
   {
     const int sb = int(smem_bytes());
-    CK(cudaFuncSetAttribute(k_g2p2g<true, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
-    CK(cudaFuncSetAttribute(k_g2p2g<false, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
-    CK(cudaFuncSetAttribute(k_g2p2g<true, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
-    CK(cudaFuncSetAttribute(k_g2p2g<false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
-    CK(cudaFuncSetAttribute(k_g2p2g<true, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
-    CK(cudaFuncSetAttribute(k_g2p2g<false, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<true, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<false, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<true, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<false, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<true, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<false, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<true, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g<false, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
   }
   int occ = 0, sms = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<true, 2, false>, CTA, smem_bytes()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<true, 2, 0>, CTA, smem_bytes()));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
   s->persist_blocks = std::max(1, occ) * sms;
   for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&s->ev[i]));
@@ -2404,11 +2413,15 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
     r.n_active = int64_t(st.n_active);
     r.n_blocks = int64_t(st.n_owned);
     // work-item layout of the next step: wide (block ranges) while the
-    // 8-slot layout would need > 5 % extra items, back below 2 %
-    if (st.n_blocks) {
-      const double extra = double(st.n_items8) / double(st.n_blocks);
-      if (s->nkk == 2 && extra > 1.05 && s->allow_wide) s->nkk = 3;
-      else if (s->nkk == 3 && extra < 1.02 && !s->pin_wide) s->nkk = 2;
+    // narrow layout needs > 10 % more items than the wide one (~ the non-empty
+    // blocks, so the choice does not depend on the backend's empty blocks),
+    // back below 5 % (a wide item costs ~11 % more than a narrow one)
+    {
+      const bool was_wide = s->nkk_scan == 3;
+      const uint32_t n8 = was_wide ? st.n_items_alt : st.n_items, nw = was_wide ? st.n_items : st.n_items_alt;
+      const double extra = nw ? double(n8) / double(nw) : 1.0;
+      if (s->nkk == 2 && extra > 1.10 && s->allow_wide) s->nkk = 3;
+      else if (s->nkk == 3 && extra < 1.05 && !s->pin_wide) s->nkk = 2;
     }
     s->n_store = st.n_binned;  // positions written by the fused kernel (holes included)
     s->vmax = std::sqrt(double(__uint_as_float_host(nx.vmax2_bits)));

@@ -21,12 +21,21 @@ from tests.test_oracle_golden import _boundaries  # noqa: E402
 TOL = dict(x=1e-6, v=2e-5, C=2e-4, F=2e-5, mass=1e-5, mom=1e-5, force=1e-4)
 
 
-def column_scene(h=0.05, size=(0.4, 0.3, 0.5), seed=3, vx=0.4, bcs="mixed", mat=None):
+def column_scene(h=0.05, size=(0.4, 0.3, 0.5), seed=3, vx=0.4, bcs="mixed", mat=None, prestrain=0.0):
     pos, vol = scenes.sample_box((-size[0] / 2, -size[1] / 2, 0.03), (size[0] / 2, size[1] / 2, size[2]), h, 2)
     rng = np.random.default_rng(seed)
     pos = pos + rng.uniform(-0.2, 0.2, pos.shape) * h / 2
     mat = mat or scenes.SAND
     ps = scenes.rest_particles(pos, vol, mat.density, velocity=(vx, 0.0, 0.0))
+    if prestrain:
+        # F = Q diag(s) R^T with principal stretches s in [1 - prestrain, 1 + prestrain]:
+        # elastic strains past the small-strain series range (||B - I|| > 0.05)
+        n = ps.x.shape[0]
+        q1, _ = np.linalg.qr(rng.normal(size=(n, 3, 3)))
+        q2, _ = np.linalg.qr(rng.normal(size=(n, 3, 3)))
+        q2[:, :, 0] *= np.sign(np.linalg.det(q1) * np.linalg.det(q2))[:, None]  # det F > 0
+        st = rng.uniform(1.0 - prestrain, 1.0 + prestrain, (n, 3))
+        ps.F = np.ascontiguousarray(q1 * st[:, None, :] @ np.transpose(q2, (0, 2, 1)))
     cfg = SimConfig(h=h, gravity=np.array([0.5, 0.0, -9.81]), total_time=1.0, domain_min=np.array([-1.0, -1.0, -0.2]),
                     domain_max=np.array([1.0, 1.0, 1.0]))
     b = _boundaries() if bcs == "mixed" else []
@@ -69,9 +78,20 @@ def compare_grid(oracle, sim, cfg, mats, ref_state):
     return dict(mass=normwise(mg, mr), mom=normwise(pg, pr), force=normwise(fg, frr))
 
 
-@pytest.mark.parametrize("bcs,det", [("mixed", False), ("none", False), ("mixed", True)])
-def test_steps_match_oracle(oracle, bcs, det):
-    ps, cfg, mats, bc = column_scene(bcs=bcs)
+ELASTIC = MaterialModel(kind="elastic", density=1000.0, youngs_modulus=1e6, poisson_ratio=0.3)
+
+
+@pytest.mark.parametrize("bcs,det,layout,prestrain", [
+    ("mixed", False, "auto", 0.0), ("none", False, "auto", 0.0), ("mixed", True, "auto", 0.0),
+    # wide work-item layout (block ranges) and the moderate-strain constitutive
+    # path it carries; prestrained elastic particles exercise that path
+    ("mixed", False, "wide", 0.0), ("mixed", False, "wide", 0.3), ("mixed", False, "wide", 0.55),
+    ("mixed", False, "narrow", 0.3),
+    ("mixed", True, "narrow", 0.3)])
+def test_steps_match_oracle(oracle, monkeypatch, bcs, det, layout, prestrain):
+    if layout != "auto":
+        monkeypatch.setenv("SMPM_ITEM_LAYOUT", layout)
+    ps, cfg, mats, bc = column_scene(bcs=bcs, prestrain=prestrain, mat=ELASTIC if prestrain else None)
     cfg.deterministic = det  # deterministic mode: int64 fixed-point grid sums
     sim = Simulation(ps, cfg, mats, bc)
     worst = {}
@@ -117,6 +137,26 @@ def test_deterministic_mode_is_bitwise_reproducible():
     for s in range(12):
         ref.step(2e-4)
     assert np.abs(ref.particles.x - runs[0][0]).max() < 1e-6 * np.abs(runs[0][0]).max()
+
+
+@pytest.mark.parametrize("mat", ["sand", "elastic"])
+def test_item_layouts_are_bitwise_identical_in_deterministic_mode(monkeypatch, mat):
+    """The narrow (cell-slot) and wide (block-range) work-item layouts group
+    particles differently; in deterministic mode grid sums are int64 and the
+    constitutive path is the same, so the states agree bit for bit."""
+    ps, cfg, mats, bc = column_scene(vx=3.0, prestrain=0.25 if mat == "elastic" else 0.0,
+                                     mat=ELASTIC if mat == "elastic" else None)
+    cfg.deterministic = True
+    runs = []
+    for layout in ("narrow", "wide"):
+        monkeypatch.setenv("SMPM_ITEM_LAYOUT", layout)
+        sim = Simulation(ps.copy(), cfg, mats, bc)
+        for s in range(10):
+            sim.step(1e-4)
+        p = sim.particles
+        runs.append((p.x.copy(), p.v.copy(), p.C.copy(), p.F.copy()))
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)
 
 
 def test_capacity_growth_replays_exactly(oracle):
