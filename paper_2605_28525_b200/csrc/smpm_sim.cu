@@ -678,10 +678,10 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
 // disorder (late in a landslide most blocks have some cell with more than 8,
 // so the narrow layout needs a second, nearly empty item per block), the host
 // switches to the wide layout (NKK = 3): an item is a range of up to WIDE_CAP
-// of the block's cell-sorted particles, lane L = tid + 256 kk taking particle
-// (L & 31) * R + (L >> 5), R = ceil(n / 32), so a warp's lanes stay ~n/32
-// particles (several cells) apart; the particle's cell comes from its
-// position.  The third particle of a thread is read straight from global
+// of the block's cell-sorted particles, thread t taking particle
+// 256 kk + 8 (t & 31) + (t >> 5), so a warp's lanes are 8 particles (about a
+// cell) apart and hit distinct shared-memory banks, as in the narrow layout;
+// the particle's cell comes from its position.  The third particle of a thread is read straight from global
 // memory (no staging), so the shared-memory footprint and the steady-state
 // pipeline stay those of NKK = 2.  CV selects the constitutive variant
 // (hencky_dp).  Item i, parity p = i & 1:
@@ -739,12 +739,15 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
     } else {
       const uint32_t first = inf.g() * WIDE_CAP;
       const uint32_t n = inf.r() != BAD_KEY && cnt > first ? min(cnt - first, WIDE_CAP) : 0u;
-      const uint32_t R = (n + 31) >> 5;
 #pragma unroll
-      for (int kk = 0; kk < NKK; ++kk) {
-        const uint32_t L = uint32_t(tid) + CTA * kk, w = L >> 5, j = (L & 31) * R + w;
-        sm.posr[ring][kk][tid] = (w < R && j < n) ? off - cnt + first + j : NOPOS;
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint32_t j = CTA * kk + 8 * (tid & 31) + (tid >> 5);
+        sm.posr[ring][kk][tid] = j < n ? off - cnt + first + j : NOPOS;
       }
+      // the (< 256) particles past 512 go to the first warps, R2 apart
+      const uint32_t m = n > 2 * CTA ? n - 2 * CTA : 0u, R2 = (m + 31) >> 5, w = tid >> 5;
+      const uint32_t j2 = (tid & 31) * R2 + w;
+      sm.posr[ring][2][tid] = (w < R2 && j2 < m) ? off - cnt + first + 2 * CTA + j2 : NOPOS;
     }
   };
   auto item_counts = [&](uint32_t r, uint32_t& cnt, uint32_t& off) {
@@ -2420,8 +2423,8 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
       const bool was_wide = s->nkk_scan == 3;
       const uint32_t n8 = was_wide ? st.n_items_alt : st.n_items, nw = was_wide ? st.n_items : st.n_items_alt;
       const double extra = nw ? double(n8) / double(nw) : 1.0;
-      if (s->nkk == 2 && extra > 1.10 && s->allow_wide) s->nkk = 3;
-      else if (s->nkk == 3 && extra < 1.05 && !s->pin_wide) s->nkk = 2;
+      if (s->nkk == 2 && extra > 1.03 && s->allow_wide) s->nkk = 3;
+      else if (s->nkk == 3 && extra < 1.01 && !s->pin_wide) s->nkk = 2;
     }
     s->n_store = st.n_binned;  // positions written by the fused kernel (holes included)
     s->vmax = std::sqrt(double(__uint_as_float_host(nx.vmax2_bits)));
