@@ -258,7 +258,15 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
 
 // scan2: cell offsets (particles sorted by block rank, then cell) and work
 // items (one per block and group of SLOTS particles per cell).
-__global__ void __launch_bounds__(256) k_scan2(TableDev S) {
+// Wide layout (k_g2p2g NKK = 3): the block's particles are placed slot-major
+// (all cells' first particle, then all second particles, ...) so 32
+// consecutive positions lie in 32 distinct cells.  Per block, cell_off holds
+// the level table instead of cell offsets: words 0..31 the cell masks of
+// levels 0..15 (cells with more than s particles, u64 as two words), 32..48
+// the start of each level and of the tail (levels >= 16, placed by a cursor
+// in word 49); cell_count becomes the per-cell cursor.
+constexpr int WL = 16;
+__global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide) {
   __shared__ uint32_t sh[8];
   __shared__ uint32_t boff[TB], ioff[TB];
   const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
@@ -289,8 +297,31 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S) {
         uint32_t y = __shfl_up_sync(0xffffffffu, x1, o);
         if (lane >= o) x1 += y;
       }
-      S.cell_off[size_t(rr) * 64 + lane] = boff[b] + x0 - c0;
-      S.cell_off[size_t(rr) * 64 + 32 + lane] = boff[b] + sum0 + x1 - c1;
+      if (!wide) {
+        S.cell_off[size_t(rr) * 64 + lane] = boff[b] + x0 - c0;
+        S.cell_off[size_t(rr) * 64 + 32 + lane] = boff[b] + sum0 + x1 - c1;
+      } else {
+        uint32_t* T = S.cell_off + size_t(rr) * 64;
+        uint32_t pos = boff[b];
+#pragma unroll 1
+        for (int lv = 0; lv < WL; ++lv) {
+          const uint32_t m0 = __ballot_sync(0xffffffffu, c0 > uint32_t(lv)),
+                         m1 = __ballot_sync(0xffffffffu, c1 > uint32_t(lv));
+          if (lane == 0) {
+            T[2 * lv] = m0;
+            T[2 * lv + 1] = m1;
+            T[32 + lv] = pos;
+          }
+          pos += __popc(m0) + __popc(m1);
+          if (!(m0 | m1)) break;  // no deeper levels (unused entries are never read)
+        }
+        if (lane == 0) {
+          T[32 + WL] = pos;  // = block start + sum_c min(count_c, WL): the tail
+          T[33 + WL] = 0;    // tail cursor
+        }
+        S.cell_count[size_t(rr) * 64 + lane] = 0;
+        S.cell_count[size_t(rr) * 64 + 32 + lane] = 0;
+      }
       const uint32_t nit = S.block_items[rr];
       const uint64_t key = S.hv.active_keys[rr];
       for (uint32_t g = lane; g < nit; g += 32)
@@ -302,11 +333,28 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S) {
 
 // bin: every particle takes the next position of its cell (atomic cursor that
 // starts at the scanned cell offset and ends at offset + count).
-__global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm) {
+// Wide layout: the particle's level s comes from the per-cell cursor, its
+// position from the block's level table (see k_scan2).
+__global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm,
+                      int wide) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     uint32_t key = bin[i];
     if (key >= MIG_KEY) continue;
-    perm[atomicAdd(&S.cell_off[key], 1u)] = uint32_t(i);
+    if (!wide) {
+      perm[atomicAdd(&S.cell_off[key], 1u)] = uint32_t(i);
+      continue;
+    }
+    uint32_t* T = S.cell_off + size_t(key >> 6) * 64;
+    const uint32_t c = key & 63u, lv = atomicAdd(&S.cell_count[key], 1u);
+    uint32_t pos;
+    if (lv < uint32_t(WL)) {
+      const uint2 m = reinterpret_cast<const uint2*>(T)[lv];
+      const uint64_t mm = uint64_t(m.x) | (uint64_t(m.y) << 32);
+      pos = T[32 + lv] + __popcll(mm & ((uint64_t(1) << c) - 1));
+    } else {
+      pos = T[32 + WL] + atomicAdd(&T[33 + WL], 1u);
+    }
+    perm[pos] = uint32_t(i);
   }
 }
 
@@ -677,11 +725,11 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
 // of ppc^3 = 8 particles per cell is one item.  Once the particles of a block
 // disorder (late in a landslide most blocks have some cell with more than 8,
 // so the narrow layout needs a second, nearly empty item per block), the host
-// switches to the wide layout (NKK = 3): an item is a range of up to WIDE_CAP
-// of the block's cell-sorted particles, thread t taking particle
-// 256 kk + 8 (t & 31) + (t >> 5), so a warp's lanes are 8 particles (about a
-// cell) apart and hit distinct shared-memory banks, as in the narrow layout;
-// the particle's cell comes from its position.  The third particle of a thread is read straight from global
+// switches to the wide layout (NKK = 3): k_bin places a block's particles
+// slot-major (level s = every cell's s-th particle), an item is a range of up
+// to WIDE_CAP of them and thread t takes position 256 kk + t, so a warp's 32
+// lanes sit in 32 distinct cells whatever the per-cell counts; the particle's
+// cell comes from its position.  The third particle of a thread is read straight from global
 // memory (no staging), so the shared-memory footprint and the steady-state
 // pipeline stay those of NKK = 2.  CV selects the constitutive variant
 // (hencky_dp).  Item i, parity p = i & 1:
@@ -740,14 +788,10 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
       const uint32_t first = inf.g() * WIDE_CAP;
       const uint32_t n = inf.r() != BAD_KEY && cnt > first ? min(cnt - first, WIDE_CAP) : 0u;
 #pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        const uint32_t j = CTA * kk + 8 * (tid & 31) + (tid >> 5);
+      for (int kk = 0; kk < NKK; ++kk) {
+        const uint32_t j = CTA * kk + tid;  // slot-major positions: a warp's lanes in distinct cells
         sm.posr[ring][kk][tid] = j < n ? off - cnt + first + j : NOPOS;
       }
-      // the (< 256) particles past 512 go to the first warps, R2 apart
-      const uint32_t m = n > 2 * CTA ? n - 2 * CTA : 0u, R2 = (m + 31) >> 5, w = tid >> 5;
-      const uint32_t j2 = (tid & 31) * R2 + w;
-      sm.posr[ring][2][tid] = (w < R2 && j2 < m) ? off - cnt + first + 2 * CTA + j2 : NOPOS;
     }
   };
   auto item_counts = [&](uint32_t r, uint32_t& cnt, uint32_t& off) {
@@ -756,7 +800,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
       off = A.B.cell_off[r * 64 + cell];  // k_bin advanced cell_off to the cell's end
     } else {
       cnt = A.B.block_total[r];
-      off = A.B.cell_off[r * 64 + 63];  // end of the block's last cell
+      off = A.B.cell_off[r * 64 + 32] + cnt;  // level table: block start (k_scan2)
     }
   };
   // ---- prime the pipeline: records of item 0, positions of item 1, metadata
@@ -1764,8 +1808,8 @@ int scan_and_bin(smpm_sim* s, int Sx, double dt) {
   s->nkk_scan = s->nkk;  // the items just built are laid out for this kernel variant
   int grid = std::max(1, std::min<int>(s->max_tiles, 148 * 8));
   k_scan1<<<grid, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp);
-  k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx]);
-  k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm);
+  k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx], sp.wide);
+  k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm, sp.wide);
   CK(cudaGetLastError());
   return SMPM_OK;
 }
