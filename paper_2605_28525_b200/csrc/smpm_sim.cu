@@ -20,6 +20,7 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1643,6 +1644,9 @@ struct smpm_sim {
   // work-item layout (k_g2p2g NKK): 2 particles per thread (8 slots per cell),
   // or 3 once cells hold more than 8; SMPM_ITEM_LAYOUT=narrow|wide pins it
   int nkk = 2, nkk_scan = 2;
+  // download scratch (inverse permutation, two staging chunks), kept once made
+  uint32_t* dl_inv = nullptr;
+  double* dl_dst[2] = {nullptr, nullptr};
   bool allow_wide = true, pin_wide = false;
   bool in_flight = false; // a step was launched and not yet synced
   uint32_t* hcount = nullptr;  // pinned: counter/overflow of the table just filled
@@ -2092,10 +2096,16 @@ int upload_host(smpm_sim* s, int64_t n, const double* x, const double* v, const 
   const int64_t CH = int64_t(s->pin_bytes / 128);
   double m_max = 0.0;
   int64_t mat_lo = INT64_MAX, mat_hi = INT64_MIN;
+  const bool trace = std::getenv("SMPM_TRACE") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  double t_wait = 0;
   for (int64_t k = 0, off = 0; off < n; ++k, off += CH) {
     const int b = int(k & 1);
     const int64_t c = std::min(CH, n - off);
+    const auto t0 = clk::now();
     if (k >= 2) CK(cudaEventSynchronize(s->pin_ev[b]));
+    t_wait += std::chrono::duration<double>(clk::now() - t0).count();
     float* dst = reinterpret_cast<float*>(s->pin[b]);
     std::mutex red_mu;
     parallel_range(s->host_threads, c, [&](int64_t a, int64_t e) {
@@ -2112,6 +2122,9 @@ int upload_host(smpm_sim* s, int64_t n, const double* x, const double* v, const 
   }
   // the shared pinned buffers are free again only when the copies are done
   for (int b = 0; b < 2; ++b) CK(cudaEventSynchronize(s->pin_ev[b]));
+  if (trace)
+    std::fprintf(stderr, "[smpm] upload: %d threads, wait %.3f s, total %.3f s\n", s->host_threads, t_wait,
+                 std::chrono::duration<double>(clk::now() - t_start).count());
   if (mat_lo < 0 || mat_hi >= s->n_mat) return set_err(SMPM_ERR_CONFIG, "particle material id out of range");
   if (s->mass_floor < 0) s->mass_floor = 1e-12 * m_max;  // MASS_FLOOR_SCALE * max m (solver.py:952)
   return SMPM_OK;
@@ -2124,11 +2137,15 @@ int download_xv_host(smpm_sim* s, double* x, double* v) {
   std::lock_guard<std::mutex> lk(g_pin_mu);
   const int64_t n = s->n;
   const int64_t CH = int64_t(s->pin_bytes / 48);
-  uint32_t* inv = nullptr;
-  double* dst[2] = {nullptr, nullptr};
-  CK(cudaMallocAsync(&inv, size_t(n) * 4, s->stream));
+  if (!s->dl_inv) {
+    // persistent: per-call allocations would make every download wait for
+    // the driver to map (and after large frees, scrub) device memory
+    DA(s->dl_inv, size_t(s->cap_p));
+    for (int b = 0; b < 2; ++b) DA(s->dl_dst[b], size_t(CH) * 6);
+  }
+  uint32_t* inv = s->dl_inv;
+  double* dst[2] = {s->dl_dst[0], s->dl_dst[1]};
   CK(cudaMemsetAsync(inv, 0, size_t(n) * 4, s->stream));
-  for (int b = 0; b < 2; ++b) CK(cudaMallocAsync(&dst[b], size_t(CH) * 48, s->stream));
   k_invperm<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n_store, s->pid_base, n, s->bin, inv);
   CK(cudaGetLastError());
   const int64_t nch = (n + CH - 1) / CH;
@@ -2141,22 +2158,32 @@ int download_xv_host(smpm_sim* s, double* x, double* v) {
     CK(cudaEventRecord(s->pin_ev[b], s->stream));
     return SMPM_OK;
   };
+  const bool trace = std::getenv("SMPM_TRACE") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  double t_wait = 0, t_copy = 0;
   for (int64_t k = 0; k < std::min<int64_t>(2, nch); ++k)
     if ((rc = issue(k))) return rc;
   for (int64_t k = 0; k < nch; ++k) {
     const int b = int(k & 1);
     const int64_t lo = k * CH, c = std::min(CH, n - lo);
+    const auto t0 = clk::now();
     CK(cudaEventSynchronize(s->pin_ev[b]));
+    const auto t1 = clk::now();
     const double* src = reinterpret_cast<const double*>(s->pin[b]);
     parallel_range(s->host_threads, c, [&](int64_t a, int64_t e) {
       if (x) std::memcpy(x + 3 * (lo + a), src + 3 * a, size_t(e - a) * 24);
       if (v) std::memcpy(v + 3 * (lo + a), src + 3 * c + 3 * a, size_t(e - a) * 24);
     });
+    t_wait += std::chrono::duration<double>(t1 - t0).count();
+    t_copy += std::chrono::duration<double>(clk::now() - t1).count();
     if (k + 2 < nch && (rc = issue(k + 2))) return rc;
   }
-  CK(cudaFreeAsync(inv, s->stream));
-  for (int b = 0; b < 2; ++b) CK(cudaFreeAsync(dst[b], s->stream));
   CK(cudaStreamSynchronize(s->stream));
+  if (trace)
+    std::fprintf(stderr, "[smpm] download x/v: %lld chunks, %d threads, wait %.3f s, host copy %.3f s, total %.3f s\n",
+                 (long long)nch, s->host_threads, t_wait, t_copy,
+                 std::chrono::duration<double>(clk::now() - t_start).count());
   return SMPM_OK;
 }
 

@@ -543,12 +543,18 @@ class Simulation:
         self._exported = None
 
     def _download(self, ps):
-        out = {k: np.empty(getattr(ps, k).shape, dtype=np.float64) for k in ("x", "v", "C", "F", "sigma", "jac")}
-        _lib.check(_lib.load().smpm_sim_get_particles(self._h, *(out[k].ctypes.data for k in
-                                                                  ("x", "v", "C", "F", "sigma", "jac"))),
-                   "get particles")
-        for k, a in out.items():
-            getattr(ps, k)[...] = a
+        keys = ("x", "v", "C", "F", "sigma", "jac")
+        # straight into the caller's arrays when they are C-contiguous fp64
+        # (no temporaries: the host side of a large download is page-bound)
+        out = {}
+        for k in keys:
+            a = getattr(ps, k)
+            out[k] = a if (a.dtype == np.float64 and a.flags.c_contiguous and a.flags.writeable) else \
+                np.empty(a.shape, dtype=np.float64)
+        _lib.check(_lib.load().smpm_sim_get_particles(self._h, *(out[k].ctypes.data for k in keys)), "get particles")
+        for k in keys:
+            if out[k] is not getattr(ps, k):
+                getattr(ps, k)[...] = out[k]
 
     @property
     def particles(self):
