@@ -1647,6 +1647,7 @@ struct smpm_sim {
   // download scratch (inverse permutation, two staging chunks), kept once made
   uint32_t* dl_inv = nullptr;
   double* dl_dst[2] = {nullptr, nullptr};
+  double* dl_all = nullptr;  // full-state download staging (34 doubles per particle of a chunk)
   bool allow_wide = true, pin_wide = false;
   bool in_flight = false; // a step was launched and not yet synced
   uint32_t* hcount = nullptr;  // pinned: counter/overflow of the table just filled
@@ -2390,15 +2391,16 @@ int smpm_sim_get_particles(smpm_sim* s, double* x, double* v, double* C, double*
     if (rc) return rc;
   }
   if (!C && !F && !sigma && !jac && (x || v) && is_host_ptr(x ? x : v)) return download_xv_host(s, x, v);
-  const int64_t CH = 1 << 22;
+  const int64_t CH = 1 << 20;
   const int64_t n = s->n;
-  double *sx = nullptr, *sv = nullptr, *sC = nullptr, *sF = nullptr, *ss = nullptr, *sj = nullptr;
-  if (x) CK(cudaMallocAsync(&sx, CH * 24, s->stream));
-  if (v) CK(cudaMallocAsync(&sv, CH * 24, s->stream));
-  if (C) CK(cudaMallocAsync(&sC, CH * 72, s->stream));
-  if (F) CK(cudaMallocAsync(&sF, CH * 72, s->stream));
-  if (sigma) CK(cudaMallocAsync(&ss, CH * 72, s->stream));
-  if (jac) CK(cudaMallocAsync(&sj, CH * 8, s->stream));
+  if (!s->dl_all) DA(s->dl_all, size_t(CH) * 34);  // kept: no per-call device allocation
+  double* const base = s->dl_all;
+  double* sx = x ? base : nullptr;
+  double* sv = v ? base + 3 * CH : nullptr;
+  double* sC = C ? base + 6 * CH : nullptr;
+  double* sF = F ? base + 15 * CH : nullptr;
+  double* ss = sigma ? base + 24 * CH : nullptr;
+  double* sj = jac ? base + 33 * CH : nullptr;
   for (int64_t lo = 0; lo < n; lo += CH) {
     int64_t c = std::min(CH, n - lo);
     k_download<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], n, lo, lo + c, sx, sv, sC, sF, ss, sj, s->dmats,
@@ -2411,8 +2413,6 @@ int smpm_sim_get_particles(smpm_sim* s, double* x, double* v, double* C, double*
     if (sigma) CK(cudaMemcpyAsync(sigma + 9 * lo, ss, c * 72, cudaMemcpyDefault, s->stream));
     if (jac) CK(cudaMemcpyAsync(jac + lo, sj, c * 8, cudaMemcpyDefault, s->stream));
   }
-  for (double* p : {sx, sv, sC, sF, ss, sj})
-    if (p) CK(cudaFreeAsync(p, s->stream));
   CK(cudaStreamSynchronize(s->stream));
   return SMPM_OK;
 }
