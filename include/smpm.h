@@ -221,7 +221,8 @@ int smpm_sim_p2g_bounds(smpm_sim* s, int set, float* bounds);
 /* Diagnostics: per table (n_blocks, n_binned, n_items, scale_ovf, overflow,
  * n_owned) x 2, then S, n_store, need_prologue, migrants_sent, and the bin
  * census of the stored particles (holes, in-flight migrants, overflowed,
- * unresolved, binned): 21 int64. */
+ * unresolved, binned), then the work-item layout of the last scan and of the
+ * next step (0 narrow, 1 wide): 23 int64. */
 int smpm_sim_debug_stats(smpm_sim* s, int64_t* out);
 /* Bytes per block record of smpm_sim_exchange_pack (2064 fp32, 4112 deterministic). */
 int64_t smpm_sim_exchange_record_bytes(const smpm_sim* s);

@@ -2654,6 +2654,8 @@ int smpm_sim_debug_stats(smpm_sim* s, int64_t* out) {
   int64_t c[5] = {0, 0, 0, 0, 0};
   for (uint32_t v : b) c[v == BAD_KEY ? 0 : v == MIG_KEY ? 1 : v == OVF_KEY ? 2 : v >= 0x80000000u ? 3 : 4]++;
   for (int k = 0; k < 5; ++k) out[16 + k] = c[k];
+  out[21] = s->nkk_scan == 3 ? 1 : 0;  // work-item layout of the last scan (1 wide)
+  out[22] = s->nkk == 3 ? 1 : 0;       // layout chosen for the next step
   return SMPM_OK;
 }
 

@@ -159,6 +159,35 @@ def test_item_layouts_are_bitwise_identical_in_deterministic_mode(monkeypatch, m
         assert np.array_equal(a, b)
 
 
+def _layout(sim):
+    import ctypes
+    from paper_2605_28525_b200 import _lib
+    out = (ctypes.c_int64 * 23)()
+    _lib.check(_lib.load().smpm_sim_debug_stats(sim._h, out), "debug stats")
+    return int(out[21])
+
+
+def test_layout_switch_mid_run_keeps_deterministic_results(monkeypatch):
+    """The host switches the work-item layout between steps once particles
+    disorder; in deterministic mode the run with switches is bit-identical to
+    a run pinned to the narrow layout."""
+    ps, cfg, mats, bc = column_scene(vx=3.0, size=(0.6, 0.4, 0.6))
+    cfg.deterministic = True
+    monkeypatch.delenv("SMPM_ITEM_LAYOUT", raising=False)
+    auto = Simulation(ps.copy(), cfg, mats, bc)
+    monkeypatch.setenv("SMPM_ITEM_LAYOUT", "narrow")
+    pinned = Simulation(ps.copy(), cfg, mats, bc)
+    layouts = []
+    for s in range(40):
+        auto.step(2e-4)
+        pinned.step(2e-4)
+        layouts.append(_layout(auto))
+    assert 1 in layouts, layouts  # the switch happened
+    a, b = auto.particles, pinned.particles
+    for k in ("x", "v", "C", "F"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
 def test_capacity_growth_replays_exactly(oracle):
     ps, cfg, mats, bc = column_scene()
     a = Simulation(ps.copy(), cfg, mats, bc)

@@ -18,11 +18,11 @@ hist = []
 def item_stats(tag):
     import ctypes
     from paper_2605_28525_b200 import _lib
-    out = (ctypes.c_int64 * 21)()
+    out = (ctypes.c_int64 * 23)()
     _lib.check(_lib.load().smpm_sim_debug_stats(sim._h, out), "debug stats")
     o = list(out)
     print(f"{tag}: blocks {o[0]} items {o[2]} ({o[2] / max(o[0], 1):.2f}/block) binned {o[1]} | bins: bad {o[16]} "
-          f"mig {o[17]} ovf {o[18]} arena {o[19]} direct {o[20]}")
+          f"mig {o[17]} ovf {o[18]} arena {o[19]} direct {o[20]} | layout {'wide' if o[21] else 'narrow'}")
 
 
 for s in range(n):
