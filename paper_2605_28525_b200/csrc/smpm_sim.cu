@@ -1140,16 +1140,15 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
             }
           }
           // contribution bounds: |w| <= prod_a max_o w_a(o); |grad w_a| <= max|g_a| prod_{b!=a} max w_b / h;
-          // |dx_a| <= h * max(d_a, 2 - d_a)
+          // |dx_a| <= h * max(d_a, 2 - d_a).  With d in [0.5, 1.5] and t = |d - 1|:
+          // max_o w = w_1 = 0.75 - t^2, max |g| = 0.5 + t, max(d, 2 - d) = 1 + t
           float wmax[3], gmax[3], dxm[3];
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
-            const float dd = d1[a];
-            const float w0 = 0.5f * (1.5f - dd) * (1.5f - dd), w1 = 0.75f - (dd - 1.f) * (dd - 1.f),
-                        w2 = 0.5f * (dd - 0.5f) * (dd - 0.5f);
-            wmax[a] = fmaxf(w0, fmaxf(w1, w2));
-            gmax[a] = fmaxf(fabsf(dd - 1.5f), fmaxf(fabsf(2.f * (dd - 1.f)), fabsf(dd - 0.5f)));
-            dxm[a] = hf_ * fmaxf(dd, 2.f - dd);
+            const float t = fabsf(d1[a] - 1.f);
+            wmax[a] = fmaf(-t, t, 0.75f);
+            gmax[a] = 0.5f + t;
+            dxm[a] = fmaf(hf_, t, hf_);
           }
           const float W = wmax[0] * wmax[1] * wmax[2];
           const float G0 = gmax[0] * wmax[1] * wmax[2] * ih, G1 = wmax[0] * gmax[1] * wmax[2] * ih,
