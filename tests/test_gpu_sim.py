@@ -21,8 +21,8 @@ from tests.test_oracle_golden import _boundaries  # noqa: E402
 TOL = dict(x=1e-6, v=2e-5, C=2e-4, F=2e-5, mass=1e-5, mom=1e-5, force=1e-4)
 
 
-def column_scene(h=0.05, size=(0.4, 0.3, 0.5), seed=3, vx=0.4, bcs="mixed", mat=None, prestrain=0.0):
-    pos, vol = scenes.sample_box((-size[0] / 2, -size[1] / 2, 0.03), (size[0] / 2, size[1] / 2, size[2]), h, 2)
+def column_scene(h=0.05, size=(0.4, 0.3, 0.5), seed=3, vx=0.4, bcs="mixed", mat=None, prestrain=0.0, ppc=2):
+    pos, vol = scenes.sample_box((-size[0] / 2, -size[1] / 2, 0.03), (size[0] / 2, size[1] / 2, size[2]), h, ppc)
     rng = np.random.default_rng(seed)
     pos = pos + rng.uniform(-0.2, 0.2, pos.shape) * h / 2
     mat = mat or scenes.SAND
@@ -81,17 +81,19 @@ def compare_grid(oracle, sim, cfg, mats, ref_state):
 ELASTIC = MaterialModel(kind="elastic", density=1000.0, youngs_modulus=1e6, poisson_ratio=0.3)
 
 
-@pytest.mark.parametrize("bcs,det,layout,prestrain", [
-    ("mixed", False, "auto", 0.0), ("none", False, "auto", 0.0), ("mixed", True, "auto", 0.0),
+@pytest.mark.parametrize("bcs,det,layout,prestrain,ppc", [
+    ("mixed", False, "auto", 0.0, 2), ("none", False, "auto", 0.0, 2), ("mixed", True, "auto", 0.0, 2),
     # wide work-item layout (block ranges) and the moderate-strain constitutive
     # path it carries; prestrained elastic particles exercise that path
-    ("mixed", False, "wide", 0.0), ("mixed", False, "wide", 0.3), ("mixed", False, "wide", 0.55),
-    ("mixed", False, "narrow", 0.3),
-    ("mixed", True, "narrow", 0.3)])
-def test_steps_match_oracle(oracle, monkeypatch, bcs, det, layout, prestrain):
+    ("mixed", False, "wide", 0.0, 2), ("mixed", False, "wide", 0.3, 2), ("mixed", False, "wide", 0.55, 2),
+    ("mixed", False, "narrow", 0.3, 2), ("mixed", True, "narrow", 0.3, 2),
+    # 27 particles per cell: several narrow items per block; wide level
+    # tables past their 16 levels (tail placement)
+    ("mixed", False, "narrow", 0.0, 3), ("mixed", False, "wide", 0.0, 3)])
+def test_steps_match_oracle(oracle, monkeypatch, bcs, det, layout, prestrain, ppc):
     if layout != "auto":
         monkeypatch.setenv("SMPM_ITEM_LAYOUT", layout)
-    ps, cfg, mats, bc = column_scene(bcs=bcs, prestrain=prestrain, mat=ELASTIC if prestrain else None)
+    ps, cfg, mats, bc = column_scene(bcs=bcs, prestrain=prestrain, mat=ELASTIC if prestrain else None, ppc=ppc)
     cfg.deterministic = det  # deterministic mode: int64 fixed-point grid sums
     sim = Simulation(ps, cfg, mats, bc)
     worst = {}
