@@ -338,15 +338,33 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide) {
 // position from the block's level table (see k_scan2).
 __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm,
                       int wide) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    uint32_t key = bin[i];
-    if (key >= MIG_KEY) continue;
+  // Storage order is the previous step's sorted order, so equal bins come in
+  // runs: one atomic per run of a warp (head lane), ranks within the run from
+  // the ballot of run heads.
+  const int lane = threadIdx.x & 31;
+  const int64_t w_first = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t w_step = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w0 = w_first * 32; w0 < n; w0 += w_step * 32) {
+    const int64_t i = w0 + lane;
+    const uint32_t key = i < n ? bin[i] : BAD_KEY;
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+    const bool head = lane == 0 || key != prev;
+    const uint32_t heads = __ballot_sync(0xffffffffu, head);
+    const uint32_t upto = heads & (0xffffffffu >> (31 - lane));  // heads at lanes <= lane
+    const int start = 31 - __clz(upto);
+    const uint32_t later = heads & ~(0xffffffffu >> (31 - lane));  // heads after lane
+    const uint32_t len = (later ? uint32_t(__ffs(later) - 1) : 32u) - uint32_t(lane);
+    const bool valid = key < MIG_KEY;
+    uint32_t base = 0;
+    if (head && valid) base = atomicAdd(wide ? &S.cell_count[key] : &S.cell_off[key], len);
+    base = __shfl_sync(0xffffffffu, base, start) + uint32_t(lane - start);
+    if (!valid) continue;
     if (!wide) {
-      perm[atomicAdd(&S.cell_off[key], 1u)] = uint32_t(i);
+      perm[base] = uint32_t(i);
       continue;
     }
     uint32_t* T = S.cell_off + size_t(key >> 6) * 64;
-    const uint32_t c = key & 63u, lv = atomicAdd(&S.cell_count[key], 1u);
+    const uint32_t c = key & 63u, lv = base;
     uint32_t pos;
     if (lv < uint32_t(WL)) {
       const uint2 m = reinterpret_cast<const uint2*>(T)[lv];
