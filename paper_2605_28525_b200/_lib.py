@@ -116,6 +116,7 @@ _SIGS = {
     "smpm_sim_p2g_bounds": (ctypes.c_int, [P, ctypes.c_int, P]),
     "smpm_sim_exchange_record_bytes": (I64, [P]),
     "smpm_sim_debug_stats": (ctypes.c_int, [P, P]),
+    "smpm_release_cached_memory": (ctypes.c_int, []),
     "smpm_sim_exchange_pack": (ctypes.c_int, [P, ctypes.c_int, P, I64, P]),
     "smpm_sim_exchange_unpack": (ctypes.c_int, [P, P, I64, ctypes.c_int]),
     "smpm_sim_migrants": (ctypes.c_int, [P, ctypes.c_int, P, I64, P]),

@@ -1610,7 +1610,7 @@ struct smpm_sim {
   uint32_t cap_b = 0, cap_items = 0, max_tiles = 0;
   uint64_t n_slots = 0;
   // device buffers
-  std::vector<void*> allocs;
+  std::vector<std::pair<void*, size_t>> allocs;  // device buffers (returned to the cache on destroy)
   Particles state[2];
   int cur = 0;  // state buffer holding the current particles
   uint32_t* bin = nullptr;
@@ -1697,11 +1697,69 @@ int set_err(int code, const char* msg) {
     }                                                                                              \
   } while (0)
 
+// Process-wide cache of device buffers released by destroyed simulations
+// (exact-size reuse, like a caching allocator): a simulation created after
+// another of the same configuration skips cudaMalloc, whose cost varies with
+// the driver's scrubbing of recently freed memory.  Bounded to half the
+// device memory; dropped on allocation failure and by
+// smpm_release_cached_memory().
+struct CachedBuf {
+  int device;
+  size_t bytes;
+  void* p;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBuf> g_cache;
+size_t g_cache_bytes = 0;
+
+void cache_drop(int device) {  // caller holds g_cache_mu
+  std::vector<CachedBuf> keep;
+  for (const CachedBuf& b : g_cache) {
+    if (device < 0 || b.device == device) {
+      cudaFree(b.p);
+      g_cache_bytes -= b.bytes;
+    } else {
+      keep.push_back(b);
+    }
+  }
+  g_cache = keep;
+}
+
+void cache_release(int device, void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  if (g_cache_bytes + bytes > total_b / 2) {
+    cudaFree(p);
+    return;
+  }
+  g_cache.push_back({device, bytes, p});
+  g_cache_bytes += bytes;
+}
+
 template <class T>
 int dalloc(smpm_sim* s, T** p, size_t count) {
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
   void* q = nullptr;
-  CK(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
-  s->allocs.push_back(q);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (size_t i = 0; i < g_cache.size(); ++i) {
+      if (g_cache[i].device == s->device && g_cache[i].bytes == bytes) {
+        q = g_cache[i].p;
+        g_cache_bytes -= bytes;
+        g_cache.erase(g_cache.begin() + i);
+        break;
+      }
+    }
+    if (!q && cudaMalloc(&q, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      cache_drop(s->device);  // cached buffers of other sizes: give them back and retry
+      q = nullptr;
+      CK(cudaMalloc(&q, bytes));
+    }
+  }
+  s->allocs.push_back({q, bytes});
   *p = reinterpret_cast<T*>(q);
   return SMPM_OK;
 }
@@ -1920,12 +1978,12 @@ int grow_grid(smpm_sim* s, uint32_t need) {
   grid_ptrs.push_back(s->acc);
   grid_ptrs.push_back(s->acc_fx);
   grid_ptrs.push_back(s->gv);
-  std::vector<void*> keep;
-  for (void* p : s->allocs) {
-    if (std::find(grid_ptrs.begin(), grid_ptrs.end(), p) != grid_ptrs.end())
-      CK(cudaFree(p));
+  std::vector<std::pair<void*, size_t>> keep;
+  for (const auto& a : s->allocs) {
+    if (std::find(grid_ptrs.begin(), grid_ptrs.end(), a.first) != grid_ptrs.end())
+      CK(cudaFree(a.first));
     else
-      keep.push_back(p);
+      keep.push_back(a);
   }
   s->allocs = keep;
   uint64_t nc = std::max<uint64_t>(uint64_t(s->cap_b) * 2, next_pow2(uint64_t(need) + need / 4));
@@ -2155,12 +2213,9 @@ int download_xv_host(smpm_sim* s, double* x, double* v) {
   std::lock_guard<std::mutex> lk(g_pin_mu);
   const int64_t n = s->n;
   const int64_t CH = int64_t(s->pin_bytes / 48);
-  if (!s->dl_inv) {
-    // persistent: per-call allocations would make every download wait for
-    // the driver to map (and after large frees, scrub) device memory
-    DA(s->dl_inv, size_t(s->cap_p));
-    for (int b = 0; b < 2; ++b) DA(s->dl_dst[b], size_t(CH) * 6);
-  }
+  // (scratch allocated with the simulation: per-call allocations would make
+  // every download wait for the driver to map, and after large frees scrub,
+  // device memory)
   uint32_t* inv = s->dl_inv;
   double* dst[2] = {s->dl_dst[0], s->dl_dst[1]};
   CK(cudaMemsetAsync(inv, 0, size_t(n) * 4, s->stream));
@@ -2210,6 +2265,12 @@ int download_xv_host(smpm_sim* s, double* x, double* v) {
 extern "C" {
 
 const char* smpm_last_error(void) { return g_err; }
+
+int smpm_release_cached_memory(void) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  cache_drop(-1);
+  return SMPM_OK;
+}
 int smpm_version(void) { return 1; }
 
 int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
@@ -2305,6 +2366,14 @@ int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
   CK(cudaMallocHost(&s->hxcount, 4 * sizeof(uint32_t)));
   rc = dalloc(s, &s->xcount, 4);
   if (rc) return rc;
+  // x/v download scratch up front: a simulation's buffer set is then fixed at
+  // creation (and reusable as a whole through the device-memory cache)
+  rc = dalloc(s, &s->dl_inv, size_t(s->cap_p));
+  if (rc) return rc;
+  for (int b = 0; b < 2; ++b) {
+    rc = dalloc(s, &s->dl_dst[b], std::min<size_t>(PIN_BYTES / 48, size_t(s->cap_p)) * 6);
+    if (rc) return rc;
+  }
   {
     const int sb = int(smem_bytes());
     CK(cudaFuncSetAttribute(k_g2p2g<true, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
@@ -2329,7 +2398,7 @@ int smpm_sim_destroy(smpm_sim* s) {
   if (!s) return SMPM_OK;
   cudaSetDevice(s->device);
   cudaStreamSynchronize(s->stream);
-  for (void* p : s->allocs) cudaFree(p);
+  for (const auto& a : s->allocs) cache_release(s->device, a.first, a.second);
   if (s->hstats) cudaFreeHost(s->hstats);
   if (s->herr) cudaFreeHost(s->herr);
   if (s->hcount) cudaFreeHost(s->hcount);

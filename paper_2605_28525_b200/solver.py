@@ -656,6 +656,12 @@ class Simulation:
         return blocks[:nb].astype(np.int64), f
 
 
+def release_cached_memory():
+    """Return the device memory that destroyed simulations left in the
+    library's reuse cache (include/smpm.h) to the driver."""
+    _lib.check(_lib.load().smpm_release_cached_memory(), "release cached memory")
+
+
 __all__ = ["ParticleSet", "NodalFields", "Heightfield", "BoundaryCondition", "SimConfig", "StepStats", "Simulation",
            "PHASES", "EXTRA_PHASES", "NODE_BYTES", "bspline_weights", "p2g", "grid_forces", "grid_update", "g2p",
-           "count_active_nodes", "apply_friction_boundary", "ActiveIndexMap"]
+           "count_active_nodes", "apply_friction_boundary", "ActiveIndexMap", "release_cached_memory"]

@@ -292,3 +292,26 @@ def test_large_upload_validates_material_ids():
     ps.mat_id[12345] = 3
     with pytest.raises(ConfigError, match="material id out of range"):
         Simulation(ps, cfg, [scenes.SAND], [])
+
+
+def test_device_memory_cache_reuse_and_release():
+    """Buffers of a destroyed simulation are reused by the next one of the
+    same configuration (include/smpm.h: smpm_release_cached_memory); results
+    do not depend on whether the memory came from the cache."""
+    import gc
+
+    from paper_2605_28525_b200.solver import release_cached_memory
+    ps, cfg, mats, bc = column_scene()
+    runs = []
+    for _ in range(2):  # second run: every buffer comes from the cache
+        cfg.deterministic = True
+        sim = Simulation(ps.copy(), cfg, mats, bc)
+        for _ in range(3):
+            sim.step(1e-4)
+        runs.append(sim.particles.x.copy())
+        del sim
+        gc.collect()
+    assert np.array_equal(runs[0], runs[1])
+    release_cached_memory()
+    sim = Simulation(ps.copy(), cfg, mats, bc)  # fresh allocations after the release
+    sim.step(1e-4)
