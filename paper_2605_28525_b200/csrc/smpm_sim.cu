@@ -1376,6 +1376,40 @@ __global__ void k_invperm(Particles P, int64_t n_store, int64_t lo, int64_t n, c
 
 // Gather x and v of pids [lo, lo + c) in reference layout (fp64) into one
 // staging block: x[3c] then v[3c].
+// storage indices of the live particles (not holes / handed-over migrants);
+// one counter atomic per warp
+__global__ void k_compact_live(const uint32_t* __restrict__ bin, uint32_t n_store, uint32_t* count,
+                               uint32_t* __restrict__ idx) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; i0 < n_store; i0 += stride) {
+    const uint32_t i = i0 + lane;
+    const bool live = i < n_store && bin[i] != BAD_KEY && bin[i] != MIG_KEY;
+    const uint32_t m = __ballot_sync(0xffffffffu, live);
+    uint32_t base = 0;
+    if (lane == 0 && m) base = atomicAdd(count, uint32_t(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (live) idx[base + __popc(m & ((1u << lane) - 1))] = i;
+  }
+}
+// pid (int64), x, v of c compacted particles -> out[c] | out[3c] | out[3c]
+__global__ void k_gather_local(Particles P, const uint32_t* __restrict__ idx, int64_t lo, int64_t c,
+                               double* __restrict__ out) {
+  int64_t* pid = reinterpret_cast<int64_t*>(out);
+  double* x = out + c;
+  double* v = out + 4 * c;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < c; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4* r4 = P.rec + size_t(idx[lo + i]) * 8;
+    const float4 c0 = r4[0], c1 = r4[1], c4 = r4[4], c5 = r4[5];
+    pid[i] = int64_t(__float_as_uint(c4.y) & PID_MASK);
+    x[3 * i] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
+    x[3 * i + 1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
+    x[3 * i + 2] = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
+    v[3 * i] = c4.z;
+    v[3 * i + 1] = c4.w;
+    v[3 * i + 2] = c5.x;
+  }
+}
 __global__ void k_gather_xv(Particles P, const uint32_t* __restrict__ inv, int64_t lo, int64_t c,
                             double* __restrict__ out) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < c; i += int64_t(gridDim.x) * blockDim.x) {
@@ -1579,22 +1613,6 @@ __global__ void k_accept(const float4* __restrict__ in, uint32_t n, Particles ds
 
 // Live particles of this rank in storage order (holes left by departed
 // particles carry no bin): pid + reference-layout fields.
-__global__ void k_download_local(Particles P, const uint32_t* __restrict__ bin, uint32_t n_store, uint32_t* count,
-                                 int64_t* pid, double* x, double* v) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_store; i += gridDim.x * blockDim.x) {
-    if (bin[i] == BAD_KEY || bin[i] == MIG_KEY) continue;
-    const uint32_t o = atomicAdd(count, 1u);
-    const float4* r4 = P.rec + size_t(i) * 8;
-    const float4 c0 = r4[0], c1 = r4[1], c4 = r4[4], c5 = r4[5];
-    pid[o] = int64_t(__float_as_uint(c4.y) & PID_MASK);
-    x[3 * o] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
-    x[3 * o + 1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
-    x[3 * o + 2] = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
-    v[3 * o] = c4.z;
-    v[3 * o + 1] = c4.w;
-    v[3 * o + 2] = c5.x;
-  }
-}
 
 }  // namespace smpm
 
@@ -2930,26 +2948,46 @@ int smpm_sim_get_local(smpm_sim* s, int64_t* n_live, int64_t* pid, double* x, do
     int rc = smpm_sim_sync(s, nullptr);
     if (rc) return rc;
   }
-  const size_t ns = std::max<uint32_t>(s->n_store, 1);
-  int64_t* dp;
-  double *dx, *dv;
-  uint32_t* dc;
-  CK(cudaMallocAsync(&dp, ns * 8, s->stream));
-  CK(cudaMallocAsync(&dx, ns * 24, s->stream));
-  CK(cudaMallocAsync(&dv, ns * 24, s->stream));
-  CK(cudaMallocAsync(&dc, 4, s->stream));
-  CK(cudaMemsetAsync(dc, 0, 4, s->stream));
-  k_download_local<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], s->bin, s->n_store, dc, dp, dx, dv);
+  // compact the live storage indices into the download scratch, then stream
+  // (pid, x, v) through the pinned double buffer like the x/v download
+  int rc = ensure_pinned(s);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  uint32_t* idx = s->dl_inv;  // cap_p entries >= n_store
+  CK(cudaMemsetAsync(s->xcount, 0, 4, s->stream));
+  k_compact_live<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->xcount, idx);
   CK(cudaGetLastError());
-  uint32_t c = 0;
-  CK(cudaMemcpyAsync(&c, dc, 4, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->hxcount, s->xcount, 4, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
-  if (pid) CK(cudaMemcpyAsync(pid, dp, size_t(c) * 8, cudaMemcpyDefault, s->stream));
-  if (x) CK(cudaMemcpyAsync(x, dx, size_t(c) * 24, cudaMemcpyDefault, s->stream));
-  if (v) CK(cudaMemcpyAsync(v, dv, size_t(c) * 24, cudaMemcpyDefault, s->stream));
-  for (void* p : {(void*)dp, (void*)dx, (void*)dv, (void*)dc}) CK(cudaFreeAsync(p, s->stream));
+  const int64_t n = int64_t(s->hxcount[0]);
+  const size_t dst_bytes = std::min<size_t>(PIN_BYTES / 48, size_t(s->cap_p)) * 48;
+  const int64_t CH = int64_t(std::min(s->pin_bytes, dst_bytes) / 56);
+  const int64_t nch = (n + CH - 1) / CH;
+  auto issue = [&](int64_t k) -> int {
+    const int b = int(k & 1);
+    const int64_t lo = k * CH, c = std::min(CH, n - lo);
+    k_gather_local<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], idx, lo, c, s->dl_dst[b]);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->pin[b], s->dl_dst[b], size_t(c) * 56, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaEventRecord(s->pin_ev[b], s->stream));
+    return SMPM_OK;
+  };
+  for (int64_t k = 0; k < std::min<int64_t>(2, nch); ++k)
+    if ((rc = issue(k))) return rc;
+  for (int64_t k = 0; k < nch; ++k) {
+    const int b = int(k & 1);
+    const int64_t lo = k * CH, c = std::min(CH, n - lo);
+    CK(cudaEventSynchronize(s->pin_ev[b]));
+    const double* src = reinterpret_cast<const double*>(s->pin[b]);
+    parallel_range(s->host_threads, c, [&](int64_t a, int64_t e) {
+      if (pid) std::memcpy(pid + lo + a, src + a, size_t(e - a) * 8);
+      if (x) std::memcpy(x + 3 * (lo + a), src + c + 3 * a, size_t(e - a) * 24);
+      if (v) std::memcpy(v + 3 * (lo + a), src + 4 * c + 3 * a, size_t(e - a) * 24);
+    });
+    if (k + 2 < nch && (rc = issue(k + 2))) return rc;
+  }
   CK(cudaStreamSynchronize(s->stream));
-  *n_live = int64_t(c);
+  *n_live = n;
   return SMPM_OK;
 }
 
