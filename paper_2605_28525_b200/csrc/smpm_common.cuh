@@ -720,13 +720,32 @@ __device__ inline void err_report(unsigned long long* err, uint32_t code, uint64
 // every deterministic kernel variant (both work-item layouts) runs the same
 // machine code and bitwise results do not depend on the layout choice
 // (inlined copies may contract multiply-adds differently).
-static __device__ __noinline__ bool hencky_dp_shared(float* H, const Material& mat, bool project, float* tau,
-                                                     float& J) {
-  return hencky_dp_body<true>(H, mat, project, tau, J);
+// By-value argument and result (registers under the device ABI) instead of
+// pointers to the caller's arrays, which would force them to local memory.
+struct HenckyIO {
+  float H[9];
+  float tau[6];
+  float J;
+  int ok;
+};
+static __device__ __noinline__ HenckyIO hencky_dp_shared(HenckyIO io, const Material& mat, bool project) {
+  io.ok = hencky_dp_body<true>(io.H, mat, project, io.tau, io.J) ? 1 : 0;
+  return io;
 }
 template <int CV = 0>
 __device__ __forceinline__ bool hencky_dp(float H[9], const Material& mat, bool project, float tau[6], float& J) {
-  if (CV == 2) return hencky_dp_shared(H, mat, project, tau, J);
+  if (CV == 2) {
+    HenckyIO io;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) io.H[q] = H[q];
+    io = hencky_dp_shared(io, mat, project);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) H[q] = io.H[q];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) tau[q] = io.tau[q];
+    J = io.J;
+    return io.ok != 0;
+  }
   return hencky_dp_body<CV == 1>(H, mat, project, tau, J);
 }
 
