@@ -110,13 +110,13 @@ def build_hash_sparse_grid(positions, h, block_size=4, initial_capacity=None, de
         raise ValueError("particle positions must be finite")
     if rank_order is None and deterministic:
         rank_order = "encounter"
-    torch = _lib.torch_cuda()
     if initial_capacity is None:
         capacity = _next_pow2(max(64, xp.shape[0] // 4))
     else:
         capacity = int(initial_capacity)
         if capacity < 1 or capacity & (capacity - 1):
             raise ValueError(f"table capacity must be a power of two, got {capacity}")
+    torch = _lib.torch_cuda()
     x = _lib.to_dev(xp, np.float64)
     inv_h = 1.0 / float(h)
     for _ in range(max_rebuilds):
