@@ -259,6 +259,16 @@ def test_dt_above_bound_raises():
     sim.step(0.5 * sim.dt_bound())  # the rejected step left no trace
 
 
+def test_oversized_fixed_timestep_rejected():
+    """SimConfig.dt above the stability bound is a ConfigError at construction
+    (solver.py:966-969, T/test_solver.py:373-375)."""
+    from paper_2605_28525_b200.errors import ConfigError
+    ps, cfg, mats, bc = column_scene(bcs="none")
+    cfg.dt = 1.0
+    with pytest.raises(ConfigError, match="stability bound"):
+        Simulation(ps, cfg, mats, [])
+
+
 def test_nonfinite_position_raises():
     ps, cfg, mats, bc = column_scene(bcs="none")
     ps.x[5, 1] = np.nan
