@@ -404,7 +404,9 @@ __global__ void k_stress(const Material* __restrict__ mats, int n_mat, int64_t n
     for (int q = 0; q < 9; ++q) Fl[q] = float(F[9 * p + q] - ((q == 0 || q == 4 || q == 8) ? 1.0 : 0.0));
     int64_t mid = mat_id[p];
     Material m = mats[(mid >= 0 && mid < n_mat) ? mid : 0];
-    if (!hencky_dp(Fl, m, true, tau, J)) {
+    // moderate-strain path as in the late-time fused kernel (its Jacobi
+    // fallback beyond), so module-level parity covers both
+    if (!hencky_dp<1>(Fl, m, true, tau, J)) {
       err_report(err, ERR_DEGENERATE_F, p);
       continue;
     }
