@@ -190,3 +190,59 @@ def test_friction_projection():
     np.testing.assert_allclose(out, [1.0, 2.0, 3.0], atol=1e-7)
     out = S.apply_friction_boundary([0.1, 0.0, -1.0], [0, 0, 1], 0.5)
     np.testing.assert_allclose(out, [0.0, 0.0, 0.0], atol=1e-7)
+
+
+def _stress_of(F, mat_id=0):
+    n = F.shape[0]
+    ps = S.ParticleSet.from_samples(np.zeros((n, 3)), np.ones(n), 1.0)
+    ps.F = np.ascontiguousarray(F, dtype=np.float64)
+    ps.mat_id = np.full(n, mat_id, dtype=np.int64)
+    update_stress(ps, _materials())
+    return ps
+
+
+def _rotations(n, seed):
+    q, _ = np.linalg.qr(np.random.default_rng(seed).normal(size=(n, 3, 3)))
+    q[:, :, 0] *= np.sign(np.linalg.det(q))[:, None]
+    return q
+
+
+@pytest.mark.parametrize("mat_id", [0, 1])
+def test_pure_rotation_is_stress_free(mat_id):
+    """T/test_materials.py:126-132 on the GPU path (fp32: |sigma| ~ 1e-7 E)."""
+    ps = _stress_of(_rotations(256, 1), mat_id)
+    assert np.abs(ps.sigma).max() < 1e-6 * 1e6
+
+
+@pytest.mark.parametrize("mat_id", [0, 1])
+def test_rotation_equivariance(mat_id):
+    """sigma(Q F) = Q sigma(F) Q^T (T/test_materials.py:147-156), moderate strains."""
+    rng = np.random.default_rng(5)
+    F = np.eye(3) + rng.uniform(-0.15, 0.15, (256, 3, 3))
+    Q = _rotations(256, 6)
+    a = _stress_of(F, mat_id).sigma
+    b = _stress_of(Q @ F, mat_id).sigma
+    assert normwise(b, Q @ a @ np.transpose(Q, (0, 2, 1))) < 1e-4
+
+
+def test_net_extension_collapses_to_apex():
+    """Drucker-Prager without cohesion: a net extension returns to the apex,
+    stress-free with F a pure rotation (T/test_materials.py:249-255)."""
+    Q = _rotations(64, 7)
+    ps = _stress_of(Q @ np.diag([1.08, 1.05, 1.1]), 0)
+    assert np.abs(ps.sigma).max() < 1e-6 * 1e6
+    FtF = np.transpose(ps.F, (0, 2, 1)) @ ps.F
+    assert np.abs(FtF - np.eye(3)).max() < 1e-5
+
+
+def test_shear_return_lands_on_yield_surface():
+    """A return lands on the yield cone (T/test_materials.py:257-268): applying
+    the return map again to the projected F leaves F and sigma unchanged
+    (within fp32)."""
+    rng = np.random.default_rng(8)
+    F = np.eye(3) + rng.uniform(-0.12, 0.12, (256, 3, 3))
+    F = F @ np.diag([0.95, 0.95, 0.95])  # compressive, so the return lands on the cone
+    once = _stress_of(F, 0)
+    twice = _stress_of(once.F.copy(), 0)
+    assert normwise(twice.F, once.F) < 1e-5
+    assert normwise(twice.sigma, once.sigma) < 1e-4
