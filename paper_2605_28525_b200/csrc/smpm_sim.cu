@@ -3,15 +3,20 @@
 //
 // Per step (S = table of this step's particles, T = the other table):
 //   scan1(S)  block totals, item counts, dt, snapshot T
-//   scan2(S)  cell offsets + work items (block rank, slot group)
-//   bin(S)    perm[cell_off[key] + idx] = storage index
+//   scan2(S)  cell offsets + work items (block rank, slot group); in the wide
+//             layout per-block level tables instead of cell offsets
+//   bin(S)    perm[position] = storage index (cell-major, or slot-major in the
+//             wide layout), one atomic per run of equal bins in a warp
 //   grid(S)   momentum -> velocity + boundaries over active nodes, n_active; zero the
 //             accumulators; clear table T
 //   g2p2g(S -> T)  per work item: G2P from the smem velocity arena, F update,
 //             advection, Hencky/DP return map of the *next* step's stress,
-//             next-step block keys + node masks + bins, and the next step's
+//             next-step block keys + touched blocks + bins, and the next step's
 //             P2G into a fixed-point int32 smem arena flushed with
-//             red.global.add.v4.f32.
+//             red.global.add.v4.f32.  Two variants (narrow / wide work-item
+//             layout), picked per step by the host from scan1's item counts.
+// Device buffers of destroyed simulations are kept in a process-wide cache
+// for reuse (smpm_release_cached_memory).
 // The reference's step order stress -> map -> p2g -> grid -> g2p is the same
 // computation rotated: stress(n+1), map(n+1) and p2g(n+1) depend only on the
 // state G2P(n) writes, so they run in G2P(n)'s epilogue (a prologue kernel
