@@ -35,9 +35,10 @@ enum {
 
 const char* smpm_last_error(void);
 /* Device memory of destroyed simulations is kept in a process-wide cache and
- * reused by later simulations with the same buffer sizes (bounded to half the
- * device memory, dropped automatically when an allocation fails).  This
- * returns the cached memory to the driver. */
+ * reused by later simulations with the same buffer sizes (bounded to a quarter
+ * of the device memory, dropped automatically when one of this library's
+ * allocations fails).  This returns the cached memory to the driver; call it
+ * before large allocations by other libraries in the same process. */
 int smpm_release_cached_memory(void);
 int smpm_version(void);
 

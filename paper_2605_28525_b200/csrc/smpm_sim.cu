@@ -1726,9 +1726,10 @@ int set_err(int code, const char* msg) {
 // Process-wide cache of device buffers released by destroyed simulations
 // (exact-size reuse, like a caching allocator): a simulation created after
 // another of the same configuration skips cudaMalloc, whose cost varies with
-// the driver's scrubbing of recently freed memory.  Bounded to half the
-// device memory; dropped on allocation failure and by
-// smpm_release_cached_memory().
+// the driver's scrubbing of recently freed memory.  Bounded to a quarter of
+// the device memory; dropped on allocation failure and by
+// smpm_release_cached_memory() (call it before large allocations by other
+// libraries, e.g. torch, in the same process).
 struct CachedBuf {
   int device;
   size_t bytes;
@@ -1756,7 +1757,7 @@ void cache_release(int device, void* p, size_t bytes) {
   std::lock_guard<std::mutex> lk(g_cache_mu);
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  if (g_cache_bytes + bytes > total_b / 2) {
+  if (g_cache_bytes + bytes > total_b / 4) {
     cudaFree(p);
     return;
   }
