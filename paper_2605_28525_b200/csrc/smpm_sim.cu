@@ -387,7 +387,13 @@ __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, u
 
 // grid update over the active nodes of S (+ accumulator zeroing, clearing of
 // table T for reuse by the next P2G).
-__global__ void __launch_bounds__(256, 2) k_grid(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
+#ifndef SMPM_GRID_MINB
+#define SMPM_GRID_MINB 2
+#endif
+// DET: deterministic mode (int64 fixed-point accumulators); a separate
+// instantiation so the fp32 path's register budget does not carry it
+template <bool DET>
+__global__ void __launch_bounds__(256, DET ? 2 : SMPM_GRID_MINB) k_grid(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
                                                  float4* __restrict__ acc, float4* __restrict__ gv, GridParams gp,
                                                  int record, int bx0, int bx1, unsigned long long* acc_fx) {
   __shared__ Boundary sbc[8];
@@ -408,7 +414,7 @@ __global__ void __launch_bounds__(256, 2) k_grid(TableDev S, TableDev T, DevStat
     const uint64_t key = S.hv.active_keys[r];
     const size_t c0 = size_t(r) * 64 + (li << 4) + (lj << 2);
     float4 a[4], b[4];
-    if (acc_fx) {
+    if (DET) {
       // deterministic mode: exact int64 fixed-point sums -> values (the scales
       // are powers of two, the sums < 2^53: the conversion is exact)
       const double iSm = stS->scale_inv[0], iSp = stS->scale_inv[1], iSf = stS->scale_inv[2];
@@ -2580,7 +2586,8 @@ int smpm_sim_step(smpm_sim* s, double dt) {
   if (rc) return rc;
   CK(cudaEventRecord(s->ev[1], s->stream));
   GridParams gp = grid_params(s);
-  k_grid<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
+  auto kg = s->acc_fx ? k_grid<true> : k_grid<false>;
+  kg<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
                                          s->gv, gp, s->record, s->bx0, s->bx1, s->acc_fx);
   CK(cudaGetLastError());
   rc = dense_insert(s, 1 - Sx);
