@@ -145,7 +145,9 @@ def reference_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[args.config], "config": args.config},
+            # same workload naming as our arm (C5 = the C4 landslide on N GPUs)
+            "config": {"workload": CONFIG_NAMES[args.config],
+                       "config": args.config if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "C5"},
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": base["value"], "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
