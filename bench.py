@@ -6,13 +6,17 @@
 One JSON line on rank 0.  metric: particle-steps/s (BASELINE.json).  A "step"
 is one Simulation.step of the whole scene (inputs resident in HBM for
 `value`; through the public API from host buffers for `e2e`).  The default
-workload is C4 (the ~99M-particle landslide) on 1 GPU.
+workload is C4 (the 101M-particle landslide) on 1 GPU.
 `--impl reference` times the CPU oracle port of the reference path (the
-reference is Python/numba; oracle/ restates it in C + OpenMP) on a bounded
-sample of the same scene, with all host threads.
+reference is Python/numba; oracle/ restates it in C + OpenMP) on the same
+full scene, with all host threads, for the SURVEY.md 8d step budget (C4: 2
+steps after 1 warm step) and reports the steps it timed.  Our line adds a
+late-time point (`late`: the same simulation after --late-steps steps of
+flow) and a fresh-process end-to-end figure (`e2e.cold`).
 """
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -105,51 +109,65 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_sample_scene(cfg_name):
-    """Bounded sample of the bench scene for the CPU port (10-30 s of work)."""
-    from paper_2605_28525_b200 import scenes
-
-    if cfg_name == "C4":
-        return scenes.landslide(fraction=0.05), "first 5% (12.5 m) of the landslide release zone (4.95M particles)"
-    if cfg_name == "C3":
-        return scenes.incline(h=0.04), "incline at h=0.04 (1/8 of the particles)"
-    return make_scene(cfg_name, 1.0), "full scene"
+# steps the CPU port times per configuration (K = 20
+# for C1/C2, 5 for C3, 2-3 for C4 -- about 10-30 s of CPU work each)
+CPU_STEPS = {"C1": 20, "C2": 20, "C3": 5, "C4": 2}
 
 
-def run_cpu_port(cfg_name, steps, threads=None):
-    """Time the oracle port of the reference's CPU scan path (S/bench.py:172-233
-    compute_total: stress, map_build, alloc_zero, p2g, grid_update, g2p)."""
+def workload_config(cfg_name, sc, n, deterministic, world=1):
+    """The workload description both arms print (same dict: same scene,
+    particle count, resolution and time-step rule; C5 = C4 on N GPUs)."""
+    label = "C5" if world > 1 and cfg_name == "C4" else cfg_name
+    return {"workload": CONFIG_NAMES[cfg_name], "config": label, "n_particles": int(n), "h": sc.config.h,
+            "ppc": 2, "dt": "CFL bound (cfl=0.4)", "l2": "inputs larger than L2 (state %.1f GB)" % (n * 242 / 1e9)
+            if n * 242 > 126e6 else "L2 flushed between steps: no (state fits in L2)",
+            "deterministic": bool(deterministic)}
+
+
+def run_cpu_port(cfg_name, steps, scale=1.0, threads=None, scene=None):
+    """Time the oracle port of the reference's CPU scan path on the full
+    scene (S/bench.py:172-233 compute_total: stress, map_build, alloc_zero,
+    p2g, grid_update, g2p), CFL time step, one untimed warm step first."""
     from oracle import oracle as o
 
-    sc, desc = cpu_sample_scene(cfg_name)
+    sc = scene if scene is not None else make_scene(cfg_name, scale)
+    ps = sc.particles
     threads = threads or len(os.sched_getaffinity(0))
-    sim = o.OracleSimulation(sc.particles, sc.config.h, sc.config.gravity, sc.materials, sc.boundaries,
-                             backend="scan", deterministic=False, threads=threads)
-    sim.step(count_nodes=False)  # warm (page-in)
+    t0 = time.perf_counter()
+    sim = o.OracleSimulation(ps, sc.config.h, sc.config.gravity, sc.materials, sc.boundaries,
+                             backend="scan", deterministic=False, threads=threads, adopt=True)
+    sim.step(count_nodes=False)  # warm (page-in, first-touch of the per-step arrays)
     total = 0.0
     for _ in range(steps):
         st = sim.step(count_nodes=False)
         total += sum(st["times"][p] for p in o.COMPUTE_PHASES)
-    n = sc.particles.n
+    n = ps.n
     return {"value": n * steps / total, "unit": METRIC, "cores": threads, "kind": "port",
-            "sample": f"{desc}: {n} particles x {steps} steps, scan backend, {threads} OpenMP threads",
-            "ms_per_step": 1e3 * total / steps, "n_particles": n}
+            "sample": f"full {CONFIG_NAMES[cfg_name]} scene ({cfg_name}, {n} particles) x {steps} timed steps after "
+                      f"1 warm step, scan backend, CFL dt, {threads} OpenMP threads (oracle/ C port of the "
+                      f"reference's numba path)",
+            "ms_per_step": 1e3 * total / steps, "n_particles": n, "steps": steps, "wall_s": time.perf_counter() - t0}
 
 
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    base = run_cpu_port(args.config, max(1, min(args.steps, 3)))
+    sc = make_scene(args.config, args.scale)
+    n = sc.particles.n
+    steps = max(1, min(args.steps, CPU_STEPS[args.config]))
+    base = run_cpu_port(args.config, steps, scene=sc)
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": METRIC, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["ms_per_step"],
+            "steps": steps, "warmup": 1, "ms_per_step": base["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            # same workload naming as our arm (C5 = the C4 landslide on N GPUs)
-            "config": {"workload": CONFIG_NAMES[args.config],
-                       "config": args.config if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "C5"},
+            "config": workload_config(args.config, sc, n, args.deterministic,
+                                      int(os.environ.get("WORLD_SIZE", "1"))),
+            "parallelism": f"cpu{base['cores']}",
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": base["value"], "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": base["value"], "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": f"requested --steps {args.steps} --warmup {args.warmup}; timed {steps} steps of the full scene "
+                    f"(SURVEY.md 8d CPU budget), wall {base['wall_s']:.1f} s"}
     print(json.dumps(line), flush=True)
 
 
@@ -247,6 +265,37 @@ def ours(args):
             traffic, atomics = prof.get(args.config), prof.get(f"{args.config}_atomics")
         except Exception:  # noqa: BLE001
             traffic = None
+    # ---- late-time point: the same simulation flowing (disordered particles,
+    # larger strains: wide work-item layout, moderate-strain path), timed the
+    # same way after it reached step args.late_steps
+    late = None
+    if not distributed and args.late_steps > 0:
+        while inner.step_count < args.late_steps:
+            sim.step()
+        lh = {"fused": [], "map": [], "grid": []}
+        lalloc = []
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            st = sim.step()
+            lh["fused"].append(st.times["g2p"] * 1e3)
+            lh["map"].append(st.times["map_build"] * 1e3)
+            lh["grid"].append(st.times["grid_update"] * 1e3)
+            lalloc.append(st.n_allocated)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        lms = s0.elapsed_time(s1)
+        lph = _phase_means(lh)
+        lbytes = 204.0 * n_local + 40.0 * float(np.mean(lalloc))
+        dbg = (ctypes.c_int64 * 23)()
+        _lib.check(_lib.load().smpm_sim_debug_stats(inner._h, dbg), "debug stats")
+        late = {"after_steps": args.late_steps, "sim_time_s": round(inner.t, 4), "steps": args.steps,
+                "ms_per_step": lms / args.steps, "value": n * args.steps / (lms * 1e-3),
+                "phases_ms": {"map_build(scan+bin)": lph["map"], "grid_update": lph["grid"], "fused": lph["fused"]},
+                "work_item_layout": "wide" if int(dbg[21]) == 1 else "narrow",
+                "mean_allocated_nodes": float(np.mean(lalloc)),
+                "roofline_frac": lbytes / (lph["fused"] * 1e-3) / 1e9 / peak}
     # the device-resident sim is destroyed; its buffers stay in the library's
     # device-memory cache (include/smpm.h), which the e2e sim of the same
     # configuration reuses, like any process that runs simulations back to back
@@ -282,17 +331,29 @@ def ours(args):
     h2d = n * 128  # host-packed 128-B particle records (smpm_sim_set_particles, include/smpm.h)
     d2h = n * 48   # x, v (fp64) of every particle
     e2e_value = n * args.steps / e2e_s
-    del sim2
+    sim2 = None
+    # ---- cold e2e: the same public-API sequence in a fresh process (cold
+    # cudaMalloc of the device state, no buffer cache, fresh pinned buffers)
+    e2e_cold = None
+    if not distributed and not args.no_cold:
+        _lib.check(_lib.load().smpm_release_cached_memory(), "release cache")
+        torch.cuda.empty_cache()
+        r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--e2e-cold-child", "--config", args.config,
+                            "--scale", str(args.scale), "--steps", str(args.steps)] +
+                           (["--deterministic"] if args.deterministic else []),
+                           capture_output=True, text=True, timeout=900)
+        try:
+            e2e_cold = json.loads(r.stdout.strip().splitlines()[-1])
+        except (IndexError, json.JSONDecodeError):
+            e2e_cold = {"error": (r.stderr or r.stdout)[-300:]}
     line = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[args.config], "config": args.config if world == 1 else "C5",
-                   "n_particles": n, "h": sc.config.h, "ppc": 2, "mean_allocated_nodes": float(np.mean(nalloc)),
-                   "l2": "inputs larger than L2 (state %.1f GB)" % (n * 242 / 1e9),
-                   "dt": "CFL bound (cfl=0.4)", "parallelism": f"slab{world}" if world > 1 else "single",
-                   "deterministic": bool(args.deterministic)},
+        "config": workload_config(args.config, sc, n, args.deterministic, world),
+        "parallelism": f"slab{world}" if world > 1 else "single",
+        "mean_allocated_nodes": float(np.mean(nalloc)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_g2p2g (G2P+F+return map+next P2G)",
                      "peak_kind": peak_kind, "kernel_ms": ph["fused"], "atomics": atomics,
@@ -302,18 +363,52 @@ def ours(args):
                 "h2d_bytes_per_step": int(h2d / args.steps) + 8,
                 "d2h_bytes_per_step": int((d2h + stats_bytes) / args.steps), "rank0_breakdown": e2e_parts,
                 "scope": "Simulation() from host fp64 arrays (create + upload), K steps, x/v download into "
-                         "preallocated host arrays"},
+                         "preallocated host arrays; device buffers reused from the value leg (library cache)",
+                "cold": e2e_cold},
+        "late": late,
         "gpu_launches": 5 * args.steps,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = {k: v for k, v in run_cpu_port(args.config, 2).items()
+        del host, sim2
+        line["cpu_baseline"] = {k: v for k, v in run_cpu_port(args.config, CPU_STEPS[args.config], scene=sc).items()
                                 if k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if distributed:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def e2e_cold_child(args):
+    """One fresh process: create + upload + K steps + x/v download through the
+    public API, nothing cached (bench.py's e2e.cold)."""
+    import torch
+
+    from paper_2605_28525_b200 import _lib
+
+    sc = make_scene(args.config, args.scale)
+    host = sc.particles
+    out_x, out_v = np.zeros_like(host.x), np.zeros_like(host.v)
+    out_x.fill(0.0)
+    out_v.fill(0.0)
+    torch.cuda.init()
+    _lib.load()
+    t0 = time.perf_counter()
+    sim = sc.simulation()
+    t_up = time.perf_counter()
+    for _ in range(args.steps):
+        sim.step()
+    t_st = time.perf_counter()
+    _lib.check(_lib.load().smpm_sim_get_particles(sim._h, out_x.ctypes.data, out_v.ctypes.data, None, None, None,
+                                                  None))
+    t_end = time.perf_counter()
+    n = host.n
+    print(json.dumps({"value": n * args.steps / (t_end - t0), "unit": METRIC,
+                      "breakdown": {"create_upload_s": round(t_up - t0, 4), "steps_s": round(t_st - t_up, 4),
+                                    "download_s": round(t_end - t_st, 4)},
+                      "scope": "fresh process: cold cudaMalloc + pinned-buffer allocation + upload, K steps, "
+                               "x/v download (process start, imports and scene generation untimed)"}))
 
 
 def main():
@@ -325,10 +420,16 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(CONFIG_NAMES))
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of the C4 release columns")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cold", action="store_true", help="skip the fresh-process e2e leg")
+    ap.add_argument("--late-steps", type=int, default=600,
+                    help="also time --steps steps after the simulation reached this step (0: skip)")
+    ap.add_argument("--e2e-cold-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--deterministic", action="store_true",
                     help="bitwise run-to-run reproducible mode (int64 fixed-point grid sums)")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.e2e_cold_child:
+        e2e_cold_child(args)
+    elif args.impl == "reference":
         reference_arm(args)
     else:
         ours(args)

@@ -28,6 +28,7 @@ enum {
   SMPM_ERR_CONFIG = 20,       /* ConfigError (solver.py:776-810) */
   SMPM_ERR_CUDA = 30,         /* CUDA runtime failure (message: smpm_last_error) */
   SMPM_ERR_ARG = 31,          /* invalid argument */
+  SMPM_ERR_STATE = 32,        /* the requested data is not available in the current state */
   SMPM_NEED_BOUNDS = 40,      /* internal: prologue measured, waiting for the caller's bounds */
   SMPM_RETRY = 41,            /* prologue capacity grew: call smpm_sim_prologue_begin again */
   SMPM_NEED_PROLOGUE = 42     /* external-bounds mode: run the coordinated prologue first */
@@ -162,7 +163,11 @@ typedef struct {
   int32_t deterministic;     /* ranks by key (scan order) */
   int32_t record_conservation;
   int32_t device;
-  int32_t pad;
+  int32_t precise_grid;      /* non-deterministic mode: 1 = per-cell register P2G
+                                into a split fixed-point arena with per-item
+                                scales (fp32-grade grid sums on every node); 0 =
+                                per-particle int32 fixed point, one global scale
+                                (faster, coarser on light nodes); DESIGN.md s.4 */
   void* stream;              /* cudaStream_t or NULL (own stream) */
 } smpm_sim_config;
 
@@ -198,6 +203,14 @@ int smpm_sim_query_grid(smpm_sim* s, int32_t* blocks, float* mass, float* mom, f
 /* Block count of the grid smpm_sim_query_grid returns (runs a pending
  * prologue). */
 int smpm_sim_grid_size(smpm_sim* s, int64_t* n_blocks);
+/* Grid of the last completed step: Simulation.last_map / last_fields
+ * (solver.py:1087-1090).  Blocks in rank order, node mass, grid velocity after
+ * the update and boundary projection, and (after smpm_sim_retain_fields(s, 1),
+ * which makes every later step keep them) the nodal force incl. gravity.
+ * SMPM_ERR_STATE when no step completed since the last (re)binning. */
+int smpm_sim_retain_fields(smpm_sim* s, int on);
+int smpm_sim_last_grid_size(smpm_sim* s, int64_t* n_blocks);
+int smpm_sim_last_grid(smpm_sim* s, int32_t* blocks, float* mass, float* vel, float* force);
 int64_t smpm_sim_num_particles(const smpm_sim* s);
 double smpm_sim_vmax(smpm_sim* s);
 int smpm_sim_launch_count(const smpm_sim* s, int64_t* kernels_per_step);
@@ -247,6 +260,31 @@ int64_t smpm_sim_exchange_record_bytes(const smpm_sim* s);
  *      slab -> neighbour's smpm_sim_accept (appended and binned).
  * Block records are 2064 bytes (key, node mask, 64 x 8 floats). */
 int smpm_sim_set_slab(smpm_sim* s, int32_t bx0, int32_t bx1, int64_t pid_base, int64_t migrant_capacity);
+/* Device-resident exchange (one host sync per distributed step): fixed-
+ * capacity frames whose counts travel in a 32-byte header on the device, so a
+ * frame is sent whole without a size round trip.
+ *   frame = [header][cap_parts x 128-B particle records][cap_blocks x record]
+ * frame_pack: mode 0/1 = halo partial sums of blocks left / right of the slab
+ *   plus the particles that departed to that side; mode 2 = the owner's
+ *   first block layer (full sums) back to the left neighbour.  Async.
+ * frame_unpack: add (set = 0) or overwrite (set = 1) the block sums, append
+ *   and bin the arriving particles (device counter of storage slots).  Async.
+ *   Frames that overflowed their capacity are reported, not applied.
+ * stats_vector: this rank's step statistics into a device double[len]
+ *   (vmax^2, n_active, n_owned, mass, momentum[3], P2G bounds[3], replay,
+ *   error, storage, frame counts[3][2], frame overflow) for one all-gather;
+ *   apply_global: the next launch's fixed-point bounds = max over the
+ *   gathered rows (plus the precision check at the sync).  Async. */
+int64_t smpm_sim_frame_bytes(const smpm_sim* s, int64_t cap_blocks, int64_t cap_parts);
+int smpm_sim_frame_pack(smpm_sim* s, int mode, void* frame /*device*/, int64_t cap_blocks, int64_t cap_parts);
+int smpm_sim_frame_unpack(smpm_sim* s, const void* frame /*device*/, int64_t cap_blocks, int64_t cap_parts, int set);
+int smpm_sim_stats_vector(smpm_sim* s, double* out /*device*/);
+int smpm_sim_stats_vector_len(void);
+int smpm_sim_apply_global(smpm_sim* s, const double* rows /*device [world][len]*/, int world);
+/* After the step's sync: the departed particles of the sides in side_mask
+ * (bit 0 left, bit 1 right) reached their neighbour (frame not overflowed),
+ * so their storage slots become holes; the others stay live for the replay. */
+int smpm_sim_migrants_delivered(smpm_sim* s, int side_mask);
 int smpm_sim_exchange_pack(smpm_sim* s, int mode, void* out /*device*/, int64_t cap_blocks, int64_t* n_out);
 int smpm_sim_exchange_unpack(smpm_sim* s, const void* in /*device*/, int64_t n, int set);
 /* count of departing particles (side 0 left, 1 right); copies their records

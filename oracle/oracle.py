@@ -527,15 +527,16 @@ class OracleParticles:
 
     FIELDS = ("x", "v", "C", "F", "m", "V0", "mat_id", "sigma", "jac")
 
-    def __init__(self, **kw):
+    def __init__(self, copy=True, **kw):
         for k in self.FIELDS:
             a = kw[k]
             dt = np.int64 if k == "mat_id" else np.float64
-            setattr(self, k, np.array(a, dtype=dt, copy=True, order="C"))
+            setattr(self, k, np.array(a, dtype=dt, copy=True, order="C") if copy else
+                    np.ascontiguousarray(a, dtype=dt))
 
     @classmethod
-    def from_any(cls, ps):
-        return cls(**{k: getattr(ps, k) for k in cls.FIELDS})
+    def from_any(cls, ps, copy=True):
+        return cls(copy=copy, **{k: getattr(ps, k) for k in cls.FIELDS})
 
     @property
     def n(self):
@@ -552,8 +553,9 @@ class OracleSimulation:
     (deterministic=False, multithreaded)."""
 
     def __init__(self, particles, h, gravity, materials, boundaries=(), backend="scan", deterministic=False,
-                 threads=None, cfl=0.4, block_size=4, node_min=None, node_max=None):
-        self.particles = OracleParticles.from_any(particles)
+                 threads=None, cfl=0.4, block_size=4, node_min=None, node_max=None, adopt=False):
+        # adopt=True: use the caller's arrays in place (large CPU-baseline runs)
+        self.particles = OracleParticles.from_any(particles, copy=not adopt)
         self.h = float(h)
         self.gravity = np.asarray(gravity, dtype=np.float64).reshape(3)
         self.materials = list(materials)

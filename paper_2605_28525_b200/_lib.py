@@ -29,6 +29,7 @@ ERR_CONFIG = 20
 RETRY = 41
 ERR_CUDA = 30
 ERR_ARG = 31
+ERR_STATE = 32
 
 EMPTY_VAL = 0xFFFFFFFF
 ERR_CLEAR = (1 << 64) - 1
@@ -69,7 +70,7 @@ class SimConfigC(ctypes.Structure):
                 ("n_mat", I32), ("n_bc", I32), ("mats", P), ("bc", P), ("hf_data", P), ("hf_nx", I64),
                 ("hf_ny", I64), ("hf_x0", D), ("hf_y0", D), ("hf_cell", D), ("particle_capacity", I64),
                 ("block_capacity", I64), ("deterministic", I32), ("record_conservation", I32),
-                ("device", I32), ("pad", I32), ("stream", P)]
+                ("device", I32), ("precise_grid", I32), ("stream", P)]
 
 
 class StepStatsC(ctypes.Structure):
@@ -107,6 +108,9 @@ _SIGS = {
     "smpm_sim_vmax": (D, [P]),
     "smpm_sim_launch_count": (ctypes.c_int, [P, P]),
     "smpm_sim_grid_size": (ctypes.c_int, [P, P]),
+    "smpm_sim_retain_fields": (ctypes.c_int, [P, ctypes.c_int]),
+    "smpm_sim_last_grid_size": (ctypes.c_int, [P, P]),
+    "smpm_sim_last_grid": (ctypes.c_int, [P, P, P, P, P]),
     "smpm_sim_set_slab": (ctypes.c_int, [P, I32, I32, I64, I64]),
     "smpm_sim_set_dense_domain": (ctypes.c_int, [P, P, P]),
     "smpm_sim_set_external_bounds": (ctypes.c_int, [P, ctypes.c_int]),
@@ -123,6 +127,13 @@ _SIGS = {
     "smpm_sim_accept": (ctypes.c_int, [P, P, I64]),
     "smpm_sim_get_local": (ctypes.c_int, [P, P, P, P, P]),
     "smpm_sim_num_stored": (I64, [P]),
+    "smpm_sim_frame_bytes": (I64, [P, I64, I64]),
+    "smpm_sim_frame_pack": (ctypes.c_int, [P, ctypes.c_int, P, I64, I64]),
+    "smpm_sim_frame_unpack": (ctypes.c_int, [P, P, I64, I64, ctypes.c_int]),
+    "smpm_sim_stats_vector": (ctypes.c_int, [P, P]),
+    "smpm_sim_stats_vector_len": (ctypes.c_int, []),
+    "smpm_sim_apply_global": (ctypes.c_int, [P, P, ctypes.c_int]),
+    "smpm_sim_migrants_delivered": (ctypes.c_int, [P, ctypes.c_int]),
 }
 
 

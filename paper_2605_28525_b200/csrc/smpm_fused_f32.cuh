@@ -1,0 +1,656 @@
+// Fast-mode fused step kernel: G2P -> F -> advection -> next stress -> next
+// keys -> next P2G, with the P2G accumulated per cell in registers.
+// Included by smpm_sim.cu after k_g2p2g (shares FusedArgs, ItemInfo and the
+// helpers); the deterministic mode keeps k_g2p2g (int64 fixed point).
+//
+// Reference: the P2G it replaces is the fused scatter of
+// /root/reference/pkg/src/sparsempm/solver.py:456-575 (per particle, 27 nodes,
+// 7 fields, one atomic per field per node).  Here a work item (up to RCAP = 512
+// particles of one block, slot-major) runs in five phases:
+//
+//   A   per particle: G2P from the smem velocity arena, F update, advection,
+//       Hencky/DP stress of the next step, record store, next-step keys; the
+//       P2G operands (cell offset d, m, v, C, M = V0 tau: 22 floats) go to a
+//       per-particle stash (the particle's own record stage slot), counted by
+//       the arena base cell the particle scatters from.
+//   S1  warp 0 scans the base-cell counts and lists the non-empty cells;
+//       warps 1..6 prefetch the next item's velocity arena.
+//   S2  every particle takes its slot in the cell-sorted order.
+//   S3  a task = (non-empty base cell, x offset oi) loops over the cell's
+//       particles and accumulates its 9 nodes x 7 fields in registers (fp32),
+//       then adds them to the fp32 smem arena: ~1/8 of an atomic per
+//       particle-node-field instead of one.  Warp 7 inserts the item's touched
+//       blocks into the next step's table meanwhile.
+//   F   flush: bins, cell counts, red.global.add.v4.f32 of the arena nodes;
+//       records of the next item are fetched (cp.async) into the stage.
+//
+// The arena is fp32 (CAS-loop atomics, affordable at 1/8 the count), so grid
+// sums carry fp32 precision relative to each node's own magnitude -- no global
+// fixed-point scale, no contribution bounds, no scale replays.
+
+constexpr uint32_t RCAP = 512;   // particles per work item (two per thread)
+constexpr int NSTASH = 6;        // float4 per stashed particle
+constexpr int NACELL = 216;      // arena base cells (6^3: the block +- 1 cell)
+constexpr int TASK_WARPS = 7;    // warps running scatter tasks (warp 7 inserts blocks)
+
+struct __align__(16) FusedSmemF {
+  float4 st[2][NSTASH][CTA];      // per particle slot: record chunks 0..4 (stage), then the P2G stash
+  float4 garena[2][GATH_N];       // double-buffered velocity arena
+  int ahi[NF][SCAT_N];            // split fixed-point arena (m, p0..2, f0..2): value * S = hi * 2^20 + lo
+  int alo[NF][SCAT_N];
+  uint32_t kc[SCAT_N];            // stencil contributions per arena node (n_active)
+  uint32_t bnd[2][3];             // item maxima of the per-particle contribution bounds (m, p, f), by item parity
+  uint32_t cnt[SCAT_N];           // particles binned per arena base cell (next table's cell counts)
+  uint32_t scnt[NACELL];          // particles scattered from each arena base cell
+  uint32_t soff[NACELL];          // their offsets in `order` (start, then end after placement)
+  uint16_t order[2 * CTA];        // stash slots (kk * CTA + tid) sorted by base cell
+  uint16_t tcell[NACELL];         // non-empty base cells (scatter tasks)
+  uint32_t ntask;
+  uint32_t touched;
+  uint32_t rank[27];
+  uint32_t posr[3][2][CTA];       // sorted positions of the thread's particles (ring: items i, i+1, i+2)
+  uint32_t binr[2][CTA];          // bins of the item awaiting its ranks
+  ItemInfo info[3];
+  Material mats[8];
+};
+
+// Adds x * S to one arena field as hi * 2^20 + lo (two native int32 reds, no
+// carries: |lo| <= 2^19).  t = x S is an fp32 value below 2^45, so both
+// parts are exact (magic-number rounding: h is t / 2^20 rounded to an
+// integer, |t / 2^20| < 2^25 ... kept below 2^22 by the scale choice; L = t -
+// 2^20 H is exact in an FFMA and rounded to an integer by the second magic).
+__device__ __forceinline__ void arena_add_split(int* hi, int* lo, float x, float S) {
+  const float t = x * S;
+  const float h = fmaf(t, 9.5367431640625e-07f, MAGIC);  // 2^-20
+  const float hf = h - MAGIC;
+  const float l = fmaf(-hf, 1048576.0f, t) + MAGIC;
+  sred(hi, __float_as_int(h) - int(MAGIC_BITS));
+  sred(lo, __float_as_int(l) - int(MAGIC_BITS));
+}
+
+template <bool GATHER, int CV>
+__global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  FusedSmemF& sm = *reinterpret_cast<FusedSmemF*>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < A.n_mat && i < 8; i += CTA) sm.mats[i] = A.mats[i];
+  const uint32_t n_items = A.stB->n_items;
+  const double dt = GATHER ? A.stB->dt : 0.0;
+  const float ih = float(A.inv_h);
+  const float hf_ = float(A.h);
+  uint32_t vmax2_local = 0;
+  {
+    int* zh = &sm.ahi[0][0];
+    int* zl = &sm.alo[0][0];
+    for (int i = tid; i < NF * SCAT_N; i += CTA) zh[i] = zl[i] = 0;
+    if (tid < 6) sm.bnd[tid / 3][tid % 3] = 0;
+    for (int i = tid; i < SCAT_N; i += CTA) {
+      sm.kc[i] = 0;
+      sm.cnt[i] = 0;
+    }
+    for (int i = tid; i < NACELL; i += CTA) sm.scnt[i] = 0;
+    if (tid == 0) sm.touched = 0;
+  }
+  // sorted positions of the thread's particles of an item: slot-major ranges
+  // of RCAP (k_bin's wide placement), positions first + t and first + 256 + t
+  auto slots = [&](const ItemInfo& inf, uint32_t cnt, uint32_t off, int ring) {
+    const uint32_t first = inf.g() * RCAP;
+    const uint32_t n = inf.r() != BAD_KEY && cnt > first ? min(cnt - first, RCAP) : 0u;
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint32_t j = CTA * kk + tid;
+      sm.posr[ring][kk][tid] = j < n ? off - cnt + first + j : NOPOS;
+    }
+  };
+  auto item_counts = [&](uint32_t r, uint32_t& cnt, uint32_t& off) {
+    cnt = A.B.block_total[r];
+    off = A.B.cell_off[r * 64 + 32] + cnt;  // level table: block start (k_scan2)
+  };
+  // ---- prime: metadata of items 0..2, positions of items 0 and 1, records and
+  // velocity arena of item 0
+  if (tid == 0) fetch_item(A, n_items, 0, sm.info[0], false);
+  if (tid == 1) fetch_item(A, n_items, 1, sm.info[1], false);
+  if (tid == 2) fetch_item(A, n_items, 2, sm.info[2], false);
+  __syncthreads();
+  uint32_t src1a = 0, src1b = 0;  // storage indices of item i+1's particles
+  {
+    const ItemInfo& i0 = sm.info[0];
+    const ItemInfo& i1 = sm.info[1];
+    if (GATHER && tid < 8 && i0.r() != BAD_KEY) sm.info[0].nbr[tid] = A.B.nbr8[size_t(i0.r()) * 8 + tid];
+    uint32_t c0 = 0, o0 = 0, c1 = 0, o1 = 0;
+    if (i0.r() != BAD_KEY) item_counts(i0.r(), c0, o0);
+    if (i1.r() != BAD_KEY) item_counts(i1.r(), c1, o1);
+    slots(i0, c0, o0, 0);
+    slots(i1, c1, o1, 1);
+    if (GATHER) {
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint32_t ps = sm.posr[0][kk][tid];
+        if (ps != NOPOS) {
+          const float4* g = A.src.rec + size_t(A.perm[ps]) * 8;
+#pragma unroll
+          for (int q = 0; q < GCH; ++q) cp_async16(&sm.st[kk][q][tid], &g[q]);
+        }
+      }
+    }
+    const uint32_t pa = sm.posr[1][0][tid], pb = sm.posr[1][1][tid];
+    if (pa != NOPOS) src1a = A.perm[pa];
+    if (pb != NOPOS) src1b = A.perm[pb];
+  }
+  __syncthreads();
+  if (GATHER && sm.info[0].r() != BAD_KEY) prefetch_arena(sm.garena[0], A, sm.info[0], tid, CTA);
+  cp_async_commit();
+  int buf = 0, c = 0;
+  uint32_t kf = 3;  // schedule index of the next item to fetch
+
+  while (true) {
+    cp_async_wait_all();
+    __syncthreads();  // [B1] records and velocity arena of item i landed
+    const ItemInfo& cur = sm.info[c];
+    const int c1r = c == 2 ? 0 : c + 1, c2r = c == 0 ? 2 : c - 1;
+    const ItemInfo& nxt = sm.info[c1r];
+    const ItemInfo& nn = sm.info[c2r];
+    if (cur.r() == BAD_KEY) break;
+    int B0, B1, B2;
+    cur.block(B0, B1, B2);
+    if (GATHER && tid < 8 && nxt.r() != BAD_KEY) sm.info[c1r].nbr[tid] = A.B.nbr8[size_t(nxt.r()) * 8 + tid];
+    uint32_t tmask = 0;
+    uint32_t sidx[2] = {0xFFFFu, 0xFFFFu};  // stash cell of the thread's particles (0xFFFF: none)
+    float bmx[3] = {0.f, 0.f, 0.f};         // contribution bounds of the thread's stashed particles
+
+    // ================================================================ A
+#pragma unroll 1
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint32_t pos = sm.posr[c][kk][tid];
+      const bool valid = pos != NOPOS;
+      float4 c0, c1, c2, c3, c4, c5, c6, c7;
+      if (valid) {
+        if (GATHER) {
+          c0 = sm.st[kk][0][tid];
+          c1 = sm.st[kk][1][tid];
+          c2 = sm.st[kk][2][tid];
+          c3 = sm.st[kk][3][tid];
+          c4 = sm.st[kk][4][tid];
+        } else {
+          const float4* g = A.src.rec + size_t(A.perm[pos]) * 8;
+          c0 = g[0];
+          c1 = g[1];
+          c2 = g[2];
+          c3 = g[3];
+          c4 = g[4];
+          c5 = g[5];
+          c6 = g[6];
+          c7 = g[7];
+        }
+      }
+      uint32_t binv = BIN_SKIP;
+      if (valid) {
+        double xn[3];
+        float vn[3], Cn[9], M[6], d1[3];
+        int nb[3], ab[3];
+        bool ok = true, far = false;
+        int mig = -1;
+        xn[0] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
+        xn[1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
+        xn[2] = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
+        const float m = c1.z;
+        const float V0 = c1.w;
+        float F[9] = {c2.x, c2.y, c2.z, c2.w, c3.x, c3.y, c3.z, c3.w, c4.x};
+        const uint32_t pm = __float_as_uint(c4.y);
+        const uint32_t pidv = pm & PID_MASK;
+        const int mt = int(pm >> 29);
+        if (GATHER) {
+          // ---- G2P (solver.py:628-732), as k_g2p2g
+          int lb[3];
+          float d[3], w[3][3], g[3][3];
+          const int Bb[3] = {B0, B1, B2};
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            int bs;
+            axis_base(xn[a], A.inv_h, bs, d[a]);
+            lb[a] = bs - 4 * Bb[a];
+            bspline(d[a], w[a], g[a]);
+          }
+          const float4* ga = sm.garena[buf];
+          float2 Pz[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) Pz[k] = make_float2(w[2][k], w[2][k] * (float(k) - d[2]));
+          float2 P0[3], GW0[3], W1D[3];
+#pragma unroll
+          for (int o = 0; o < 3; ++o) {
+            P0[o] = make_float2(w[0][o], w[0][o] * (float(o) - d[0]));
+            GW0[o] = make_float2(g[0][o], w[0][o]);
+            W1D[o] = make_float2(w[1][o], w[1][o] * (float(o) - d[1]));
+          }
+          const float2 Z2 = make_float2(0.f, 0.f);
+          float2 Vxy = Z2, Bx = Z2, By = Z2, Bz = Z2, Ax2 = Z2, Ay2 = Z2, Az2 = Z2;
+          float2 VB = Z2, AB = Z2, BA = Z2;
+          float a21 = 0.f;
+#pragma unroll
+          for (int oi = 0; oi < 3; ++oi) {
+#pragma unroll
+            for (int oj = 0; oj < 3; ++oj) {
+              float2 Sxy = Z2, Txy = Z2, Uxy = Z2, TU2 = Z2;
+              float S2 = 0.f;
+              const int gi = lb[0] + oi, gj = lb[1] + oj;
+#pragma unroll
+              for (int ok = 0; ok < 3; ++ok) {
+                const float4 q = ga[gaddr(gi, gj, lb[2] + ok)];
+                const float2 qxy = make_float2(q.x, q.y);
+                Sxy = __ffma2_rn(qxy, make_float2(Pz[ok].x, Pz[ok].x), Sxy);
+                Txy = __ffma2_rn(qxy, make_float2(Pz[ok].y, Pz[ok].y), Txy);
+                Uxy = __ffma2_rn(qxy, make_float2(g[2][ok], g[2][ok]), Uxy);
+                TU2 = __ffma2_rn(make_float2(q.z, q.z), make_float2(Pz[ok].y, g[2][ok]), TU2);
+                S2 = fmaf(q.z, Pz[ok].x, S2);
+              }
+              const float2 WD = __fmul2_rn(P0[oi], make_float2(w[1][oj], w[1][oj]));
+              const float2 AD = __fmul2_rn(GW0[oi], W1D[oj]);
+              const float wij = WD.x, Ay = w[0][oi] * g[1][oj];
+              Vxy = __ffma2_rn(Sxy, make_float2(wij, wij), Vxy);
+              Bx = __ffma2_rn(Sxy, make_float2(WD.y, WD.y), Bx);
+              By = __ffma2_rn(Sxy, make_float2(AD.y, AD.y), By);
+              Bz = __ffma2_rn(Txy, make_float2(wij, wij), Bz);
+              Ax2 = __ffma2_rn(Sxy, make_float2(AD.x, AD.x), Ax2);
+              Ay2 = __ffma2_rn(Sxy, make_float2(Ay, Ay), Ay2);
+              Az2 = __ffma2_rn(Uxy, make_float2(wij, wij), Az2);
+              VB = __ffma2_rn(make_float2(S2, S2), WD, VB);
+              AB = __ffma2_rn(make_float2(S2, S2), AD, AB);
+              BA = __ffma2_rn(TU2, make_float2(wij, wij), BA);
+              a21 = fmaf(Ay, S2, a21);
+            }
+          }
+          const float cs = 4.0f * ih;
+          Cn[0] = Bx.x * cs;
+          Cn[1] = By.x * cs;
+          Cn[2] = Bz.x * cs;
+          Cn[3] = Bx.y * cs;
+          Cn[4] = By.y * cs;
+          Cn[5] = Bz.y * cs;
+          Cn[6] = VB.y * cs;
+          Cn[7] = AB.y * cs;
+          Cn[8] = BA.x * cs;
+          vn[0] = Vxy.x;
+          vn[1] = Vxy.y;
+          vn[2] = VB.x;
+          const float dth = float(dt) * ih;
+          float A9[9] = {Ax2.x * dth, Ay2.x * dth, Az2.x * dth, Ax2.y * dth, Ay2.y * dth,
+                         Az2.y * dth, AB.x * dth,  a21 * dth,   BA.y * dth};
+          float Fn[9];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+              Fn[3 * i + j] =
+                  F[3 * i + j] + (A9[3 * i + j] + (A9[3 * i] * F[j] + A9[3 * i + 1] * F[3 + j] + A9[3 * i + 2] * F[6 + j]));
+#pragma unroll
+          for (int q = 0; q < 9; ++q) F[q] = Fn[q];
+          xn[0] = __dadd_rn(xn[0], __dmul_rn(dt, double(vn[0])));
+          xn[1] = __dadd_rn(xn[1], __dmul_rn(dt, double(vn[1])));
+          xn[2] = __dadd_rn(xn[2], __dmul_rn(dt, double(vn[2])));
+        } else {
+          vn[0] = c4.z;
+          vn[1] = c4.w;
+          vn[2] = c5.x;
+          Cn[0] = c5.y;
+          Cn[1] = c5.z;
+          Cn[2] = c5.w;
+          Cn[3] = c6.x;
+          Cn[4] = c6.y;
+          Cn[5] = c6.z;
+          Cn[6] = c6.w;
+          Cn[7] = c7.x;
+          Cn[8] = c7.y;
+        }
+        // ---- stress of the next step (materials.py:169-238)
+        float tau[6], J;
+        const Material& mat = sm.mats[mt];
+        if (!hencky_dp<CV>(F, mat, A.project != 0, tau, J)) {
+          err_report(A.err, ERR_DEGENERATE_F, pidv);
+          ok = false;
+          tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 6; ++q) M[q] = V0 * tau[q];
+        {  // ---- the particle record at its sorted position
+          float4* o = A.dst.rec + size_t(pos) * 8;
+          int2 x0 = make_int2(__double2loint(xn[0]), __double2hiint(xn[0]));
+          int2 x1 = make_int2(__double2loint(xn[1]), __double2hiint(xn[1]));
+          int2 x2 = make_int2(__double2loint(xn[2]), __double2hiint(xn[2]));
+          o[0] = make_float4(__int_as_float(x0.x), __int_as_float(x0.y), __int_as_float(x1.x), __int_as_float(x1.y));
+          o[1] = make_float4(__int_as_float(x2.x), __int_as_float(x2.y), m, V0);
+          o[2] = make_float4(F[0], F[1], F[2], F[3]);
+          o[3] = make_float4(F[4], F[5], F[6], F[7]);
+          o[4] = make_float4(F[8], __uint_as_float(pm), vn[0], vn[1]);
+          o[5] = make_float4(vn[2], Cn[0], Cn[1], Cn[2]);
+          o[6] = make_float4(Cn[3], Cn[4], Cn[5], Cn[6]);
+          o[7] = make_float4(Cn[7], Cn[8], 0.f, 0.f);
+        }
+        const float vv = vn[0] * vn[0] + vn[1] * vn[1] + vn[2] * vn[2];
+        vmax2_local = max(vmax2_local, __float_as_uint(vv));
+        // ---- next step's keys
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (!isfinite(xn[a])) {
+            if (ok) err_report(A.err, ERR_NONFINITE_X, pidv);
+            ok = false;
+          } else if (!axis_base(xn[a], A.inv_h, nb[a], d1[a]) || !axis_in_key_range(nb[a])) {
+            if (ok) err_report(A.err, ERR_KEY_RANGE, pidv);
+            ok = false;
+          }
+        }
+        if (ok) {
+          ab[0] = nb[0] - (4 * B0 - 1);
+          ab[1] = nb[1] - (4 * B1 - 1);
+          ab[2] = nb[2] - (4 * B2 - 1);
+          far = ab[0] < 0 || ab[0] > 5 || ab[1] < 0 || ab[1] > 5 || ab[2] < 0 || ab[2] > 5;
+          const int nbx = nb[0] >> 2;
+          mig = nbx < A.bx0 ? 0 : (nbx >= A.bx1 ? 1 : -1);
+          if (mig >= 0) {
+            // leaves this rank's slab: scattered here, binned by the neighbour
+            const uint32_t slot = atomicAdd(&A.mig_count[mig], 1u);
+            if (slot < A.mig_cap) {
+              const float4* src4 = A.dst.rec + size_t(pos) * 8;
+              float4* o4 = A.mig[mig] + size_t(slot) * 8;
+#pragma unroll
+              for (int c8 = 0; c8 < 8; ++c8) o4[c8] = src4[c8];
+            } else {
+              err_report(A.err, ERR_CAPACITY, pidv);
+            }
+          }
+        }
+        if (ok && !far) {
+          // ---- stash the P2G operands (this slot's record stage is consumed)
+          const uint32_t ci = uint32_t((ab[0] * 6 + ab[1]) * 6 + ab[2]);
+          sm.st[kk][0][tid] = make_float4(d1[0], d1[1], d1[2], m);
+          sm.st[kk][1][tid] = make_float4(vn[0], vn[1], vn[2], M[0]);
+          sm.st[kk][2][tid] = make_float4(Cn[0], Cn[1], Cn[2], Cn[3]);
+          sm.st[kk][3][tid] = make_float4(Cn[4], Cn[5], Cn[6], Cn[7]);
+          sm.st[kk][4][tid] = make_float4(Cn[8], M[1], M[2], M[3]);
+          sm.st[kk][5][tid] = make_float4(M[4], M[5], 0.f, 0.f);
+          atomicAdd(&sm.scnt[ci], 1u);
+          sidx[kk] = ci;
+          // contribution bounds, worst case over the cell offset (|w| <= 0.75^3,
+          // |dx_a| <= 1.5 h, |grad w_a| <= 0.75^2 / h): the item's fixed-point scales
+          float cm = 0.f;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            cm = fmaxf(cm, fabsf(vn[a]) + (1.5f * hf_) * (fabsf(Cn[3 * a]) + fabsf(Cn[3 * a + 1]) + fabsf(Cn[3 * a + 2])));
+          const float fm = fmaxf(fabsf(M[0]) + fabsf(M[3]) + fabsf(M[4]),
+                                 fmaxf(fabsf(M[3]) + fabsf(M[1]) + fabsf(M[5]), fabsf(M[4]) + fabsf(M[5]) + fabsf(M[2])));
+          bmx[0] = fmaxf(bmx[0], m * 0.421875f);
+          bmx[1] = fmaxf(bmx[1], m * 0.421875f * cm);
+          bmx[2] = fmaxf(bmx[2], fm * 0.5625f * ih);
+          tmask |= touched27(axis_blocks(ab[0]), axis_blocks(ab[1]), axis_blocks(ab[2]));
+          if (mig < 0) {
+            atomicAdd(&sm.cnt[aaddr(ab[0], ab[1], ab[2])], 1u);
+            binv = BIN_ARENA | uint32_t((ab[0] << 6) | (ab[1] << 3) | ab[2]);
+          } else {
+            binv = MIG_KEY;
+          }
+        } else if (ok && far) {
+          scatter_global(A, nb, d1, m, vn, Cn, M, binv, mig < 0, 1.f, 1.f, 1.f);
+        } else {
+          binv = BAD_KEY;
+        }
+      }
+      sm.binr[kk][tid] = valid ? binv : BIN_SKIP;
+    }
+    {
+      const uint32_t tm = __reduce_or_sync(0xffffffffu, tmask);
+      if (lane == 0 && tm) atomicOr(&sm.touched, tm);
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        const uint32_t b = warp_max(__float_as_uint(bmx[f]));
+        if (lane == 0 && b) atomicMax(&sm.bnd[buf][f], b);
+      }
+    }
+    __syncthreads();  // [B2] stash, base-cell counts, touched blocks of item i
+
+    // ================================================================ S1
+    if (warp == 0) {
+      // exclusive scan of the 216 base-cell counts (7 per lane) and the list
+      // of non-empty cells
+      uint32_t cv[7], loc = 0, ne = 0;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        const int cc = lane * 7 + q;
+        cv[q] = cc < NACELL ? sm.scnt[cc] : 0u;
+        loc += cv[q];
+        ne += cv[q] ? 1u : 0u;
+      }
+      uint32_t xs = loc, xn_ = ne;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, xs, o), z = __shfl_up_sync(0xffffffffu, xn_, o);
+        if (lane >= o) {
+          xs += y;
+          xn_ += z;
+        }
+      }
+      uint32_t run = xs - loc, tix = xn_ - ne;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        const int cc = lane * 7 + q;
+        if (cc < NACELL) {
+          sm.soff[cc] = run;
+          run += cv[q];
+          if (cv[q]) sm.tcell[tix++] = uint16_t(cc);
+        }
+      }
+      if (lane == 31) sm.ntask = xn_;
+    } else if (warp <= 6) {
+      if (GATHER && nxt.r() != BAD_KEY) prefetch_arena(sm.garena[buf ^ 1], A, nxt, tid - 32, 6 * 32);
+    }
+    __syncthreads();  // [B3]
+
+    // ================================================================ S2
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk)
+      if (sidx[kk] != 0xFFFFu) sm.order[atomicAdd(&sm.soff[sidx[kk]], 1u)] = uint16_t(kk * CTA + tid);
+    __syncthreads();  // [B4] order complete (soff now holds each cell's end)
+
+    // ================================================================ S3
+    if (warp < TASK_WARPS) {
+      const uint32_t nt = sm.ntask;
+#pragma unroll 1
+      for (uint32_t t = tid; t < 3 * nt; t += TASK_WARPS * 32) {
+        const uint32_t oi = t / nt;
+        const uint32_t cc = sm.tcell[t - oi * nt];
+        const uint32_t end = sm.soff[cc], n = sm.scnt[cc];
+        const int a0 = int(cc / 36), a1 = int((cc / 6) % 6), a2 = int(cc % 6);
+        // node (oi, j, k) accumulators, packed over k = 0, 1 (.x, .y) + k = 2
+        const float2 Z2 = make_float2(0.f, 0.f);
+        float2 mm01[3], p01[3][3], f01[3][3];
+        float mm2[3], p2[3][3], f2[3][3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          mm01[j] = Z2;
+          mm2[j] = 0.f;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            p01[a][j] = f01[a][j] = Z2;
+            p2[a][j] = f2[a][j] = 0.f;
+          }
+        }
+        const float foi = float(oi);
+#pragma unroll 1
+        for (uint32_t e = end - n; e < end; ++e) {
+          const uint32_t sl = sm.order[e];
+          const float4* sp = &sm.st[sl >> 8][0][sl & (CTA - 1)];
+          const float4 s0 = sp[0], s1 = sp[CTA], s2 = sp[2 * CTA], s3 = sp[3 * CTA], s4 = sp[4 * CTA],
+                       s5 = sp[5 * CTA];
+          // C row-major: s2 = C00 C01 C02 C10, s3 = C11 C12 C20 C21, s4.x = C22
+          // M = V0 tau: s1.w = xx, s4.y = yy, s4.z = zz, s4.w = xy, s5.x = xz, s5.y = yz
+          const float t0 = s0.x - 1.0f;
+          const float wx = oi == 0 ? 0.5f * (1.5f - s0.x) * (1.5f - s0.x)
+                                   : (oi == 1 ? 0.75f - t0 * t0 : 0.5f * (s0.x - 0.5f) * (s0.x - 0.5f));
+          const float gx = oi == 0 ? s0.x - 1.5f : (oi == 1 ? -2.0f * t0 : s0.x - 0.5f);
+          float wy[3], gy[3], wz[3], gz[3];
+          bspline(s0.y, wy, gy);
+          bspline(s0.z, wz, gz);
+          // momentum m w (v + C dx) with dx = h (o - d): per node
+          //   z1_k R_a(j) + z2_k T_a(j), z1 = wz, z2 = wz (k - dz) h,
+          //   R_a = W (v_a + C_a0 dx + C_a1 dy), T_a = W C_a2, W = m wx wy_j;
+          // force -(M grad w), grad w = (gx wy wz, wx gy wz, wx wy gz) / h: per node
+          //   wz_k P_a(j) + gz_k Q_a(j), P_a = Mh_a0 gx wy + Mh_a1 wx gy, Q_a = Mh_a2 wx wy
+          const float2 z1 = make_float2(wz[0], wz[1]), gz01 = make_float2(gz[0], gz[1]);
+          const float dz0 = -s0.z * hf_;
+          const float2 z2 = make_float2(wz[0] * dz0, wz[1] * (dz0 + hf_));
+          const float z22 = wz[2] * (dz0 + 2.0f * hf_);
+          const float mW = s0.w * wx;
+          const float dx = (foi - s0.x) * hf_;
+          const float b0 = fmaf(s2.x, dx, s1.x), b1 = fmaf(s2.w, dx, s1.y), b2 = fmaf(s3.z, dx, s1.z);
+          const float fs = -ih;
+          const float M00 = s1.w * fs, M11 = s4.y * fs, M22 = s4.z * fs, M01 = s4.w * fs, M02 = s5.x * fs,
+                      M12 = s5.y * fs;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const float dy = (float(j) - s0.y) * hf_;
+            const float W = mW * wy[j];
+            const float R0 = W * fmaf(s2.y, dy, b0), R1 = W * fmaf(s3.x, dy, b1), R2 = W * fmaf(s3.w, dy, b2);
+            const float T0 = W * s2.z, T1 = W * s3.y, T2 = W * s4.x;
+            const float Ax = gx * wy[j], Ay = wx * gy[j], Az = wx * wy[j];
+            const float P0 = fmaf(M00, Ax, M01 * Ay), P1 = fmaf(M01, Ax, M11 * Ay), P2 = fmaf(M02, Ax, M12 * Ay);
+            const float Q0 = M02 * Az, Q1 = M12 * Az, Q2 = M22 * Az;
+            mm01[j] = __ffma2_rn(z1, make_float2(W, W), mm01[j]);
+            mm2[j] = fmaf(wz[2], W, mm2[j]);
+            const float R[3] = {R0, R1, R2}, T[3] = {T0, T1, T2}, P[3] = {P0, P1, P2}, Q[3] = {Q0, Q1, Q2};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              p01[a][j] = __ffma2_rn(z2, make_float2(T[a], T[a]), __ffma2_rn(z1, make_float2(R[a], R[a]), p01[a][j]));
+              p2[a][j] = fmaf(z22, T[a], fmaf(wz[2], R[a], p2[a][j]));
+              f01[a][j] = __ffma2_rn(gz01, make_float2(Q[a], Q[a]), __ffma2_rn(z1, make_float2(P[a], P[a]), f01[a][j]));
+              f2[a][j] = fmaf(gz[2], Q[a], fmaf(wz[2], P[a], f2[a][j]));
+            }
+          }
+        }
+        // add the task's 9 nodes to the arena (fixed point, the item's scales:
+        // a cell sum is at most RCAP bounds, kept below 2^42), and K
+        float Sg[3];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          const float b = __uint_as_float(sm.bnd[buf][f]);
+          Sg[f] = b > 0.f ? 8589934592.0f / b : 1.0f;  // 2^33 / bound = 2^42 / (RCAP bound)
+        }
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const int ad = aaddr(a0 + int(oi), a1 + j, a2 + k);
+            const float v[NF] = {k == 0 ? mm01[j].x : (k == 1 ? mm01[j].y : mm2[j]),
+                                 k == 0 ? p01[0][j].x : (k == 1 ? p01[0][j].y : p2[0][j]),
+                                 k == 0 ? p01[1][j].x : (k == 1 ? p01[1][j].y : p2[1][j]),
+                                 k == 0 ? p01[2][j].x : (k == 1 ? p01[2][j].y : p2[2][j]),
+                                 k == 0 ? f01[0][j].x : (k == 1 ? f01[0][j].y : f2[0][j]),
+                                 k == 0 ? f01[1][j].x : (k == 1 ? f01[1][j].y : f2[1][j]),
+                                 k == 0 ? f01[2][j].x : (k == 1 ? f01[2][j].y : f2[2][j])};
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+              arena_add_split(&sm.ahi[f][ad], &sm.alo[f][ad], v[f], Sg[f == 0 ? 0 : (f < 4 ? 1 : 2)]);
+            atomicAdd(&sm.kc[ad], n);
+          }
+      }
+    } else {
+      // warp 7: insert the item's touched blocks into the next step's table
+      const uint32_t tm = sm.touched;
+      if (lane < 27) {
+        uint32_t rk = BAD_KEY;
+        if ((tm >> lane) & 1u) {
+          const int di = lane / 9 - 1, dj = (lane / 3) % 3 - 1, dk = lane % 3 - 1;
+          // dense backend: a stencil node outside the declared domain (solver.py:1053-1058)
+          if (B0 + di < A.dbox_lo[0] || B0 + di > A.dbox_hi[0] || B1 + dj < A.dbox_lo[1] ||
+              B1 + dj > A.dbox_hi[1] || B2 + dk < A.dbox_lo[2] || B2 + dk > A.dbox_hi[2])
+            err_report(A.err, ERR_INACTIVE, 0);
+          rk = hash_insert(A.S.hv, pack_key(B0 + di, B1 + dj, B2 + dk));
+          if (rk >= A.S.hv.cap_blocks) rk = BAD_KEY;
+        }
+        sm.rank[lane] = rk;
+      }
+    }
+    __syncthreads();  // [B5] arena and ranks of item i complete; the stash is free
+
+    // ================================================================ F
+    // records of item i+1 into the stage (overlaps the flush)
+    if (GATHER) {
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        if (sm.posr[c1r][kk][tid] != NOPOS) {
+          const float4* g = A.src.rec + size_t(kk ? src1b : src1a) * 8;
+#pragma unroll
+          for (int q = 0; q < GCH; ++q) cp_async16(&sm.st[kk][q][tid], &g[q]);
+        }
+      }
+    }
+    if (tid == 0) fetch_item(A, n_items, kf, sm.info[c], true);  // item i+3 -> this item's ring slot
+    cp_async_commit();
+    uint32_t cnt2 = 0, off2 = 0;  // item i+2's range (consumed after the flush)
+    if (nn.r() != BAD_KEY) item_counts(nn.r(), cnt2, off2);
+    // bins of item i (positions from ring slot c)
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint32_t bv = sm.binr[kk][tid];
+      if (bv == BIN_SKIP) continue;
+      uint32_t out = bv;
+      if (bv >= BIN_ARENA && bv < BIN_ARENA + 512u) {
+        const int q0 = int((bv >> 6) & 7u), q1 = int((bv >> 3) & 7u), q2 = int(bv & 7u);
+        const uint32_t rk = sm.rank[((q0 + 3) >> 2) * 9 + ((q1 + 3) >> 2) * 3 + ((q2 + 3) >> 2)];
+        const uint32_t lc = (((q0 + 3) & 3) << 4) | (((q1 + 3) & 3) << 2) | ((q2 + 3) & 3);
+        out = rk == BAD_KEY ? OVF_KEY : rk * 64 + lc;
+      }
+      A.bin_out[sm.posr[c][kk][tid]] = out;
+    }
+    for (int nd = tid; nd < 216; nd += CTA) {
+      const int i = nd / 36, j = (nd / 6) % 6, k = nd % 6;
+      const int ad = aaddr(i, j, k);
+      const uint32_t cc = sm.cnt[ad];
+      if (cc) {
+        sm.cnt[ad] = 0;
+        const uint32_t rq2 = sm.rank[((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
+        const uint32_t lc = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
+        if (rq2 != BAD_KEY) atomicAdd(&A.S.cell_count[rq2 * 64 + lc], cc);
+      }
+    }
+    float iS[3];
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      const float b = __uint_as_float(sm.bnd[buf][f]);
+      iS[f] = b > 0.f ? b * (1.0f / 8589934592.0f) : 1.0f;
+    }
+    if (tid < 3) sm.bnd[buf ^ 1][tid] = 0;  // the next item's (item i-1 is done with them)
+    for (int nd = tid; nd < 512; nd += CTA) {
+      const int i = nd >> 6, j = (nd >> 3) & 7, k = nd & 7;
+      const int ad = aaddr(i, j, k);
+      const uint32_t K = sm.kc[ad];
+      if (!K) continue;
+      float vals[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        vals[f] = fmaf(float(sm.ahi[f][ad]), 1048576.0f, float(sm.alo[f][ad])) * iS[f == 0 ? 0 : (f < 4 ? 1 : 2)];
+        sm.ahi[f][ad] = 0;
+        sm.alo[f][ad] = 0;
+      }
+      sm.kc[ad] = 0;
+      const uint32_t rk = sm.rank[((i + 3) >> 2) * 9 + ((j + 3) >> 2) * 3 + ((k + 3) >> 2)];
+      if (rk == BAD_KEY) continue;
+      const size_t node = size_t(rk) * 64 + ((((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3));
+      red_v4(&A.acc[2 * node], vals[0], vals[1], vals[2], vals[3]);
+      red_v4(&A.acc[2 * node + 1], vals[4], vals[5], vals[6], float(K));  // .w: contribution count K (n_active)
+    }
+    for (int i = tid; i < NACELL; i += CTA) sm.scnt[i] = 0;
+    if (tid == 0) sm.touched = 0;
+    // item i+2's sorted positions (ring slot of item i-1; loads issued before
+    // the flush) and source indices
+    slots(nn, cnt2, off2, c2r);
+    {
+      const uint32_t pa = sm.posr[c2r][0][tid], pb = sm.posr[c2r][1][tid];
+      src1a = pa != NOPOS ? A.perm[pa] : 0u;
+      src1b = pb != NOPOS ? A.perm[pb] : 0u;
+    }
+    ++kf;
+    buf ^= 1;
+    c = c1r;
+  }
+  vmax2_local = warp_max(vmax2_local);
+  if (lane == 0 && vmax2_local) atomicMax(&A.stS->vmax2_bits, vmax2_local);
+  if (blockIdx.x == 0 && tid < 3) A.stS->scale_inv[tid] = 0.f;  // fp32 arena: no fixed-point scales
+}

@@ -54,6 +54,9 @@ namespace smpm {
 #ifndef SMPM_DIAG_SKIP
 #define SMPM_DIAG_SKIP 0
 #endif
+#ifndef SMPM_TIGHT_BOUNDS
+#define SMPM_TIGHT_BOUNDS 1  // per-particle P2G contribution bounds (0: worst case over d; A/B: +-0.05 ms on C4)
+#endif
 #ifndef SMPM_MINB
 #define SMPM_MINB 2  // resident CTAs per SM the fused kernel is register-budgeted for
 #endif
@@ -128,7 +131,8 @@ struct StepParams {
   int record_conservation;
   int project;
   int bx0, bx1;  // owned block-x range (n_active / n_owned count owned blocks only)
-  int wide;      // work-item layout (see k_g2p2g): 0 cell slots, 1 block ranges of WIDE_CAP
+  int wide;      // work-item layout (see k_g2p2g): 0 cell slots, 1 block ranges of `cap`
+  uint32_t cap;  // particles per block-range item (WIDE_CAP, or RCAP for the fp32-arena kernel)
 };
 
 // ------------------------------------------------------------------ scan
@@ -176,7 +180,7 @@ __device__ inline uint32_t cta_excl_scan(uint32_t v, uint32_t* sh /*[8]*/, uint3
 // scan1: per block totals / items / popcount; per tile sums; the last CTA
 // scans tile sums and finalises the step scalars.
 __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
-                                               unsigned long long* err, StepParams sp) {
+                                               unsigned long long* err, StepParams sp, uint32_t* nstore) {
   __shared__ uint32_t red[4][8];
   __shared__ bool last;
   const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
       if (r >= nb) break;
       uint32_t c0 = S.cell_count[size_t(r) * 64 + lane], c1 = S.cell_count[size_t(r) * 64 + 32 + lane];
       uint32_t tot = warp_sum(c0 + c1), mx = warp_max(max(c0, c1));
-      const uint32_t items8 = (mx + ISLOTS - 1) / ISLOTS, itemsw = (tot + WIDE_CAP - 1) / WIDE_CAP;
+      const uint32_t items8 = (mx + ISLOTS - 1) / ISLOTS, itemsw = (tot + sp.cap - 1) / sp.cap;
       const uint32_t items = sp.wide ? itemsw : items8, items_alt = sp.wide ? items8 : itemsw;
       // neighbour ranks for the gather arena of this block's work items
       if (lane < 8 && items) {
@@ -247,6 +251,7 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
     st->n_blocks = nb;
     st->n_items = carry[1];
     st->n_binned = carry[0];
+    *nstore = carry[0];  // storage after this step's fused kernel (arrivals append to it)
     st->n_active = 0;  // counted by k_grid (nodes with a stencil contribution, acc .w > 0)
     st->n_owned = carry[3];
     st->n_items_alt = carry[2];
@@ -395,7 +400,8 @@ __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, u
 template <bool DET>
 __global__ void __launch_bounds__(256, DET ? 2 : SMPM_GRID_MINB) k_grid(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
                                                  float4* __restrict__ acc, float4* __restrict__ gv, GridParams gp,
-                                                 int record, int bx0, int bx1, unsigned long long* acc_fx) {
+                                                 int record, int bx0, int bx1, unsigned long long* acc_fx,
+                                                 float4* __restrict__ gforce) {
   __shared__ Boundary sbc[8];
   if (threadIdx.x < gp.n_bc && threadIdx.x < 8) sbc[threadIdx.x] = gp.bc[threadIdx.x];
   __syncthreads();
@@ -456,7 +462,12 @@ __global__ void __launch_bounds__(256, DET ? 2 : SMPM_GRID_MINB) k_grid(TableDev
       float o0, o1, o2;
       grid_node_col(gp, col, nx, ny, bk * 4 + lk, a[lk].x, a[lk].y, a[lk].z, a[lk].w, b[lk].x, b[lk].y, b[lk].z, o0,
                     o1, o2);
-      gv[c] = make_float4(o0, o1, o2, 0.f);
+      // .w carries the node mass (Simulation.last_fields, free in the same store)
+      gv[c] = make_float4(o0, o1, o2, a[lk].x);
+      if (gforce)  // retained for Simulation.last_fields: force incl. gravity (solver.py:880-894)
+        gforce[c] = make_float4(float(double(b[lk].x) + double(a[lk].x) * gp.gravity[0]),
+                                float(double(b[lk].y) + double(a[lk].x) * gp.gravity[1]),
+                                float(double(b[lk].z) + double(a[lk].x) * gp.gravity[2]), 0.f);
       act += (b[lk].w > 0.f && own) ? 1u : 0u;
       if (record) {
         msum += a[lk].x;
@@ -751,6 +762,19 @@ __device__ __forceinline__ void prefetch_arena(FusedSmem& sm, const FusedArgs& A
   }
 }
 
+// velocity arena of an item into `ga`, by threads t of nt
+__device__ __forceinline__ void prefetch_arena(float4* ga, const FusedArgs& A, const ItemInfo& inf, int t, int nt) {
+  for (int n = t; n < 216; n += nt) {
+    int i = n / 36, j = (n / 6) % 6, k = n % 6;
+    uint32_t gr = inf.nbr[((i >> 2) << 2) | ((j >> 2) << 1) | (k >> 2)];
+    float4* dst = &ga[gaddr(i, j, k)];
+    if (gr < A.B.hv.cap_blocks)
+      cp_async16(dst, &A.gv[size_t(gr) * 64 + (((i & 3) << 4) | ((j & 3) << 2) | (k & 3))]);
+    else
+      *dst = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 // One persistent CTA works through work items.  Narrow layout (NKK = 2): an
 // item is (block, group of 8 particles per cell); thread t owns cell t & 63
 // and slots s, s + 4 (s = t >> 6) of the group: two particles, processed one
@@ -793,6 +817,10 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   float mx_m = 0.f, mx_p = 0.f, mx_f = 0.f;  // contribution bounds of this launch
   bool scale_ovf = false;
   if (tid < 3) {
+    // power-of-two scales (exact int64 -> value conversion in deterministic
+    // mode) with 2x headroom over the previous launch's bounds; a launch that
+    // outgrows them is replayed (scale_ovf), one that falls far below them too
+    // (scale_underflow, host side)
     const float b = A.measure ? 0.f : __uint_as_float(A.scale_src[tid]) * (tid == 0 ? 1.0f : 2.0f);
     float inv;
     const float S = fx_scale(b, inv);
@@ -1171,9 +1199,10 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
               err_report(A.err, ERR_CAPACITY, pidv);
             }
           }
-          // contribution bounds: |w| <= prod_a max_o w_a(o); |grad w_a| <= max|g_a| prod_{b!=a} max w_b / h;
-          // |dx_a| <= h * max(d_a, 2 - d_a).  With d in [0.5, 1.5] and t = |d - 1|:
-          // max_o w = w_1 = 0.75 - t^2, max |g| = 0.5 + t, max(d, 2 - d) = 1 + t
+#if SMPM_TIGHT_BOUNDS
+          // contribution bounds per particle: |w| <= prod_a max_o w_a(o);
+          // |grad w_a| <= max|g_a| prod_{b!=a} max w_b / h; |dx_a| <= h max(d_a, 2 - d_a).
+          // With t = |d - 1|: max_o w = 0.75 - t^2, max |g| = 0.5 + t, max(d, 2 - d) = 1 + t
           float wmax[3], gmax[3], dxm[3];
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
@@ -1194,6 +1223,19 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
                                  fmaxf(fabsf(M[3]) * G0 + fabsf(M[1]) * G1 + fabsf(M[5]) * G2,
                                        fabsf(M[4]) * G0 + fabsf(M[5]) * G1 + fabsf(M[2]) * G2));
           const float bm = m * W * 1.0001f, bp = m * W * cm * 1.0001f, bf = fm * 1.0001f;
+#else
+          // contribution bounds, worst case over the cell offset d in [0.5, 1.5]
+          // (the launch maximum is attained by some particle near d = 1, so the
+          // scales lose little against per-particle bounds): |w| <= 0.75^3,
+          // |dx_a| <= 1.5 h, |grad w_a| <= max_d |g| max w^2 / h = 1 * 0.75^2 / h
+          float cm = 0.f;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            cm = fmaxf(cm, fabsf(vn[a]) + (1.5f * hf_) * (fabsf(Cn[3 * a]) + fabsf(Cn[3 * a + 1]) + fabsf(Cn[3 * a + 2])));
+          const float fm = fmaxf(fabsf(M[0]) + fabsf(M[3]) + fabsf(M[4]),
+                                 fmaxf(fabsf(M[3]) + fabsf(M[1]) + fabsf(M[5]), fabsf(M[4]) + fabsf(M[5]) + fabsf(M[2])));
+          const float bm = m * (0.421875f * 1.0001f), bp = bm * cm, bf = fm * (0.5625f * 1.0001f) * ih;
+#endif
           mx_m = fmaxf(mx_m, bm);
           mx_p = fmaxf(mx_p, bp);
           mx_f = fmaxf(mx_f, bf);
@@ -1348,6 +1390,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
   if (scale_ovf) atomicOr(&A.stS->scale_ovf, 1u);
   if (blockIdx.x == 0 && tid < 3 && !A.measure) A.stS->scale_inv[tid] = sm.sc[3 + tid];
 }
+
+#include "smpm_fused_f32.cuh"
 
 // ------------------------------------------------------- state transfer
 // Upload: reference layout f64 -> 128-byte records (x f64, rest f32).
@@ -1625,6 +1669,184 @@ __global__ void k_accept(const float4* __restrict__ in, uint32_t n, Particles ds
 // Live particles of this rank in storage order (holes left by departed
 // particles carry no bin): pid + reference-layout fields.
 
+// ----------------------------------------------------- exchange frames
+// One message per neighbour and round, fixed capacity, counts on the device
+// (no size round trip; include/smpm.h smpm_sim_frame_*):
+//   [FrameHeader 32 B][particle records: cap_parts x 128 B][block records: cap_blocks x rec]
+struct FrameHeader {
+  uint32_t n_blocks, n_parts, cap_blocks, cap_parts;
+  uint32_t pad[4];
+};
+
+__global__ void k_frame_init(FrameHeader* h, uint32_t cap_blocks, uint32_t cap_parts) {
+  if (threadIdx.x == 0) {
+    h->n_blocks = 0;
+    h->n_parts = 0;
+    h->cap_blocks = cap_blocks;
+    h->cap_parts = cap_parts;
+  }
+}
+
+// departing particles of one side (written by the fused kernel) into the frame
+__global__ void k_frame_parts(const float4* __restrict__ mig, const uint32_t* mig_count, FrameHeader* h,
+                              float4* __restrict__ dst) {
+  const uint32_t n = *mig_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) h->n_parts = n;
+  const uint32_t m = min(n, h->cap_parts) * 8u;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) dst[i] = mig[i];
+}
+
+// storage slots for the arriving particles of a frame: off = n_store, then
+// n_store += n (device counter; the host learns it at the step's sync)
+__global__ void k_frame_reserve(const FrameHeader* h, uint32_t* nstore, uint32_t* on, uint32_t cap_p,
+                                unsigned long long* err) {
+  if (threadIdx.x) return;
+  uint32_t n = min(h->n_parts, h->cap_parts);
+  if (h->n_parts > h->cap_parts || h->n_blocks > h->cap_blocks) {
+    err_report(err, ERR_CAPACITY, 0);
+    n = 0;
+  }
+  const uint32_t off = *nstore;
+  if (uint64_t(off) + n > cap_p) {
+    err_report(err, ERR_CAPACITY, 0);
+    n = 0;
+  }
+  *nstore = off + n;
+  on[0] = off;
+  on[1] = n;
+}
+
+__global__ void k_frame_accept(const float4* __restrict__ in, const uint32_t* on, Particles dst, TableDev S,
+                               uint32_t* bin, double inv_h, unsigned long long* err) {
+  const uint32_t off = on[0], n = on[1];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float4* o = dst.rec + size_t(off + i) * 8;
+    for (int c = 0; c < 8; ++c) o[c] = in[size_t(i) * 8 + c];
+    const double* xr = reinterpret_cast<const double*>(o);
+    int b[3];
+    float d;
+    bool ok = true;
+    for (int a = 0; a < 3; ++a) ok = ok && axis_base(xr[a], inv_h, b[a], d);
+    uint32_t key = BAD_KEY;
+    if (ok) {
+      const uint32_t r = hash_insert(S.hv, pack_key(b[0] >> 2, b[1] >> 2, b[2] >> 2));
+      if (r < S.hv.cap_blocks) {
+        key = r * 64 + uint32_t(((b[0] & 3) << 4) | ((b[1] & 3) << 2) | (b[2] & 3));
+        atomicAdd(&S.cell_count[key], 1u);
+      } else {
+        err_report(err, ERR_CAPACITY, 0);
+      }
+    }
+    bin[off + i] = key;
+  }
+}
+
+__global__ void k_frame_unpack_blocks(TableDev S, float4* acc, const FrameHeader* h, const BlockRec* __restrict__ in,
+                                      int set, unsigned long long* err) {
+  if (h->n_blocks > h->cap_blocks || h->n_parts > h->cap_parts) return;  // overflowed frame: reported, not applied
+  const uint32_t n = h->n_blocks;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    uint32_t r = 0;
+    if (lane == 0) r = hash_insert(S.hv, in[i].key);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= S.hv.cap_blocks) {
+      if (lane == 0) err_report(err, ERR_CAPACITY, 0);
+      continue;
+    }
+    for (int q = lane; q < 128; q += 32) {
+      const float4 v = in[i].v[q];
+      float4* d = &acc[size_t(r) * 128 + q];
+      if (set)
+        *d = v;
+      else
+        red_v4(d, v.x, v.y, v.z, v.w);
+    }
+  }
+}
+
+__global__ void k_frame_unpack_blocks_fx(TableDev S, unsigned long long* acc_fx, const FrameHeader* h,
+                                         const BlockRecFx* __restrict__ in, int set, unsigned long long* err) {
+  if (h->n_blocks > h->cap_blocks || h->n_parts > h->cap_parts) return;
+  const uint32_t n = h->n_blocks;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    uint32_t r = 0;
+    if (lane == 0) r = hash_insert(S.hv, in[i].key);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= S.hv.cap_blocks) {
+      if (lane == 0) err_report(err, ERR_CAPACITY, 0);
+      continue;
+    }
+    for (int q = lane; q < 512; q += 32) {
+      unsigned long long* d = &acc_fx[size_t(r) * 512 + q];
+      if (set)
+        *d = in[i].v[q];
+      else
+        atomicAdd(d, in[i].v[q]);
+    }
+  }
+}
+
+// Per-rank step statistics for the one all-gather of a distributed step
+// (slabs.DistributedSimulation): see smpm_sim_stats_vector in include/smpm.h.
+constexpr int NSTATV = 20;
+__global__ void k_stats_vector(const DevStats* stOld, const DevStats* stNew, const HashView hvNew, uint32_t cap_b,
+                               const unsigned long long* err, const uint32_t* nstore, const FrameHeader* f0,
+                               const FrameHeader* f1, const FrameHeader* f2, double* out) {
+  if (threadIdx.x) return;
+  out[0] = double(__uint_as_float(stNew->vmax2_bits));
+  out[1] = double(stOld->n_active);
+  out[2] = double(stOld->n_owned);
+  out[3] = stOld->mass_sum;
+  out[4] = stOld->mom_sum[0];
+  out[5] = stOld->mom_sum[1];
+  out[6] = stOld->mom_sum[2];
+  for (int f = 0; f < 3; ++f) out[7 + f] = double(__uint_as_float(stNew->bnd_bits[f]));
+  // replay: table overflow or fixed-point scale overflow of the launch just made
+  const bool ovf = *hvNew.overflow != 0 || *hvNew.counter > cap_b || stNew->scale_ovf != 0;
+  out[10] = ovf ? 1.0 : 0.0;
+  out[11] = *err != ERR_CLEAR ? 1.0 : 0.0;
+  out[12] = double(*nstore);
+  const FrameHeader* fs[3] = {f0, f1, f2};
+  double fovf = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    out[13 + 2 * k] = fs[k] ? double(fs[k]->n_blocks) : 0.0;
+    out[14 + 2 * k] = fs[k] ? double(fs[k]->n_parts) : 0.0;
+    if (fs[k] && (fs[k]->n_blocks > fs[k]->cap_blocks || fs[k]->n_parts > fs[k]->cap_parts)) fovf = 1.0;
+  }
+  out[19] = fovf;
+}
+
+// Migrants of one side were delivered (their frame did not overflow): their
+// storage slots become holes.  The side follows from the particle's base
+// block x (left of the slab: side 0).
+__global__ void k_mark_delivered(const Particles P, uint32_t* bin, uint32_t n, double inv_h, int bx0, int bx1,
+                                 int side) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (bin[i] != MIG_KEY) continue;
+    const double x = reinterpret_cast<const double*>(P.rec + size_t(i) * 8)[0];
+    int b;
+    float d;
+    if (!axis_base(x, inv_h, b, d)) continue;
+    const int bx = b >> 2;
+    if ((side == 0 && bx < bx0) || (side == 1 && bx >= bx1)) bin[i] = BAD_KEY;
+  }
+}
+
+// the next launch's fixed-point bounds = max over ranks (gathered stats rows)
+__global__ void k_apply_global(const double* rows, int world, DevStats* stNew, float* out_bounds) {
+  if (threadIdx.x) return;
+  for (int f = 0; f < 3; ++f) {
+    float b = 0.f;
+    for (int r = 0; r < world; ++r) b = fmaxf(b, float(rows[r * NSTATV + 7 + f]));
+    stNew->bnd_bits[f] = __float_as_uint(b);
+    out_bounds[f] = b;
+  }
+}
+
 }  // namespace smpm
 
 
@@ -1651,6 +1873,13 @@ struct smpm_sim {
   int S = 0;  // table holding the current particles' bins
   float4* acc = nullptr;
   float4* gv = nullptr;
+  float4* gforce = nullptr;  // retained grid force of the last step (smpm_sim_retain_fields)
+  bool retain = false;
+  // grid of the last completed step (Simulation.last_fields / last_map): its
+  // table and block count; invalidated when a prologue resets the tables
+  bool last_valid = false;
+  int last_tab = 0;
+  uint32_t last_nb = 0;
   unsigned long long* acc_fx = nullptr;  // deterministic mode accumulators
   DevStats* dstats = nullptr;  // [2]
   unsigned long long* derr = nullptr;
@@ -1670,7 +1899,7 @@ struct smpm_sim {
   int pending_err = 0;
   int64_t pending_particle = 0;
   int persist_blocks = 0;
-  cudaEvent_t ev[5];
+  cudaEvent_t ev[5] = {};
   smpm_step_stats last{};
   double vmax = 0;        // max |v| of the current particles (CFL bound input)
   // slab decomposition
@@ -1693,6 +1922,9 @@ struct smpm_sim {
   // work-item layout (k_g2p2g NKK): 2 particles per thread (8 slots per cell),
   // or 3 once cells hold more than 8; SMPM_ITEM_LAYOUT=narrow|wide pins it
   int nkk = 2, nkk_scan = 2;
+  // fast (non-deterministic) mode runs k_g2p2g_f32: block ranges of RCAP
+  // particles (the wide placement), fp32 arena, no fixed-point scales
+  bool f32 = false;
   // download scratch (inverse permutation, two staging chunks), kept once made
   uint32_t* dl_inv = nullptr;
   double* dl_dst[2] = {nullptr, nullptr};
@@ -1701,6 +1933,12 @@ struct smpm_sim {
   bool in_flight = false; // a step was launched and not yet synced
   uint32_t* hcount = nullptr;  // pinned: counter/overflow of the table just filled
   uint32_t* xcount = nullptr;  // device: block count of an exchange pack (per call, no allocation)
+  uint32_t* dnstore = nullptr; // device: storage slots in use (set by k_scan1, grown by frame arrivals)
+  uint32_t* don = nullptr;     // device: (offset, count) of a frame's arrivals
+  uint32_t* hnstore = nullptr; // pinned copy of dnstore, read at the step's sync
+  float* hgbound = nullptr;    // pinned: global fixed-point bounds applied by smpm_sim_apply_global
+  bool nstore_pending = false, gbound_pending = false;
+  const void* fhdr[3] = {nullptr, nullptr, nullptr};  // frames packed since the last step (stats vector)
   uint32_t* hxcount = nullptr; // pinned host copy
   std::vector<smpm_material> host_mats;
   // host <-> device transfer pipeline (pinned double buffer, host threads)
@@ -1848,6 +2086,7 @@ int alloc_grid(smpm_sim* s) {
   }
   DA(s->acc, size_t(cb) * 64 * 2);
   DA(s->gv, size_t(cb) * 64);
+  if (s->retain) DA(s->gforce, size_t(cb) * 64);
   CK(cudaMemsetAsync(s->acc, 0, size_t(cb) * 64 * 32, s->stream));
   if (s->deterministic) {
     DA(s->acc_fx, size_t(cb) * 64 * 8);
@@ -1857,6 +2096,7 @@ int alloc_grid(smpm_sim* s) {
 }
 
 size_t smem_bytes() { return sizeof(FusedSmem); }
+size_t smem_bytes_f32() { return sizeof(FusedSmemF); }
 
 FusedArgs fused_args(smpm_sim* s, int B, int dstbuf, int project) {
   FusedArgs A;
@@ -1905,6 +2145,7 @@ StepParams step_params(smpm_sim* s, double dt) {
   sp.bx0 = s->bx0;
   sp.bx1 = s->bx1;
   sp.wide = s->nkk == 3;
+  sp.cap = s->f32 ? RCAP : WIDE_CAP;
   return sp;
 }
 
@@ -1920,7 +2161,8 @@ int scan_and_bin(smpm_sim* s, int Sx, double dt) {
   StepParams sp = step_params(s, dt);
   s->nkk_scan = s->nkk;  // the items just built are laid out for this kernel variant
   int grid = std::max(1, std::min<int>(s->max_tiles, 148 * 8));
-  k_scan1<<<grid, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp);
+  k_scan1<<<grid, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp,
+                                       s->dnstore);
   k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx], sp.wide);
   k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm, sp.wide);
   CK(cudaGetLastError());
@@ -1933,6 +2175,10 @@ int scan_and_bin(smpm_sim* s, int Sx, double dt) {
 template <bool GATHER>
 void launch_g2p2g(smpm_sim* s, const FusedArgs& A, size_t smem) {
   const bool wide = s->nkk_scan == 3;
+  if (s->f32) {
+    k_g2p2g_f32<GATHER, 1><<<s->persist_blocks, CTA, smem_bytes_f32(), s->stream>>>(A);
+    return;
+  }
   if (s->acc_fx) {
     if (wide)
       k_g2p2g<GATHER, 3, 2><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
@@ -1954,12 +2200,16 @@ int launch_fused(smpm_sim* s, bool gather, int project) {
   size_t smem = smem_bytes();
   if (!gather && s->prologue_phase != 2) {
     // P2G-only pass (prologue / replay): first measure the contribution
-    // bounds the fixed-point scales derive from (nothing is written)
-    FusedArgs Mz = A;
-    Mz.measure = 1;
-    Mz.bnd_dst = s->dstats[s->S].bnd_bits;
-    launch_g2p2g<false>(s, Mz, smem);
-    CK(cudaGetLastError());
+    // bounds the fixed-point scales derive from (nothing is written); the
+    // fp32 arena has no scales (the external-bounds protocol still runs, with
+    // zero bounds)
+    if (!s->f32) {
+      FusedArgs Mz = A;
+      Mz.measure = 1;
+      Mz.bnd_dst = s->dstats[s->S].bnd_bits;
+      launch_g2p2g<false>(s, Mz, smem);
+      CK(cudaGetLastError());
+    }
     if (s->ext_bounds && s->prologue_phase == 0) {
       s->prologue_phase = 1;
       s->prologue_proj = project;
@@ -2011,6 +2261,7 @@ int grow_grid(smpm_sim* s, uint32_t need) {
   grid_ptrs.push_back(s->acc);
   grid_ptrs.push_back(s->acc_fx);
   grid_ptrs.push_back(s->gv);
+  grid_ptrs.push_back(s->gforce);
   std::vector<std::pair<void*, size_t>> keep;
   for (const auto& a : s->allocs) {
     if (std::find(grid_ptrs.begin(), grid_ptrs.end(), a.first) != grid_ptrs.end())
@@ -2024,6 +2275,22 @@ int grow_grid(smpm_sim* s, uint32_t need) {
   s->cap_b = uint32_t(nc);
   s->cap_items = uint32_t(std::min<uint64_t>(uint64_t(s->cap_p) / ISLOTS + s->cap_b + 1024, 0xFFFFFFF0ull));
   return alloc_grid(s);
+}
+
+// The fixed-point scales of a P2G launch come from the previous launch's
+// contribution bounds (x2 headroom).  When the contributions shrink a lot in
+// one step -- or grow from zero, e.g. a scene released from rest, where the
+// previous bound is 0 and the scale carries no information -- the launch's
+// maximum sits far below the scale's 2^22 and the sums lose bits.  More than
+// 4 bits lost (max * S < 2^18; a steady flow sits at 2^20..2^21) replays the
+// P2G with measured scales, like an overflow.  `bnd`: the launch's maxima (mass, momentum, force), `sinv`: the
+// inverse scales it used.
+bool scale_underflow(const uint32_t bnd[3], const float sinv[3]) {
+  for (int f = 0; f < 3; ++f) {
+    const float b = __uint_as_float_host(bnd[f]);
+    if (b > 0.f && sinv[f] > 0.f && double(b) / double(sinv[f]) < 262144.0) return true;
+  }
+  return false;
 }
 
 int decode_err(unsigned long long w, int64_t* particle) {
@@ -2064,6 +2331,7 @@ int prologue_tail(smpm_sim* s) {
 }
 
 int run_prologue(smpm_sim* s, int project) {
+  s->last_valid = false;
   for (int attempt = 0; attempt < 24; ++attempt) {
     for (int t = 0; t < 2; ++t) {
       TableDev& T = s->tab[t];
@@ -2318,11 +2586,33 @@ int smpm_release_cached_memory(void) {
 }
 int smpm_version(void) { return 1; }
 
+namespace {
+int sim_create_body(const smpm_sim_config* cfg, smpm_sim* s);
+}
+
 int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
   if (!cfg || !out) return set_err(SMPM_ERR_ARG, "null argument");
   if (!(cfg->h > 0)) return set_err(SMPM_ERR_CONFIG, "grid cell size must be positive");
   if (cfg->n_mat < 1 || cfg->n_mat > 8) return set_err(SMPM_ERR_CONFIG, "1..8 materials supported");
   smpm_sim* s = new smpm_sim();
+  const int rc = sim_create_body(cfg, s);
+  if (rc) {
+    // any failure (e.g. cudaMalloc out of memory for a large scene) releases
+    // what was allocated so far: the caller never gets a handle to destroy
+    char msg[sizeof(g_err)];
+    std::memcpy(msg, g_err, sizeof(msg));
+    smpm_sim_destroy(s);
+    std::memcpy(g_err, msg, sizeof(msg));
+    return rc;
+  }
+  *out = s;
+  return SMPM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int sim_create_body(const smpm_sim_config* cfg, smpm_sim* s) {
   s->device = cfg->device;
   if (const char* lay = std::getenv("SMPM_ITEM_LAYOUT")) {
     if (!std::strcmp(lay, "narrow")) s->allow_wide = false;
@@ -2342,6 +2632,18 @@ int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
   s->mass_floor = cfg->mass_floor;
   for (int a = 0; a < 3; ++a) s->gravity[a] = cfg->gravity[a];
   s->deterministic = cfg->deterministic;
+  // fast mode: fp32-arena kernel (SMPM_ARENA=fixed: the int32 fixed-point
+  // kernels, kept for deterministic mode, in fast mode too -- A/B only)
+  {
+    // precise grid (k_g2p2g_f32: per-cell register sums, split fixed-point
+    // arena with per-item scales) on request; SMPM_ARENA=split|fixed overrides
+    // (A/B runs)
+    const char* ar = std::getenv("SMPM_ARENA");
+    s->f32 = !s->deterministic && (cfg->precise_grid != 0);
+    if (ar && !std::strcmp(ar, "split")) s->f32 = !s->deterministic;
+    if (ar && !std::strcmp(ar, "fixed")) s->f32 = false;
+    if (s->f32) s->nkk = 3;
+  }
   s->record = cfg->record_conservation;
   s->cap_p = std::max<int64_t>(cfg->particle_capacity, 1);
   // materials
@@ -2411,6 +2713,12 @@ int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
   CK(cudaMallocHost(&s->hxcount, 4 * sizeof(uint32_t)));
   rc = dalloc(s, &s->xcount, 4);
   if (rc) return rc;
+  rc = dalloc(s, &s->dnstore, 4);
+  if (rc) return rc;
+  rc = dalloc(s, &s->don, 4);
+  if (rc) return rc;
+  CK(cudaMallocHost(&s->hnstore, 16));
+  CK(cudaMallocHost(&s->hgbound, 16));
   // x/v download scratch up front: a simulation's buffer set is then fixed at
   // creation (and reusable as a whole through the device-memory cache)
   rc = dalloc(s, &s->dl_inv, size_t(s->cap_p));
@@ -2431,13 +2739,22 @@ int smpm_sim_create(const smpm_sim_config* cfg, smpm_sim** out) {
     CK(cudaFuncSetAttribute(k_g2p2g<false, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
   }
   int occ = 0, sms = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<true, 2, 0>, CTA, smem_bytes()));
+  if (s->f32) {
+    const int sb = int(smem_bytes_f32());
+    CK(cudaFuncSetAttribute(k_g2p2g_f32<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaFuncSetAttribute(k_g2p2g_f32<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g_f32<true, 1>, CTA, smem_bytes_f32()));
+  } else {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<true, 2, 0>, CTA, smem_bytes()));
+  }
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
   s->persist_blocks = std::max(1, occ) * sms;
   for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&s->ev[i]));
-  *out = s;
   return SMPM_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int smpm_sim_destroy(smpm_sim* s) {
   if (!s) return SMPM_OK;
@@ -2448,9 +2765,12 @@ int smpm_sim_destroy(smpm_sim* s) {
   if (s->herr) cudaFreeHost(s->herr);
   if (s->hcount) cudaFreeHost(s->hcount);
   if (s->hxcount) cudaFreeHost(s->hxcount);
+  if (s->hnstore) cudaFreeHost(s->hnstore);
+  if (s->hgbound) cudaFreeHost(s->hgbound);
   for (int b = 0; b < 2; ++b)  // the pinned buffers are process-wide
     if (s->pin_ev[b]) cudaEventDestroy(s->pin_ev[b]);
-  for (int i = 0; i < 5; ++i) cudaEventDestroy(s->ev[i]);
+  for (int i = 0; i < 5; ++i)
+    if (s->ev[i]) cudaEventDestroy(s->ev[i]);
   if (s->own_stream) cudaStreamDestroy(s->stream);
   delete s;
   return SMPM_OK;
@@ -2588,7 +2908,7 @@ int smpm_sim_step(smpm_sim* s, double dt) {
   GridParams gp = grid_params(s);
   auto kg = s->acc_fx ? k_grid<true> : k_grid<false>;
   kg<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
-                                         s->gv, gp, s->record, s->bx0, s->bx1, s->acc_fx);
+                                         s->gv, gp, s->record, s->bx0, s->bx1, s->acc_fx, s->gforce);
   CK(cudaGetLastError());
   rc = dense_insert(s, 1 - Sx);
   if (rc) return rc;
@@ -2626,10 +2946,18 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
       const bool was_wide = s->nkk_scan == 3;
       const uint32_t n8 = was_wide ? st.n_items_alt : st.n_items, nw = was_wide ? st.n_items : st.n_items_alt;
       const double extra = nw ? double(n8) / double(nw) : 1.0;
-      if (s->nkk == 2 && extra > 1.03 && s->allow_wide) s->nkk = 3;
+      if (s->f32) s->nkk = 3;  // k_g2p2g_f32: block ranges always
+      else if (s->nkk == 2 && extra > 1.03 && s->allow_wide) s->nkk = 3;
       else if (s->nkk == 3 && extra < 1.01 && !s->pin_wide) s->nkk = 2;
     }
     s->n_store = st.n_binned;  // positions written by the fused kernel (holes included)
+    if (s->nstore_pending) {  // frames delivered particles after the step's fused kernel
+      s->n_store = *s->hnstore;
+      s->nstore_pending = false;
+    }
+    s->last_valid = true;
+    s->last_tab = Sx;
+    s->last_nb = std::min(st.n_blocks, s->cap_b);
     s->vmax = std::sqrt(double(__uint_as_float_host(nx.vmax2_bits)));
     r.vmax = s->vmax;
     r.mass_sum = st.mass_sum;
@@ -2651,7 +2979,8 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
       if (rc) return rc;
       s->need_prologue = true;
       s->prologue_project = false;
-    } else if (nx.scale_ovf) {
+    } else if (nx.scale_ovf || (!s->ext_bounds && scale_underflow(nx.bnd_bits, nx.scale_inv)) ||
+               (s->gbound_pending && scale_underflow(reinterpret_cast<const uint32_t*>(s->hgbound), nx.scale_inv))) {
       // a P2G contribution outgrew the fixed-point scale derived from the
       // previous step: redo this step's P2G from the records with measured bounds
       s->need_prologue = true;
@@ -2659,6 +2988,8 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
       s->n_replays += 1;
     }
     s->last = r;
+    s->gbound_pending = false;
+    s->fhdr[0] = s->fhdr[1] = s->fhdr[2] = nullptr;
   }
   if (out) *out = s->last;
   return SMPM_OK;
@@ -2712,6 +3043,74 @@ int smpm_sim_query_grid(smpm_sim* s, int32_t* blocks, float* mass, float* mom, f
         for (int d = 0; d < 3; ++d) mom[3 * o + d] = q[1 + d];
       if (force)
         for (int d = 0; d < 3; ++d) force[3 * o + d] = float(double(q[4 + d]) + double(q[0]) * s->gravity[d]);
+    }
+  }
+  return SMPM_OK;
+}
+
+int smpm_sim_retain_fields(smpm_sim* s, int on) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  s->retain = on != 0;
+  if (s->retain && !s->gforce) {
+    DA(s->gforce, size_t(s->cap_b) * 64);
+    s->last_valid = false;  // the step before this call kept no force
+  }
+  return SMPM_OK;
+}
+
+int smpm_sim_last_grid_size(smpm_sim* s, int64_t* n_blocks) {
+  if (!s || !n_blocks) return set_err(SMPM_ERR_ARG, "null argument");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  if (!s->last_valid) return set_err(SMPM_ERR_STATE, "no grid of a completed step is available");
+  *n_blocks = s->last_nb;
+  return SMPM_OK;
+}
+
+int smpm_sim_last_grid(smpm_sim* s, int32_t* blocks, float* mass, float* vel, float* force) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  CK(cudaSetDevice(s->device));
+  if (s->in_flight) {
+    int rc = smpm_sim_sync(s, nullptr);
+    if (rc) return rc;
+  }
+  if (!s->last_valid) return set_err(SMPM_ERR_STATE, "no grid of a completed step is available");
+  if (force && !s->retain) return set_err(SMPM_ERR_STATE, "grid forces are retained only after smpm_sim_retain_fields");
+  CK(cudaStreamSynchronize(s->stream));
+  const uint32_t nb = s->last_nb;
+  std::vector<uint64_t> keys(nb);
+  std::vector<float4> g(size_t(nb) * 64), f(force ? size_t(nb) * 64 : 0);
+  CK(cudaMemcpy(keys.data(), s->tab[s->last_tab].hv.active_keys, size_t(nb) * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(g.data(), s->gv, g.size() * sizeof(float4), cudaMemcpyDeviceToHost));
+  if (force) CK(cudaMemcpy(f.data(), s->gforce, f.size() * sizeof(float4), cudaMemcpyDeviceToHost));
+  for (uint32_t r = 0; r < nb; ++r) {
+    int bi, bj, bk;
+    unpack_key(keys[r], bi, bj, bk);
+    if (blocks) {
+      blocks[3 * r] = bi;
+      blocks[3 * r + 1] = bj;
+      blocks[3 * r + 2] = bk;
+    }
+  }
+  for (size_t i = 0; i < size_t(nb) * 64; ++i) {
+    if (mass) mass[i] = g[i].w;
+    if (vel) {
+      vel[3 * i] = g[i].x;
+      vel[3 * i + 1] = g[i].y;
+      vel[3 * i + 2] = g[i].z;
+    }
+    if (force) {
+      force[3 * i] = f[i].x;
+      force[3 * i + 1] = f[i].y;
+      force[3 * i + 2] = f[i].z;
     }
   }
   return SMPM_OK;
@@ -2853,6 +3252,13 @@ int smpm_sim_p2g_bounds(smpm_sim* s, int set, float* bounds) {
   if (set) {
     for (int a = 0; a < 3; ++a) std::memcpy(&b[a], &bounds[a], 4);
     CK(cudaMemcpy(s->dstats[s->S].bnd_bits, b, 12, cudaMemcpyHostToDevice));
+    // external-bounds mode: the precision check runs on the global maxima
+    // (every rank scaled alike, so every rank reaches the same decision)
+    if (s->ext_bounds && !s->need_prologue && scale_underflow(b, s->hstats[s->S].scale_inv)) {
+      s->need_prologue = true;
+      s->prologue_project = false;
+      s->n_replays += 1;
+    }
   } else {
     CK(cudaMemcpy(b, s->dstats[s->S].bnd_bits, 12, cudaMemcpyDeviceToHost));
     for (int a = 0; a < 3; ++a) bounds[a] = __uint_as_float_host(b[a]);
@@ -2862,6 +3268,101 @@ int smpm_sim_p2g_bounds(smpm_sim* s, int set, float* bounds) {
 
 int64_t smpm_sim_exchange_record_bytes(const smpm_sim* s) {
   return s && s->deterministic ? int64_t(sizeof(BlockRecFx)) : int64_t(sizeof(BlockRec));
+}
+
+int64_t smpm_sim_frame_bytes(const smpm_sim* s, int64_t cap_blocks, int64_t cap_parts) {
+  if (!s) return 0;
+  return int64_t(sizeof(FrameHeader)) + cap_parts * 128 + cap_blocks * smpm_sim_exchange_record_bytes(s);
+}
+
+int smpm_sim_frame_pack(smpm_sim* s, int mode, void* frame, int64_t cap_blocks, int64_t cap_parts) {
+  if (!s || !frame || mode < 0 || mode > 2) return set_err(SMPM_ERR_ARG, "invalid argument");
+  CK(cudaSetDevice(s->device));
+  FrameHeader* h = reinterpret_cast<FrameHeader*>(frame);
+  unsigned char* parts = reinterpret_cast<unsigned char*>(frame) + sizeof(FrameHeader);
+  unsigned char* blocks = parts + size_t(cap_parts) * 128;
+  k_frame_init<<<1, 32, 0, s->stream>>>(h, uint32_t(cap_blocks), uint32_t(cap_parts));
+  if (mode < 2 && s->mig_count) {
+    k_frame_parts<<<148 * 2, 256, 0, s->stream>>>(s->mig[mode], s->mig_count + mode, h,
+                                                  reinterpret_cast<float4*>(parts));
+  }
+  if (s->acc_fx)
+    k_pack_blocks_fx<<<148 * 8, 256, 0, s->stream>>>(s->tab[s->S], s->acc_fx, mode, s->bx0, s->bx1,
+                                                     reinterpret_cast<BlockRecFx*>(blocks), &h->n_blocks,
+                                                     uint32_t(cap_blocks));
+  else
+    k_pack_blocks<<<148 * 8, 256, 0, s->stream>>>(s->tab[s->S], s->acc, mode, s->bx0, s->bx1,
+                                                  reinterpret_cast<BlockRec*>(blocks), &h->n_blocks,
+                                                  uint32_t(cap_blocks));
+  CK(cudaGetLastError());
+  s->fhdr[mode] = frame;
+  return SMPM_OK;
+}
+
+int smpm_sim_frame_unpack(smpm_sim* s, const void* frame, int64_t cap_blocks, int64_t cap_parts, int set) {
+  if (!s || !frame) return set_err(SMPM_ERR_ARG, "invalid argument");
+  CK(cudaSetDevice(s->device));
+  const FrameHeader* h = reinterpret_cast<const FrameHeader*>(frame);
+  const unsigned char* parts = reinterpret_cast<const unsigned char*>(frame) + sizeof(FrameHeader);
+  const unsigned char* blocks = parts + size_t(cap_parts) * 128;
+  if (s->acc_fx)
+    k_frame_unpack_blocks_fx<<<148 * 4, 256, 0, s->stream>>>(s->tab[s->S], s->acc_fx, h,
+                                                             reinterpret_cast<const BlockRecFx*>(blocks), set, s->derr);
+  else
+    k_frame_unpack_blocks<<<148 * 4, 256, 0, s->stream>>>(s->tab[s->S], s->acc, h,
+                                                          reinterpret_cast<const BlockRec*>(blocks), set, s->derr);
+  if (!set && cap_parts > 0) {
+    k_frame_reserve<<<1, 32, 0, s->stream>>>(h, s->dnstore, s->don, uint32_t(s->cap_p), s->derr);
+    k_frame_accept<<<148 * 2, 256, 0, s->stream>>>(reinterpret_cast<const float4*>(parts), s->don, s->state[s->cur],
+                                                   s->tab[s->S], s->bin, s->inv_h, s->derr);
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(s->hnstore, s->dnstore, 4, cudaMemcpyDeviceToHost, s->stream));
+  s->nstore_pending = true;
+  return SMPM_OK;
+}
+
+int smpm_sim_stats_vector(smpm_sim* s, double* out) {
+  if (!s || !out) return set_err(SMPM_ERR_ARG, "null argument");
+  CK(cudaSetDevice(s->device));
+  const int Sx = 1 - s->S;  // table of the step just launched
+  k_stats_vector<<<1, 32, 0, s->stream>>>(s->dstats + Sx, s->dstats + s->S, s->tab[s->S].hv, s->cap_b, s->derr,
+                                          s->dnstore, reinterpret_cast<const FrameHeader*>(s->fhdr[0]),
+                                          reinterpret_cast<const FrameHeader*>(s->fhdr[1]),
+                                          reinterpret_cast<const FrameHeader*>(s->fhdr[2]), out);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(s->hnstore, s->dnstore, 4, cudaMemcpyDeviceToHost, s->stream));
+  s->nstore_pending = true;
+  return SMPM_OK;
+}
+
+int smpm_sim_stats_vector_len(void) { return NSTATV; }
+
+int smpm_sim_migrants_delivered(smpm_sim* s, int side_mask) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  CK(cudaSetDevice(s->device));
+  if ((side_mask & 3) == 3) {
+    s->mig_sent = true;  // every departed particle's slot is a hole
+    return SMPM_OK;
+  }
+  // the storage of the current buffer: the fused kernel's records (the
+  // departed particles lie there, before any arrivals)
+  for (int side = 0; side < 2; ++side)
+    if ((side_mask >> side) & 1)
+      k_mark_delivered<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], s->bin, s->n_store, s->inv_h, s->bx0, s->bx1,
+                                                       side);
+  CK(cudaGetLastError());
+  s->mig_sent = false;  // the rest stays live: a replayed P2G re-scatters and re-exports it
+  return SMPM_OK;
+}
+
+int smpm_sim_apply_global(smpm_sim* s, const double* rows, int world) {
+  if (!s || !rows || world < 1) return set_err(SMPM_ERR_ARG, "invalid argument");
+  CK(cudaSetDevice(s->device));
+  k_apply_global<<<1, 32, 0, s->stream>>>(rows, world, s->dstats + s->S, s->hgbound);
+  CK(cudaGetLastError());
+  s->gbound_pending = s->ext_bounds;  // precision check on the global maxima at the sync
+  return SMPM_OK;
 }
 
 int smpm_sim_set_slab(smpm_sim* s, int32_t bx0, int32_t bx1, int64_t pid_base, int64_t migrant_capacity) {

@@ -156,6 +156,68 @@ class ActiveIndexMap:
         """The C-ABI descriptor consumed by the transfer kernels."""
         return self.table.dref
 
+    @classmethod
+    def from_blocks(cls, active_blocks):
+        """Device map whose rank r is ``active_blocks[r]`` -- any rank order,
+        e.g. the reference's scan (row-major) or dense maps
+        (grid_index.py:179-198, 256-277).  Concurrent insert, then the ranks
+        are re-ordered by each key's position in the list."""
+        torch = _lib.torch_cuda()
+        blocks = np.asarray(active_blocks, dtype=np.int64).reshape(-1, 3)
+        n = blocks.shape[0]
+        if n and (blocks.min() < COORD_MIN or blocks.max() > COORD_MAX):
+            raise KeyRangeError("block coordinate outside packable range")
+        cap = 64
+        while cap < 2 * max(n, 1):
+            cap *= 2
+        t = _lib.DeviceHashTable(cap, max(n, 1))
+        if n:
+            packed = _lib.to_dev(pack_keys(blocks).view(np.int64), np.int64)
+            ranks = torch.empty(n, dtype=torch.int32, device="cuda")
+            fresh = torch.empty(n, dtype=torch.uint8, device="cuda")
+            _lib.check(_lib.load().smpm_hash_insert_many(t.dref, _lib.ptr(packed), n, _lib.ptr(ranks),
+                                                         _lib.ptr(fresh), _lib.stream_ptr()), "insert")
+            if int(fresh.sum().item()) != n:
+                raise ValueError("active_blocks lists a block twice")
+            # first_pos[slot of the key at list position i] = i: canonical
+            # order 1 (by first encounter) is then the list order
+            first = torch.full((cap,), -1, dtype=torch.int64, device="cuda")
+            slots = t.slot_of_rank[ranks.long()].long()
+            first[slots] = torch.arange(n, dtype=torch.int64, device="cuda")
+            t.canonicalize(1, first)
+        return cls(t, n)
+
+
+def as_index_map(index_map):
+    """The device map for any of the reference's map forms: this package's
+    ActiveIndexMap, an object with ``active_blocks`` in rank order (the
+    reference's ActiveIndexMap of any backend), or the reference's flat
+    ``kernel_args()`` tuple (grid_index.py:239-248)."""
+    if isinstance(index_map, ActiveIndexMap):
+        return index_map
+    if isinstance(index_map, tuple) and len(index_map) == 11:
+        mode, b0, b1, b2, s0, s1, s2, phi_flat, keys, vals, bs = index_map
+        if int(bs) != BLOCK_SIZE:
+            raise ValueError(f"the GPU grid uses {BLOCK_SIZE}x{BLOCK_SIZE}x{BLOCK_SIZE} blocks, got {int(bs)}")
+        if int(mode) == MODE_FLAT:
+            phi = np.asarray(phi_flat, dtype=np.int64)
+            live = np.nonzero(phi >= 0)[0]
+            blocks = np.stack(np.unravel_index(live, (int(s0), int(s1), int(s2))), axis=1) + np.array(
+                [int(b0), int(b1), int(b2)], dtype=np.int64)
+            order = np.argsort(phi[live], kind="stable")
+            return ActiveIndexMap.from_blocks(blocks[order])
+        k = np.asarray(keys, dtype=np.uint64)
+        v = np.asarray(vals, dtype=np.int64)
+        used = np.nonzero((k != np.uint64(EMPTY_KEY)) & (v >= 0))[0]
+        order = np.argsort(v[used], kind="stable")
+        return ActiveIndexMap.from_blocks(unpack_keys(k[used][order]))
+    blocks = getattr(index_map, "active_blocks", None)
+    if blocks is None:
+        raise TypeError(f"not an index map: {type(index_map).__name__}")
+    if int(getattr(index_map, "block_size", BLOCK_SIZE)) != BLOCK_SIZE:
+        raise ValueError(f"the GPU grid uses {BLOCK_SIZE}x{BLOCK_SIZE}x{BLOCK_SIZE} blocks")
+    return ActiveIndexMap.from_blocks(blocks)
+
 
 def node_index(index_map, node):
     return index_map.node_index(node)

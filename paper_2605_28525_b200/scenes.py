@@ -9,7 +9,8 @@ sand (phi=30 deg, E=1e6 Pa, nu=0.3, rho=1500), g=(0,0,-9.81), CFL 0.4.
 * C2 ``two_spheres``      -- elastic spheres colliding in a large box
 * C3 ``incline``          -- 4x2.5x1 m sand block on a 35 deg incline with walls
 * C4 ``landslide``        -- terrain-conforming release over an analytic DEM
-                             (about 99M particles at h=0.5, ppc=2)
+                             (101M particles at h=0.5, ppc=2: release 250 x 125 m,
+                             0.5-51 m deep)
 """
 
 import math
@@ -119,7 +120,7 @@ def landslide_terrain(cell=5.0):
     return Heightfield(x0=0.0, y0=-250.0, cell=cell, data=data)
 
 
-def landslide(h=0.5, ppc=2, release=((100.0, 350.0), (-62.5, 62.5)), depth=(0.5, 50.0), mu=0.35, x_stride=1,
+def landslide(h=0.5, ppc=2, release=((100.0, 350.0), (-62.5, 62.5)), depth=(0.5, 51.0), mu=0.35, x_stride=1,
               fraction=1.0, columns=None):
     """C4: terrain-conforming release zone over the analytic DEM.
 
@@ -174,10 +175,16 @@ def landslide_slabs(world, h=0.5, ppc=2, fraction=1.0):
     out = []
     cuts = [0]
     for r in range(1, world):
-        c = int(round(r * len(xs) / world))
-        # move the cut to a block boundary
-        while 0 < c < len(xs) and bx[c] == bx[c - 1]:
+        c = max(int(round(r * len(xs) / world)), cuts[-1] + 1)
+        # a cut sits on a block boundary, and every interior slab is at least
+        # 2 blocks wide (slabs.slab_bounds: contributions to a block then come
+        # from at most two ranks)
+        prev_block = bx[cuts[-1]] if r > 1 else None
+        while c < len(xs) and (bx[c] == bx[c - 1] or (prev_block is not None and bx[c] < prev_block + 2)):
             c += 1
+        if c >= len(xs):
+            raise ValueError(f"the landslide release ({len(xs)} lattice columns, fraction={fraction}) is too "
+                             f"small to cut into {world} slabs of at least 2 blocks")
         cuts.append(c)
     cuts.append(len(xs))
     for r in range(world):

@@ -183,7 +183,8 @@ class DistributedSimulation:
         self._cap_mig = cap_mig
         self.sim = Simulation(particles, config, materials, boundaries, record_conservation=record_conservation,
                               block_capacity=block_capacity, particle_capacity=n + 4 * cap_mig,
-                              slab=(int(bounds[0]), int(bounds[1]), int(pid_base), cap_mig))
+                              slab=(int(bounds[0]), int(bounds[1]), int(pid_base), cap_mig),
+                              host_sync="on_access")  # the local set changes size with migration
         self._h = self.sim._h
         self.lib = _lib.load()
         self.t = 0.0
@@ -326,7 +327,8 @@ class DistributedSimulation:
         red = rows[:, 1:7].sum(axis=0)
         glob = rows[:, 7:10].max(axis=0)
         _lib.check(self.lib.smpm_sim_p2g_bounds(self._h, 1, (ctypes.c_float * 3)(*glob)), "bounds")
-        self._replay = bool(rows[:, 10].max())
+        # (setting the global bounds also runs the precision check on them)
+        self._replay = bool(rows[:, 10].max()) or bool(self.lib.smpm_sim_prologue_needed(self._h))
         if not self._replay:
             self._exchange()
         self.t += st.dt

@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, InactiveNodeError, KeyRangeError, SimulationError
-from .grid_index import ActiveIndexMap
+from .grid_index import ActiveIndexMap, as_index_map
 from .materials import _degenerate_message, material_tables  # noqa: F401
 
 BACKENDS = ("dense", "scan", "hash")
@@ -214,6 +214,14 @@ class SimConfig:
     backend: str = "hash"
     n_threads: int = 1
     deterministic: bool = False
+    # GPU option (not in the reference).  True (default): P2G summed per cell in
+    # registers into a split fixed-point arena with per-item scales -- grid
+    # sums at fp32 precision relative to each node, light surface nodes
+    # included.  False: the per-particle int32 fixed-point scatter with one
+    # global scale per launch, ~20 % faster, but light nodes and stress-
+    # cancelling contacts lose precision.  Deterministic
+    # mode always uses its int64 fixed-point path.
+    precise_grid: bool = True
 
     def __post_init__(self):
         if self.h <= 0:
@@ -299,6 +307,7 @@ def _stencil_params(h, gravity=(0.0, 0.0, 0.0)):
 
 def _scatter(particles, index_map, h, gravity, fields, want_mass_mom, want_force):
     torch = _lib.torch_cuda()
+    index_map = as_index_map(index_map)
     n = particles.n
     nn = index_map.n_nodes
     if fields is None:
@@ -368,7 +377,8 @@ def grid_update(fields, index_map, h, dt, mass_floor=0.0, boundaries=()):
     mass = _lib.to_dev(fields.mass, np.float32)
     vel = _lib.to_dev(fields.vel.reshape(-1), np.float32)
     force = _lib.to_dev(fields.force.reshape(-1), np.float32)
-    blocks = _lib.to_dev(index_map.active_blocks, np.int32)
+    blocks = index_map.active_blocks if hasattr(index_map, "active_blocks") else as_index_map(index_map).active_blocks
+    blocks = _lib.to_dev(np.asarray(blocks), np.int32)
     gp, keep = _grid_params(h, dt, mass_floor, boundaries)
     _lib.check(_lib.load().smpm_grid_update(ctypes.byref(gp), nn, _lib.ptr(mass), _lib.ptr(vel), _lib.ptr(force),
                                             _lib.ptr(blocks), _lib.stream_ptr()), "grid update")
@@ -382,6 +392,7 @@ def g2p(particles, index_map, fields, h, dt):
     import ctypes
 
     torch = _lib.torch_cuda()
+    index_map = as_index_map(index_map)
     dev = {k: _lib.to_dev(getattr(particles, k), np.float64) for k in ("x", "v", "C", "F")}
     vel = _lib.to_dev(fields.vel.reshape(-1), np.float32)
     err = torch.full((1,), -1, dtype=torch.int64, device="cuda")
@@ -445,19 +456,39 @@ def _fingerprint(ps):
     return h.digest()
 
 
+MIRROR_AUTO_MAX = 1 << 16  # host_sync="auto": mirror sets up to this many particles
+FINGERPRINT_MAX = 1 << 21  # larger host views are not fingerprinted (an edit check would cost a full hash)
+
+
 class Simulation:
     """One scenario instance on the GPU (solver.py:927-1093).
 
-    The particle state lives on the device.  ``particles`` returns the
-    caller's ParticleSet refreshed from the device; if it is modified before
-    the next ``step``, the edits are uploaded (the reference mutates the same
-    arrays in place).
+    The particle state lives on the device.  The caller's ParticleSet stays
+    the simulation's host view, like the reference's in-place arrays:
+
+    * ``host_sync="mirror"``: after every step the caller's arrays are
+      refreshed from the device, and edits made to them between steps are
+      uploaded by the next step (detected by a content fingerprint) -- the
+      reference's semantics exactly;
+    * ``host_sync="on_access"``: the caller's arrays are refreshed when
+      ``particles`` is read; edits made after that read are uploaded by the
+      next step.  Read ``particles`` again after stepping before editing
+      (a per-step download of a 100M-particle set would cost more than the
+      step);
+    * ``"auto"`` (default): mirror up to 2^16 particles, on_access above.
+
+    An edit to a host view that a later step made stale raises
+    SimulationError (sets up to 2^21 particles, which are fingerprinted).
     """
 
     def __init__(self, particles, config, materials, boundaries=(), record_conservation=False,
-                 block_capacity=None, device=0, stream=None, particle_capacity=None, slab=None):
+                 block_capacity=None, device=0, stream=None, particle_capacity=None, slab=None,
+                 host_sync="auto", retain_fields=False):
         import ctypes
 
+        if host_sync not in ("auto", "mirror", "on_access"):
+            raise ConfigError(f"host_sync must be auto, mirror or on_access, got {host_sync!r}")
+        self._mirror = host_sync == "mirror" or (host_sync == "auto" and particles.n <= MIRROR_AUTO_MAX)
         self._particles = particles
         self.config = config
         self.materials = list(materials)
@@ -505,6 +536,7 @@ class Simulation:
         cfg.particle_capacity = max(particles.n, int(particle_capacity or 0))
         cfg.block_capacity = int(block_capacity or 0)
         cfg.deterministic = int(bool(config.deterministic))
+        cfg.precise_grid = int(bool(getattr(config, "precise_grid", True)))
         cfg.record_conservation = int(bool(record_conservation))
         cfg.device = int(device)
         cfg.stream = self.stream.cuda_stream
@@ -519,10 +551,16 @@ class Simulation:
             bmin = (ctypes.c_int32 * 3)(*[int(v) // bs for v in config.node_min])
             bmax = (ctypes.c_int32 * 3)(*[int(v) // bs for v in config.node_max])
             _lib.check(lib.smpm_sim_set_dense_domain(h, bmin, bmax), "dense domain")
+        self._retain = bool(retain_fields)
+        if self._retain:
+            _lib.check(lib.smpm_sim_retain_fields(h, 1), "retain fields")
         self._upload(particles)
+        if particles.n <= FINGERPRINT_MAX:  # edits to the caller's set before the first step are taken
+            self._fp = _fingerprint(particles)
         self.t = 0.0
         self.step_count = 0
         self.last_stats = None
+        self._last = None  # (step_count, last_map, last_fields), fetched on demand
         if config.dt is not None and config.dt > self.dt_bound():
             raise ConfigError(f"fixed timestep {config.dt:g} exceeds the stability bound {self.dt_bound():g}")
 
@@ -540,7 +578,8 @@ class Simulation:
         # step bins the particles and raised by that step (solver.py:1005-1006)
         _lib.check(_lib.load().smpm_sim_set_particles(self._h, ps.n, *(a.ctypes.data for a in arrs),
                                                       mid.ctypes.data), "set particles")
-        self._exported = None
+        self._fresh = True  # device state == the caller's arrays
+        self._fp = None
 
     def _download(self, ps):
         keys = ("x", "v", "C", "F", "sigma", "jac")
@@ -556,22 +595,37 @@ class Simulation:
             if out[k] is not getattr(ps, k):
                 getattr(ps, k)[...] = out[k]
 
+    def _refresh_host(self):
+        """Make the caller's arrays equal to the device state."""
+        self._download(self._particles)
+        self._fp = _fingerprint(self._particles) if self._particles.n <= FINGERPRINT_MAX else b""
+        self._fresh = True
+
     @property
     def particles(self):
         """The caller's ParticleSet, refreshed from the device."""
-        if self._exported is None:
-            self._download(self._particles)
-            self._exported = _fingerprint(self._particles) if self._particles.n <= 2_000_000 else b""
+        if not self._fresh:
+            self._refresh_host()
+        elif self._fp is None:  # handed out without a fingerprint: edits are taken on the next step
+            self._fp = b""
         return self._particles
 
     def _sync_host_edits(self):
-        if self._exported is not None:
-            if self._exported == b"" or _fingerprint(self._particles) != self._exported:
-                self._upload(self._particles)
-            self._exported_clean()
-
-    def _exported_clean(self):
-        self._exported = None
+        """Upload edits the caller made to the host view (reference: the
+        arrays are the state).  An edit to a view the device state has moved
+        past cannot be merged and raises."""
+        if not self._fp:
+            if self._fp == b"" and self._fresh:
+                self._upload(self._particles)  # no fingerprint (large set): always take the view
+            return
+        if _fingerprint(self._particles) == self._fp:
+            return
+        if not self._fresh:
+            raise SimulationError("particles were edited after a step advanced the device state past them; "
+                                  "read sim.particles after stepping before editing (or use host_sync='mirror')")
+        self._upload(self._particles)
+        self._fp = _fingerprint(self._particles)
+        self._fresh = True
 
     # -- API ------------------------------------------------------------------
     @property
@@ -610,12 +664,14 @@ class Simulation:
         self._sync_host_edits()
         cfg = self.config
         if dt is None:
-            dt = cfg.dt if cfg.dt is not None else -1.0
-        dt = float(dt)
-        if dt == 0.0 or (dt < 0 and dt != -1.0):
-            raise SimulationError(f"timestep must be positive, got {dt}")
+            dt = cfg.dt
+        if dt is not None:
+            dt = float(dt)
+            if not dt > 0.0:
+                raise SimulationError(f"timestep must be positive, got {dt}")
         lib = _lib.load()
-        rc = lib.smpm_sim_step(self._h, dt)
+        # the library takes dt <= 0 as "use the CFL bound" (solver.py:1021-1023)
+        rc = lib.smpm_sim_step(self._h, -1.0 if dt is None else dt)
         if rc:
             self._raise_status(rc, dt)
         st = _lib.StepStatsC()
@@ -632,7 +688,50 @@ class Simulation:
                           mass_sum=float(st.mass_sum) if self.record_conservation else None,
                           mom_sum=np.array(st.mom_sum[:]) if self.record_conservation else None)
         self.last_stats = stats
+        self._fresh = False
+        if self._mirror:  # the caller's arrays follow the device state (reference: in place)
+            self._refresh_host()
         return stats
+
+    def _fetch_last(self):
+        """last_map / last_fields of the last completed step (solver.py:1087-1090),
+        downloaded on first access."""
+        import ctypes
+
+        if self._last is not None and self._last[0] == self.step_count:
+            return self._last
+        lib = _lib.load()
+        nb = ctypes.c_int64(0)
+        rc = lib.smpm_sim_last_grid_size(self._h, ctypes.byref(nb))
+        if rc == _lib.ERR_STATE:  # no step yet (or the grid was rebuilt since): the reference's None
+            self._last = (self.step_count, None, None)
+            return self._last
+        _lib.check(rc, "last grid size")
+        nb = int(nb.value)
+        blocks = np.empty((max(nb, 1), 3), dtype=np.int32)
+        mass = np.empty(max(nb, 1) * 64, dtype=np.float32)
+        vel = np.empty((max(nb, 1) * 64, 3), dtype=np.float32)
+        force = np.empty((max(nb, 1) * 64, 3), dtype=np.float32) if self._retain else None
+        _lib.check(lib.smpm_sim_last_grid(self._h, blocks.ctypes.data, mass.ctypes.data, vel.ctypes.data,
+                                          force.ctypes.data if force is not None else None), "last grid")
+        amap = ActiveIndexMap.from_blocks(blocks[:nb].astype(np.int64))
+        fields = NodalFields(mass=mass[:nb * 64].astype(np.float64), vel=vel[:nb * 64].astype(np.float64),
+                             force=force[:nb * 64].astype(np.float64) if force is not None else None)
+        self._last = (self.step_count, amap, fields)
+        return self._last
+
+    @property
+    def last_map(self):
+        """ActiveIndexMap of the last step's grid (None before the first step)."""
+        return self._fetch_last()[1]
+
+    @property
+    def last_fields(self):
+        """NodalFields of the last step after the grid update: node mass, grid
+        velocity (boundary-projected) and -- with ``retain_fields=True`` -- the
+        nodal force incl. gravity (else ``force`` is None).  None before the
+        first step."""
+        return self._fetch_last()[2]
 
     def query_grid(self):
         """(active_blocks int64 (n,3), NodalFields) of the P2G computed from

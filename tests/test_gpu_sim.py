@@ -18,7 +18,7 @@ from paper_2605_28525_b200.solver import BoundaryCondition, SimConfig, Simulatio
 from tests.test_gpu_module import keyed, normwise  # noqa: E402
 from tests.test_oracle_golden import _boundaries  # noqa: E402
 
-TOL = dict(x=1e-6, v=2e-5, C=2e-4, F=2e-5, mass=1e-5, mom=1e-5, force=1e-4)
+TOL = dict(x=1e-6, v=1e-5, C=1e-4, F=2e-5, mass=1e-5, mom=1e-5, force=1e-4)
 
 
 def column_scene(h=0.05, size=(0.4, 0.3, 0.5), seed=3, vx=0.4, bcs="mixed", mat=None, prestrain=0.0, ppc=2):

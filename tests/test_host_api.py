@@ -57,6 +57,6 @@ def test_scene_sizes():
     c2 = scenes.two_spheres()
     assert 120_000 < c2.particles.n < 140_000
     small = scenes.landslide(x_stride=50)
-    assert small.particles.n == 20 * 500 * 198
+    assert small.particles.n == 20 * 500 * 202  # 0.5..51 m deep at h/2 spacing
     ps = ParticleSet.from_samples(np.zeros((2, 3)), np.ones(2), 10.0)
     assert ps.n == 2 and np.all(ps.F == np.eye(3))
