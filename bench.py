@@ -300,6 +300,32 @@ def ours(args):
     # device-memory cache (include/smpm.h), which the e2e sim of the same
     # configuration reuses, like any process that runs simulations back to back
     del sim, inner
+    # ---- the other grid mode, same workload and timing (precise_grid=False:
+    # per-particle int32 fixed-point scatter, one global scale per launch)
+    alt = None
+    if not distributed and not args.deterministic and not args.no_alt:
+        import copy
+
+        cfg_alt = copy.copy(sc.config)
+        cfg_alt.precise_grid = not bool(getattr(sc.config, "precise_grid", True))
+        sim_a = Simulation(sc.particles, cfg_alt, sc.materials, sc.boundaries)
+        for _ in range(args.warmup):
+            sim_a.step()
+        fa = []
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(sim_a.stream)
+        for _ in range(args.steps):
+            fa.append(sim_a.step().times["g2p"] * 1e3)
+        a1.record(sim_a.stream)
+        torch.cuda.synchronize()
+        ams = a0.elapsed_time(a1)
+        alt = {"precise_grid": cfg_alt.precise_grid, "ms_per_step": ams / args.steps,
+               "value": n * args.steps / (ams * 1e-3), "fused_ms": float(np.mean(fa)),
+               "roofline_frac": fused_bytes / (float(np.mean(fa)) * 1e-3) / 1e9 / peak,
+               "note": "same workload and timing with the other P2G grid mode (DESIGN.md section 4); "
+                       "precise_grid=False trades light-node / contact precision for speed"}
+        del sim_a
     # ---- e2e: public API from host buffers (upload + K steps + download x,v)
     host = sc.particles
     if not distributed:
@@ -352,6 +378,7 @@ def ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": workload_config(args.config, sc, n, args.deterministic, world),
+        "precise_grid": bool(getattr(sc.config, "precise_grid", True)),
         "parallelism": f"slab{world}" if world > 1 else "single",
         "mean_allocated_nodes": float(np.mean(nalloc)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -366,6 +393,7 @@ def ours(args):
                          "preallocated host arrays; device buffers reused from the value leg (library cache)",
                 "cold": e2e_cold},
         "late": late,
+        "alt_grid_mode": alt,
         "gpu_launches": 5 * args.steps,
         "clocks": clk.summary(),
     }
@@ -421,6 +449,7 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of the C4 release columns")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cold", action="store_true", help="skip the fresh-process e2e leg")
+    ap.add_argument("--no-alt", action="store_true", help="skip timing the other grid mode")
     ap.add_argument("--late-steps", type=int, default=600,
                     help="also time --steps steps after the simulation reached this step (0: skip)")
     ap.add_argument("--e2e-cold-child", action="store_true", help=argparse.SUPPRESS)

@@ -272,7 +272,8 @@ int smpm_sim_set_slab(smpm_sim* s, int32_t bx0, int32_t bx1, int64_t pid_base, i
  *   Frames that overflowed their capacity are reported, not applied.
  * stats_vector: this rank's step statistics into a device double[len]
  *   (vmax^2, n_active, n_owned, mass, momentum[3], P2G bounds[3], replay,
- *   error, storage, frame counts[3][2], frame overflow) for one all-gather;
+ *   error, storage, frame counts[3][2], frame overflow, inverse fixed-point
+ *   scales[3], 0) for one all-gather;
  *   apply_global: the next launch's fixed-point bounds = max over the
  *   gathered rows (plus the precision check at the sync).  Async. */
 int64_t smpm_sim_frame_bytes(const smpm_sim* s, int64_t cap_blocks, int64_t cap_parts);

@@ -181,51 +181,32 @@ __device__ inline uint32_t cta_excl_scan(uint32_t v, uint32_t* sh /*[8]*/, uint3
 // scans tile sums and finalises the step scalars.
 __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
                                                unsigned long long* err, StepParams sp, uint32_t* nstore) {
-  __shared__ uint32_t red[4][8];
   __shared__ bool last;
   const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
   const int ntiles = (nb + TB - 1) / TB;
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    uint32_t s_tot = 0, s_items = 0, s_alt = 0, s_own = 0;
-    for (int b = w; b < TB; b += 8) {
-      uint32_t r = tile * TB + b;
-      if (r >= nb) break;
-      uint32_t c0 = S.cell_count[size_t(r) * 64 + lane], c1 = S.cell_count[size_t(r) * 64 + 32 + lane];
-      uint32_t tot = warp_sum(c0 + c1), mx = warp_max(max(c0, c1));
-      const uint32_t items8 = (mx + ISLOTS - 1) / ISLOTS, itemsw = (tot + sp.cap - 1) / sp.cap;
-      const uint32_t items = sp.wide ? itemsw : items8, items_alt = sp.wide ? items8 : itemsw;
-      // neighbour ranks for the gather arena of this block's work items
-      if (lane < 8 && items) {
-        int bi, bj, bk;
-        unpack_key(S.hv.active_keys[r], bi, bj, bk);
-        S.nbr8[size_t(r) * 8 + lane] = hash_lookup(S.hv.keys, S.hv.vals, S.hv.mask,
-                                                   pack_key(bi + (lane >> 2), bj + ((lane >> 1) & 1), bk + (lane & 1)));
-      }
-      if (lane == 0) {
-        S.block_total[r] = tot;
-        S.block_items[r] = items;
-        s_tot += tot;
-        s_items += items;
-        s_alt += items_alt;
-        int bi, bj, bk;
-        unpack_key(S.hv.active_keys[r], bi, bj, bk);
-        if (bi >= sp.bx0 && bi < sp.bx1) s_own += 1;
-      }
-    }
+  const int lane = threadIdx.x & 31;
+  // one warp per block over the whole grid (the neighbour-rank lookups are
+  // latency-bound: spread them over every warp), per-tile sums by atomics
+  // into the zeroed tile_sums
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = gw; r < nb; r += nw) {
+    uint32_t c0 = S.cell_count[size_t(r) * 64 + lane], c1 = S.cell_count[size_t(r) * 64 + 32 + lane];
+    uint32_t tot = warp_sum(c0 + c1), mx = warp_max(max(c0, c1));
+    const uint32_t items8 = (mx + ISLOTS - 1) / ISLOTS, itemsw = (tot + sp.cap - 1) / sp.cap;
+    const uint32_t items = sp.wide ? itemsw : items8, items_alt = sp.wide ? items8 : itemsw;
+    int bi, bj, bk;
+    unpack_key(S.hv.active_keys[r], bi, bj, bk);
+    // neighbour ranks for the gather arena of this block's work items
+    if (lane < 8 && items)
+      S.nbr8[size_t(r) * 8 + lane] = hash_lookup(S.hv.keys, S.hv.vals, S.hv.mask,
+                                                 pack_key(bi + (lane >> 2), bj + ((lane >> 1) & 1), bk + (lane & 1)));
     if (lane == 0) {
-      red[0][w] = s_tot;
-      red[1][w] = s_items;
-      red[2][w] = s_alt;
-      red[3][w] = s_own;
+      S.block_total[r] = tot;
+      S.block_items[r] = items;
     }
-    __syncthreads();
-    if (threadIdx.x < 4) {
-      uint32_t a = 0;
-      for (int i = 0; i < 8; ++i) a += red[threadIdx.x][i];
-      S.tile_sums[4 * tile + threadIdx.x] = a;
-    }
-    __syncthreads();
+    const uint32_t own = (bi >= sp.bx0 && bi < sp.bx1) ? 1u : 0u;
+    const uint32_t v = lane == 0 ? tot : lane == 1 ? items : lane == 2 ? items_alt : own;
+    if (lane < 4 && v) atomicAdd(&S.tile_sums[4 * (r / TB) + lane], v);
   }
   __threadfence();
   __syncthreads();
@@ -1792,7 +1773,7 @@ __global__ void k_frame_unpack_blocks_fx(TableDev S, unsigned long long* acc_fx,
 
 // Per-rank step statistics for the one all-gather of a distributed step
 // (slabs.DistributedSimulation): see smpm_sim_stats_vector in include/smpm.h.
-constexpr int NSTATV = 20;
+constexpr int NSTATV = 24;
 __global__ void k_stats_vector(const DevStats* stOld, const DevStats* stNew, const HashView hvNew, uint32_t cap_b,
                                const unsigned long long* err, const uint32_t* nstore, const FrameHeader* f0,
                                const FrameHeader* f1, const FrameHeader* f2, double* out) {
@@ -1818,6 +1799,8 @@ __global__ void k_stats_vector(const DevStats* stOld, const DevStats* stNew, con
     if (fs[k] && (fs[k]->n_blocks > fs[k]->cap_blocks || fs[k]->n_parts > fs[k]->cap_parts)) fovf = 1.0;
   }
   out[19] = fovf;
+  for (int f = 0; f < 3; ++f) out[20 + f] = double(stNew->scale_inv[f]);  // the launch's inverse scales
+  out[23] = 0.0;
 }
 
 // Migrants of one side were delivered (their frame did not overflow): their
@@ -2160,8 +2143,9 @@ int dense_insert(smpm_sim* s, int t) {
 int scan_and_bin(smpm_sim* s, int Sx, double dt) {
   StepParams sp = step_params(s, dt);
   s->nkk_scan = s->nkk;  // the items just built are laid out for this kernel variant
+  CK(cudaMemsetAsync(s->tab[Sx].tile_sums, 0, 16 * size_t(s->max_tiles), s->stream));
   int grid = std::max(1, std::min<int>(s->max_tiles, 148 * 8));
-  k_scan1<<<grid, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp,
+  k_scan1<<<148 * 4, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp,
                                        s->dnstore);
   k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx], sp.wide);
   k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm, sp.wide);
@@ -2951,10 +2935,6 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
       else if (s->nkk == 3 && extra < 1.01 && !s->pin_wide) s->nkk = 2;
     }
     s->n_store = st.n_binned;  // positions written by the fused kernel (holes included)
-    if (s->nstore_pending) {  // frames delivered particles after the step's fused kernel
-      s->n_store = *s->hnstore;
-      s->nstore_pending = false;
-    }
     s->last_valid = true;
     s->last_tab = Sx;
     s->last_nb = std::min(st.n_blocks, s->cap_b);
@@ -2990,6 +2970,10 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
     s->last = r;
     s->gbound_pending = false;
     s->fhdr[0] = s->fhdr[1] = s->fhdr[2] = nullptr;
+  }
+  if (s->nstore_pending) {  // frames delivered particles after the last fused kernel (or prologue)
+    s->n_store = *s->hnstore;
+    s->nstore_pending = false;
   }
   if (out) *out = s->last;
   return SMPM_OK;

@@ -6,17 +6,23 @@ extension.  One process per GPU; the domain is cut into slabs along the
 runout axis x at block boundaries.  A rank owns the particles whose base
 block has block-x in [bx0, bx1) and the grid blocks in that range.
 
-Per step, after the fused kernel (libsmpm.so, include/smpm.h):
+Per step, after the fused kernel (libsmpm.so, include/smpm.h), all on the
+simulation's stream with one host sync per step:
   1. partial node sums of blocks outside the slab go to their owner, which
-     adds them (insert-if-absent);
+     adds them (insert-if-absent), in the same frame as the particles whose
+     new base block left the slab (128-byte records, binned by the receiver;
+     their P2G was already done);
   2. the owner sends the full sums of its first block layer (bx == bx0) back
      to the left neighbour, whose particles' stencils reach it -- both sides
      of an interface then hold identical bits;
-  3. particles whose new base block left the slab travel as 128-byte records
-     and are binned by the receiver (their P2G was already done).
-n_active / n_blocks are sums over owned blocks; the CFL bound uses the global
-max |v|.  Transport is torch.distributed point-to-point (NCCL over NVLink on
-a GPU box; gloo with host staging in the CPU tests).
+  3. one all-gather of the step statistics (n_active, n_blocks, conservation
+     sums, max |v| for the next CFL bound, P2G bounds, replay / overflow
+     flags, frame counts), then the stream sync.
+Frames have a fixed capacity with the counts in a device header, so they are
+sent whole (no size round trip); capacities grow from the gathered counts.
+When the particle counts drift apart by more than 10 % the slab faces move
+(rebalancing).  Transport is torch.distributed point-to-point (NCCL over
+NVLink on a GPU box; gloo with host staging in the CPU tests).
 """
 
 import ctypes
@@ -145,6 +151,62 @@ class _Transport:
             torch.cuda.synchronize()  # the library consumes these on its own stream
         return out_l, out_r
 
+    def exchange_frames(self, send_l, send_r, recv_l, recv_r):
+        """Whole fixed-size frames with both neighbours, one grouped batch, no
+        size round trip.  NCCL: posted on the current (simulation) stream, which
+        then waits for them -- no host sync.  gloo (CPU tests): host-staged."""
+        dist = self.dist
+        left = self.rank - 1 if self.rank > 0 else None
+        right = self.rank + 1 if self.rank + 1 < self.world else None
+        pairs = []  # (peer, send, recv)
+        if left is not None:
+            pairs.append((left, send_l, recv_l))
+        if right is not None:
+            pairs.append((right, send_r, recv_r))
+        if not pairs:
+            return
+        if self.nccl:
+            ops = []
+            for peer, snd, rcv in pairs:
+                if snd is not None:
+                    ops.append(dist.P2POp(dist.isend, snd, peer, self.group))
+                if rcv is not None:
+                    ops.append(dist.P2POp(dist.irecv, rcv, peer, self.group))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+            return
+        import torch
+
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()
+        ops, back = [], []
+        for peer, snd, rcv in pairs:
+            if snd is not None:
+                ops.append(dist.P2POp(dist.isend, snd.cpu(), peer, self.group))
+            if rcv is not None:
+                tmp = torch.empty(rcv.numel(), dtype=rcv.dtype)
+                ops.append(dist.P2POp(dist.irecv, tmp, peer, self.group))
+                back.append((rcv, tmp))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for rcv, tmp in back:
+            rcv.copy_(tmp, non_blocking=False)
+
+    def all_gather_dev(self, vec, out):
+        """Every rank's device vector into out (world * len), one collective on
+        the current stream (NCCL) or host-staged (gloo)."""
+        dist = self.dist
+        if self.nccl:
+            dist.all_gather_into_tensor(out, vec, group=self.group)
+            return
+        import torch
+
+        parts = [torch.empty(vec.numel(), dtype=vec.dtype) for _ in range(self.world)]
+        dist.all_gather(parts, vec.cpu(), group=self.group)
+        out.copy_(torch.cat(parts))
+
     def gather(self, arr):
         """Every rank's float64 vector, stacked (one collective)."""
         import torch
@@ -172,7 +234,8 @@ class DistributedSimulation:
     its first particle."""
 
     def __init__(self, particles, config, materials, boundaries, bounds, pid_base, group=None,
-                 migrant_capacity=None, block_capacity=None, record_conservation=False):
+                 migrant_capacity=None, block_capacity=None, record_conservation=False, frame_blocks=None,
+                 frame_particles=None, rebalance=True, rebalance_threshold=0.10):
         torch = _lib.torch_cuda()
         self.config = config
         self.tr = _Transport(group)
@@ -191,10 +254,25 @@ class DistributedSimulation:
         self.step_count = 0
         self.migrated = 0  # particles received from neighbours so far
         self._torch = torch
+        self.pid_base = int(pid_base)
         self._gvmax = None  # global max |v| after the last step (next dt bound)
-        self._xcap = [4096, 4096, 4096]  # halo exchange buffers (blocks) per pack mode
-        self._xbuf = [None, None, None]
-        self._rec = int(self.lib.smpm_sim_exchange_record_bytes(self._h))
+        # exchange frames: capacities shared by all ranks, grown from the
+        # all-gathered counts (half-full -> double)
+        self._cap_blocks = int(frame_blocks or 1024)
+        self._cap_parts = int(frame_particles or 4096)
+        self.frame_growths = 0
+        self._L = int(self.lib.smpm_sim_stats_vector_len())
+        dev = self.sim.stream.device
+        self._vec = torch.zeros(self._L, dtype=torch.float64, device=dev)
+        self._rows = torch.zeros(self.tr.world * self._L, dtype=torch.float64, device=dev)
+        self._rows_host = torch.zeros(self.tr.world * self._L, dtype=torch.float64).pin_memory()
+        # deterministic mode keeps the faces fixed: a rebalance reruns the P2G
+        # (coordinated prologue) with freshly measured fixed-point scales, which
+        # the 1-GPU run does not, so bitwise equality to 1 GPU would be lost
+        self.rebalance = bool(rebalance) and not config.deterministic
+        self.rebalance_threshold = float(rebalance_threshold)
+        self.rebalances = 0
+        self.local_counts = None
         # Prologues (step 0, and replays after a rank's P2G outgrew its
         # fixed-point scales or grid capacity) run on all ranks together and
         # before the halo exchange; the fixed-point bounds are the max over
@@ -229,113 +307,202 @@ class DistributedSimulation:
         _lib.check(self.lib.smpm_sim_p2g_bounds(self._h, 1, (ctypes.c_float * 3)(*glob)), "bounds")
 
     # -- exchange -------------------------------------------------------------
-    def _pack(self, mode):
-        """Halo block records of one kind into a persistent buffer (grown on
-        demand; the C call reports the count, and overflow as CAPACITY)."""
+    def _frames(self):
+        """Fixed-capacity device frames (include/smpm.h smpm_sim_frame_*): sends
+        of mode 0 (to the left), 1 (to the right) and 2 (owner's layer to the
+        left), and the matching receives.  Every rank holds the same capacities
+        (grown from the all-gathered counts), so a frame is sent whole."""
         torch = self._torch
-        while True:
-            cap, buf = self._xcap[mode], self._xbuf[mode]
-            if buf is None:
-                buf = self._xbuf[mode] = torch.empty(cap * self._rec, dtype=torch.uint8, device="cuda")
-            n = ctypes.c_int64(0)
-            rc = self.lib.smpm_sim_exchange_pack(self._h, mode, _lib.ptr(buf), cap, ctypes.byref(n))
-            if rc == _lib.ERR_CAPACITY and n.value > cap:
-                self._xcap[mode], self._xbuf[mode] = 2 * int(n.value), None
-                continue
-            _lib.check(rc, "pack")
-            return buf[: n.value * self._rec] if n.value else None
+        key = (self._cap_blocks, self._cap_parts)
+        if getattr(self, "_fkey", None) != key:
+            fb = int(self.lib.smpm_sim_frame_bytes(self._h, self._cap_blocks, self._cap_parts))
+            fb2 = int(self.lib.smpm_sim_frame_bytes(self._h, self._cap_blocks, 0))
+            dev = self.sim.stream.device
+            self._f = {k: torch.empty(fb if k[1] != "2" else fb2, dtype=torch.uint8, device=dev)
+                       for k in ("s0", "s1", "s2", "r0", "r1", "r2")}
+            self._fkey = key
+        return self._f
 
-    def _unpack(self, buf, set_):
-        if buf is None or buf.numel() == 0:
-            return
-        _lib.check(self.lib.smpm_sim_exchange_unpack(self._h, _lib.ptr(buf), buf.numel() // self._rec,
-                                                     int(set_)), "unpack")
+    def _exchange_async(self):
+        """Two neighbour rounds on the simulation's stream, no host sync:
+        (1) halo partial sums + departing particles, (2) the owners' first
+        block layer back to the left neighbour (which needs (1) applied)."""
+        f = self._frames()
+        cb, cp = self._cap_blocks, self._cap_parts
+        lib, h = self.lib, self._h
+        has_l, has_r = self.tr.rank > 0, self.tr.rank + 1 < self.tr.world
+        if has_l:
+            _lib.check(lib.smpm_sim_frame_pack(h, 0, _lib.ptr(f["s0"]), cb, cp), "frame pack")
+        if has_r:
+            _lib.check(lib.smpm_sim_frame_pack(h, 1, _lib.ptr(f["s1"]), cb, cp), "frame pack")
+        self.tr.exchange_frames(f["s0"] if has_l else None, f["s1"] if has_r else None,
+                                f["r0"] if has_l else None, f["r1"] if has_r else None)
+        if has_l:  # the left neighbour's mode-1 frame
+            _lib.check(lib.smpm_sim_frame_unpack(h, _lib.ptr(f["r0"]), cb, cp, 0), "frame unpack")
+        if has_r:  # the right neighbour's mode-0 frame
+            _lib.check(lib.smpm_sim_frame_unpack(h, _lib.ptr(f["r1"]), cb, cp, 0), "frame unpack")
+        if has_l:
+            _lib.check(lib.smpm_sim_frame_pack(h, 2, _lib.ptr(f["s2"]), cb, 0), "frame pack")
+        self.tr.exchange_frames(f["s2"] if has_l else None, None, None, f["r2"] if has_r else None)
+        if has_r:
+            _lib.check(lib.smpm_sim_frame_unpack(h, _lib.ptr(f["r2"]), cb, 0, 1), "frame unpack")
 
-    def _migrants(self, side):
-        torch = self._torch
-        n = ctypes.c_int64(0)
-        _lib.check(self.lib.smpm_sim_migrants(self._h, side, None, 0, ctypes.byref(n)), "migrants")
-        if n.value == 0:
-            return None
-        out = torch.empty(n.value * PARTICLE_REC_BYTES, dtype=torch.uint8, device="cuda")
-        _lib.check(self.lib.smpm_sim_migrants(self._h, side, _lib.ptr(out), n.value, ctypes.byref(n)), "migrants")
-        return out
+    def _stats_async(self):
+        """This rank's step statistics, all-gathered on the device, the next
+        launch's bounds applied, and a pinned copy of the rows for the host."""
+        _lib.check(self.lib.smpm_sim_stats_vector(self._h, _lib.ptr(self._vec)), "stats vector")
+        self.tr.all_gather_dev(self._vec, self._rows)
+        _lib.check(self.lib.smpm_sim_apply_global(self._h, _lib.ptr(self._rows), self.tr.world), "apply global")
+        self._rows_host.copy_(self._rows.view(-1), non_blocking=True)
 
-    def _frame(self, blocks, parts):
-        """One message: a 16-byte header (int64 byte count of the block
-        records, pad) keeping the records 16-byte aligned, the block records
-        (exchange_record_bytes each), then particle records."""
-        torch = self._torch
-        if blocks is None and parts is None:
-            return None
-        nbytes = 0 if blocks is None else blocks.numel()
-        head = torch.tensor([nbytes, 0], dtype=torch.int64, device="cuda").view(torch.uint8)
-        return torch.cat([head] + [b for b in (blocks, parts) if b is not None])
+    def _settle(self, rows):
+        """After the sync: mark delivered migrants, frame growth, replays."""
+        L = self._L
+        rk = self.tr.rank
+        cb, cp = self._cap_blocks, self._cap_parts
+        # my frames to the left (13, 14) and right (15, 16) arrived unless overflowed
+        mask = 0
+        if rows[rk, 13] <= cb and rows[rk, 14] <= cp:
+            mask |= 1
+        if rows[rk, 15] <= cb and rows[rk, 16] <= cp:
+            mask |= 2
+        _lib.check(self.lib.smpm_sim_migrants_delivered(self._h, mask), "delivered")
+        need_b = float(rows[:, [13, 15, 17]].max())
+        need_p = float(rows[:, [14, 16]].max())
+        overflow = bool(rows[:, 19].max() > 0)
+        # proactive growth at half use: identical on every rank (gathered counts)
+        if need_b > cb / 2 or need_p > cp / 2:
+            self._cap_blocks = max(cb, 1 << int(np.ceil(np.log2(max(2.0 * need_b, 1.0)))))
+            self._cap_parts = max(cp, 1 << int(np.ceil(np.log2(max(2.0 * need_p, 1.0)))))
+            self.frame_growths += 1
+        # the precision check of the next launch's global bounds against this
+        # launch's scales (the library makes the same decision at the sync)
+        gb, sinv = rows[:, 7:10].max(axis=0), rows[0, 20:23]
+        with np.errstate(divide="ignore", invalid="ignore"):  # sinv = 0: fp32 arena, no scales
+            underflow = bool(np.any((gb > 0) & (sinv > 0) & (gb.astype(np.float32) / sinv < 262144.0)))
+        # every input is gathered, so every rank reaches the same decision
+        replay = overflow or bool(rows[:, 10].max() > 0) or underflow
+        return replay, overflow
 
-    def _unframe(self, msg):
-        if msg is None or msg.numel() == 0:
-            return None, None
-        nbytes = int(msg[:8].view(self._torch.int64).item())
-        blocks = msg[16:16 + nbytes].to("cuda")
-        parts = msg[16 + nbytes:].to("cuda")
-        return (blocks if nbytes else None), (parts if parts.numel() else None)
+    def _sync_step(self):
+        """The one host sync of a distributed step."""
+        st = _lib.StepStatsC()
+        _lib.check(self.lib.smpm_sim_sync(self._h, ctypes.byref(st)), "sync")
+        rows = self._rows_host.numpy().reshape(self.tr.world, self._L).copy()
+        return st, rows
 
     def _exchange(self):
-        """Two neighbour rounds per step: (1) partial sums of halo blocks and
-        departing particles, (2) the owners' boundary-layer sums back to the
-        left neighbour (which needs (1) applied first)."""
-        self._torch.cuda.synchronize()
-        self.sim.stream.synchronize()
-        to_l = self._frame(self._pack(0), self._migrants(0))
-        to_r = self._frame(self._pack(1), self._migrants(1))
-        for msg in self.tr.exchange(to_l, to_r):
-            blocks, parts = self._unframe(msg)
-            self._unpack(blocks, False)
-            if parts is not None:
-                self.migrated += parts.numel() // PARTICLE_REC_BYTES
-                _lib.check(self.lib.smpm_sim_accept(self._h, _lib.ptr(parts), parts.numel() // PARTICLE_REC_BYTES),
-                           "accept")
-        self.sim.stream.synchronize()
-        _, from_r = self.tr.exchange(self._pack(2), None)
-        self._unpack(from_r, True)
-        self.sim.stream.synchronize()
+        """Synchronous exchange after a coordinated prologue (construction,
+        replays, rebalancing); a frame overflow grows the frames and redoes
+        the prologue."""
+        import torch
+
+        for _ in range(8):
+            with torch.cuda.stream(self.sim.stream):
+                self._exchange_async()
+                self._stats_async()
+            _, rows = self._sync_step()
+            replay, overflow = self._settle(rows)
+            self._gvmax = float(np.sqrt(rows[:, 0].max()))
+            if not overflow:
+                return
+            self._coordinated_prologue()
+        raise RuntimeError("exchange frames did not converge")
 
     # -- API ------------------------------------------------------------------
     def dt_bound(self):
-        if self._gvmax is None:
-            self._gvmax = float(self.tr.allreduce([float(self.lib.smpm_sim_vmax(self._h))], "max")[0])
         return self.config.cfl * self.config.h / (self.sim._wave_speed + self._gvmax)
 
     def step(self, dt=None):
+        """One step on every rank: fused kernels, the device-resident frame
+        exchange and one all-gather of the step statistics, with a single
+        host sync (the stream synchronisation before the next launch)."""
+        import torch
+
         cfg = self.config
-        if dt is None:
-            dt = cfg.dt if cfg.dt is not None else self.dt_bound()
-        if self._replay:  # a rank's P2G outgrew its scales / capacity: all ranks redo it
+        if self._replay:  # a rank's P2G outgrew its scales / capacity / frames: all ranks redo it
             self._coordinated_prologue()
             self._exchange()
             self._replay = False
-        st = self.sim.step(float(dt))
-        # one collective for the step's global stats, the next dt bound and,
-        # in deterministic mode, the next launch's bounds and replay flags
-        b = (ctypes.c_float * 3)()
-        _lib.check(self.lib.smpm_sim_p2g_bounds(self._h, 0, b), "bounds")
-        extra = [*b, float(self.lib.smpm_sim_prologue_needed(self._h))]
-        rows = self.tr.gather([float(self.lib.smpm_sim_vmax(self._h)), st.n_active, st.n_allocated,
-                               st.mass_sum or 0.0, *(st.mom_sum if st.mom_sum is not None else (0.0, 0.0, 0.0)),
-                               *extra])
-        self._gvmax = float(rows[:, 0].max())
-        red = rows[:, 1:7].sum(axis=0)
-        glob = rows[:, 7:10].max(axis=0)
-        _lib.check(self.lib.smpm_sim_p2g_bounds(self._h, 1, (ctypes.c_float * 3)(*glob)), "bounds")
-        # (setting the global bounds also runs the precision check on them)
-        self._replay = bool(rows[:, 10].max()) or bool(self.lib.smpm_sim_prologue_needed(self._h))
-        if not self._replay:
-            self._exchange()
+        if dt is None:
+            dt = cfg.dt if cfg.dt is not None else self.dt_bound()
+        rc = self.lib.smpm_sim_step(self._h, float(dt))
+        if rc:
+            self.sim._raise_status(rc, dt)
+        with torch.cuda.stream(self.sim.stream):
+            self._exchange_async()
+            self._stats_async()
+        st, rows = self._sync_step()
+        replay, _ = self._settle(rows)
+        self._replay = replay
+        self._gvmax = float(np.sqrt(rows[:, 0].max()))
+        live = rows[:, 12] - rows[:, 14] - rows[:, 16]
+        self.local_counts = live
+        self.migrated += int(rows[self.tr.rank, 14] + rows[self.tr.rank, 16])
+        if self.rebalance and not replay and self.tr.world > 1:
+            self._maybe_rebalance(live)
         self.t += st.dt
         self.step_count += 1
-        return StepStats(step=self.step_count, t=self.t, dt=st.dt, n_active=int(red[0]), n_allocated=int(red[1]),
-                         times=dict(st.times), mass_sum=float(red[2]) if st.mass_sum is not None else None,
-                         mom_sum=red[3:6] if st.mom_sum is not None else None)
+        rec = self.sim.record_conservation
+        times = {p: 0.0 for p in PHASES}
+        times["map_build"] = st.ms_map * 1e-3
+        times["grid_update"] = st.ms_grid * 1e-3
+        times["g2p"] = st.ms_fused * 1e-3
+        return StepStats(step=self.step_count, t=self.t, dt=st.dt, n_active=int(rows[:, 1].sum()),
+                         n_allocated=int(rows[:, 2].sum()) * 64, times=times,
+                         mass_sum=float(rows[:, 3].sum()) if rec else None,
+                         mom_sum=rows[:, 4:7].sum(axis=0) if rec else None)
+
+    # -- rebalancing ----------------------------------------------------------
+    def _maybe_rebalance(self, live):
+        """Shift the slab faces when the particle counts drift apart by more
+        than `rebalance_threshold`: new block-aligned
+        cuts from the global block-x histogram, each face moving at most into
+        its neighbours' interiors, so particles only migrate to adjacent ranks.
+        The next step starts with a coordinated prologue under the new bounds:
+        its P2G pass exports the particles now outside each slab and sends the
+        halo sums of blocks that changed owner."""
+        mean = float(live.mean())
+        if mean <= 0 or float(live.max()) <= (1.0 + self.rebalance_threshold) * mean:
+            return
+        import torch.distributed as dist
+
+        _, x, _ = self.local_particles()
+        bx = base_block_x(x, self.config.h)
+        lo = int(bx.min()) if bx.size else 0
+        hist = np.bincount(bx - lo, minlength=1) if bx.size else np.zeros(0, np.int64)
+        objs = [None] * self.tr.world
+        dist.all_gather_object(objs, (lo, hist, tuple(self.bounds)), group=self.tr.group)
+        g_lo = min(o[0] for o in objs if o[1].size)
+        g_hi = max(o[0] + o[1].size for o in objs if o[1].size)
+        total = np.zeros(g_hi - g_lo, dtype=np.int64)
+        for o_lo, o_hist, _ in objs:
+            if o_hist.size:
+                total[o_lo - g_lo:o_lo - g_lo + o_hist.size] += o_hist
+        cum = np.cumsum(total)
+        old = [o[2] for o in objs]
+        world = self.tr.world
+        cuts = []
+        for r in range(1, world):
+            target = r * cum[-1] / world
+            # face f: blocks < f go left; choose the f whose left count is nearest the target
+            lo_lim = old[r - 1][0] + 2 if r > 1 else g_lo + 1
+            hi_lim = old[r][1] - 2 if r + 1 < world else g_hi - 1
+            lo_lim = max(lo_lim, cuts[-1] + 2 if cuts else lo_lim)
+            faces = np.arange(lo_lim, hi_lim + 1)
+            if faces.size == 0:
+                cuts.append(int(old[r][0]))
+                continue
+            left = cum[np.clip(faces - g_lo - 1, 0, cum.size - 1)] * (faces > g_lo)
+            cuts.append(int(faces[np.argmin(np.abs(left - target))]))
+        new = [(INT32_MIN if r == 0 else cuts[r - 1], INT32_MAX if r == world - 1 else cuts[r]) for r in range(world)]
+        if new == [tuple(b) for b in old]:
+            return
+        self.bounds = new[self.tr.rank]
+        _lib.check(self.lib.smpm_sim_set_slab(self._h, int(self.bounds[0]), int(self.bounds[1]), int(self.pid_base), 0),
+                   "set slab")
+        self.rebalances += 1
+        self._replay = True
 
     def local_particles(self):
         """(pid, x, v) of the particles this rank owns."""

@@ -477,8 +477,8 @@ class Simulation:
       step);
     * ``"auto"`` (default): mirror up to 2^16 particles, on_access above.
 
-    An edit to a host view that a later step made stale raises
-    SimulationError (sets up to 2^21 particles, which are fingerprinted).
+    In on_access mode an edit to a view that a later step made stale is not
+    seen (read ``particles`` again after stepping, or use "mirror").
     """
 
     def __init__(self, particles, config, materials, boundaries=(), record_conservation=False,
@@ -606,26 +606,23 @@ class Simulation:
         """The caller's ParticleSet, refreshed from the device."""
         if not self._fresh:
             self._refresh_host()
-        elif self._fp is None:  # handed out without a fingerprint: edits are taken on the next step
-            self._fp = b""
+        elif self._fp is None:  # handed out again: edits before the next step are taken
+            self._fp = _fingerprint(self._particles) if self._particles.n <= FINGERPRINT_MAX else b""
         return self._particles
 
     def _sync_host_edits(self):
         """Upload edits the caller made to the host view (reference: the
-        arrays are the state).  An edit to a view the device state has moved
-        past cannot be merged and raises."""
-        if not self._fp:
-            if self._fp == b"" and self._fresh:
-                self._upload(self._particles)  # no fingerprint (large set): always take the view
+        arrays are the state).  Only a view that still equals the device state
+        (handed out since the last step, or the constructor's set before the
+        first step) is checked -- one fingerprint, not one per step."""
+        if not self._fresh or self._fp is None:
             return
-        if _fingerprint(self._particles) == self._fp:
+        if self._fp == b"":  # no fingerprint (large set): take the view
+            self._upload(self._particles)
             return
-        if not self._fresh:
-            raise SimulationError("particles were edited after a step advanced the device state past them; "
-                                  "read sim.particles after stepping before editing (or use host_sync='mirror')")
-        self._upload(self._particles)
-        self._fp = _fingerprint(self._particles)
-        self._fresh = True
+        if _fingerprint(self._particles) != self._fp:
+            self._upload(self._particles)
+        self._fp = None  # checked: the next check needs a new view
 
     # -- API ------------------------------------------------------------------
     @property
@@ -689,6 +686,7 @@ class Simulation:
                           mom_sum=np.array(st.mom_sum[:]) if self.record_conservation else None)
         self.last_stats = stats
         self._fresh = False
+        self._fp = None
         if self._mirror:  # the caller's arrays follow the device state (reference: in place)
             self._refresh_host()
         return stats

@@ -81,3 +81,59 @@ def test_neighbour_exchange_gloo():
     assert res[1][0] == [20] * 5 and res[1][1] == [12] * 5
     assert res[2][0] == [21] * 6 and res[2][1] is None
     assert all(v[2] == 6.0 and v[3] == 3.0 for v in res.values())
+
+
+def _frame_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    tr = slabs._Transport(device="cpu")
+    size = 64  # fixed frame size: no size round trip
+    s_l = torch.full((size,), 100 + rank, dtype=torch.uint8) if rank > 0 else None
+    s_r = torch.full((size,), 200 + rank, dtype=torch.uint8) if rank + 1 < world else None
+    r_l = torch.zeros(size, dtype=torch.uint8) if rank > 0 else None
+    r_r = torch.zeros(size, dtype=torch.uint8) if rank + 1 < world else None
+    tr.exchange_frames(s_l, s_r, r_l, r_r)
+    # round 2: only leftward frames (the owners' layer sums)
+    s2 = torch.full((size,), 50 + rank, dtype=torch.uint8) if rank > 0 else None
+    r2 = torch.zeros(size, dtype=torch.uint8) if rank + 1 < world else None
+    tr.exchange_frames(s2, None, None, r2)
+    vec = torch.tensor([rank, 10.0 * rank], dtype=torch.float64)
+    out = torch.zeros(2 * world, dtype=torch.float64)
+    tr.all_gather_dev(vec, out)
+    q.put((rank, None if r_l is None else int(r_l[0]), None if r_r is None else int(r_r[0]),
+           None if r2 is None else int(r2[0]), out.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_fixed_size_frame_exchange_gloo():
+    """The distributed step's transport: whole fixed-size frames with both
+    neighbours in one batch (no size round trip), a leftward second round,
+    and the device all-gather of the stats vector (gloo, world 3)."""
+    import torch.multiprocessing as mp
+
+    world = 3
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_frame_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, gl, gr, g2, out = q.get()
+        res[r] = (gl, gr, g2, out)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert res[0][0] is None and res[0][1] == 101 and res[0][2] == 51
+    assert res[1][0] == 200 and res[1][1] == 102 and res[1][2] == 52
+    assert res[2][0] == 201 and res[2][1] is None and res[2][2] is None
+    for r in range(world):
+        assert res[r][3] == [0.0, 0.0, 1.0, 10.0, 2.0, 20.0]

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 for arena in f32 fixed; do
   if [ $arena = fixed ]; then export SMPM_ARENA=fixed; else unset SMPM_ARENA; fi
-  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-cold --late-steps ${LATE:-0} > gpurun_out/ab_$arena.log 2>&1
+  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-cold --no-alt --late-steps ${LATE:-0} > gpurun_out/ab_$arena.log 2>&1
   python - gpurun_out/ab_$arena.log $arena <<'PY'
 import json, sys
 l = [x for x in open(sys.argv[1]) if x.startswith("{")]
@@ -16,7 +16,7 @@ PY
 done
 unset SMPM_ARENA
 if [ "${NCU:-1}" = 1 ]; then
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:g2p2g -s 5 -c 1 -o gpurun_out/f32_full python bench.py --steps 2 --warmup 4 --no-cpu --no-cold --late-steps 0 > gpurun_out/ncu_f32.log 2>&1; echo ncu=$?
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:g2p2g -s 5 -c 1 -o gpurun_out/f32_full python bench.py --steps 2 --warmup 4 --no-cpu --no-cold --no-alt --late-steps 0 > gpurun_out/ncu_f32.log 2>&1; echo ncu=$?
 fi
 if [ "${TESTS:-0}" = 1 ]; then
 timeout 900 python -m pytest -q -x -m gpu tests/test_gpu_sim.py tests/test_gpu_configs.py > gpurun_out/pytest_ab.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_ab.log
