@@ -209,6 +209,11 @@ int smpm_sim_grid_size(smpm_sim* s, int64_t* n_blocks);
  * which makes every later step keep them) the nodal force incl. gravity.
  * SMPM_ERR_STATE when no step completed since the last (re)binning. */
 int smpm_sim_retain_fields(smpm_sim* s, int on);
+/* Frame output without stalling the stream (scenarios.py:483-513 frames):
+ * x then v (fp64, pid order, 6 n doubles) into a device buffer, enqueued on
+ * the simulation's stream after the last step; no host sync.  The caller
+ * copies it out on a side stream (paper_2605_28525_b200/frames.py). */
+int smpm_sim_snapshot_xv(smpm_sim* s, double* out /*device*/);
 int smpm_sim_last_grid_size(smpm_sim* s, int64_t* n_blocks);
 int smpm_sim_last_grid(smpm_sim* s, int32_t* blocks, float* mass, float* vel, float* force);
 int64_t smpm_sim_num_particles(const smpm_sim* s);

@@ -109,6 +109,7 @@ _SIGS = {
     "smpm_sim_launch_count": (ctypes.c_int, [P, P]),
     "smpm_sim_grid_size": (ctypes.c_int, [P, P]),
     "smpm_sim_retain_fields": (ctypes.c_int, [P, ctypes.c_int]),
+    "smpm_sim_snapshot_xv": (ctypes.c_int, [P, P]),
     "smpm_sim_last_grid_size": (ctypes.c_int, [P, P]),
     "smpm_sim_last_grid": (ctypes.c_int, [P, P, P, P, P]),
     "smpm_sim_set_slab": (ctypes.c_int, [P, I32, I32, I64, I64]),

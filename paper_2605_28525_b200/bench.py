@@ -22,6 +22,7 @@ import numpy as np
 
 from .errors import ConfigError, SimulationError
 from .materials import MaterialModel
+from .frames import AsyncFrameWriter
 from .scenarios import MaterialRegion, ScenarioConfig, build_simulation, load_config, write_metrics, write_particles
 from .solver import NODE_BYTES, PHASES, BoundaryCondition, Heightfield, SimConfig
 
@@ -134,7 +135,7 @@ class RunMetrics:
 
 
 def run(scenario, backend=None, threads=None, deterministic=None, out_dir=None, max_steps=None,
-        record_conservation=False, warm=True):
+        record_conservation=False, warm=True, async_frames=True):
     """Execute a scenario (ScenarioConfig or YAML path) and collect RunMetrics
     (S/bench.py:193-247).  ``out_dir`` enables frame CSVs at the configured
     cadence plus metrics.csv; ``max_steps`` truncates the run."""
@@ -154,14 +155,22 @@ def run(scenario, backend=None, threads=None, deterministic=None, out_dir=None, 
     fps, total = scenario.fps, cfg.total_time
     frame = 0
 
+    framed = out is not None and fps > 0
+    # frames leave through a device snapshot + side-stream copy + writer
+    # thread (frames.py), so stepping does not wait for the CSV text
+    writer = AsyncFrameWriter(sim) if framed and async_frames else None
+
     def emit():
         nonlocal frame
         t0 = time.perf_counter()
-        write_particles(out / f"frame_{frame:06d}.csv", sim.particles)
+        path = out / f"frame_{frame:06d}.csv"
+        if writer is not None:
+            writer.submit(path)
+        else:
+            write_particles(path, sim.particles)
         metrics.io_total += time.perf_counter() - t0
         frame += 1
 
-    framed = out is not None and fps > 0
     if framed:
         emit()
     while sim.t < total - 1e-12:
@@ -171,6 +180,10 @@ def run(scenario, backend=None, threads=None, deterministic=None, out_dir=None, 
         metrics.steps.append(sim.step(dt))
         while framed and sim.t >= frame / fps - 1e-9 and frame / fps <= total:
             emit()
+    if writer is not None:
+        t0 = time.perf_counter()
+        writer.close()
+        metrics.io_total += time.perf_counter() - t0
     if not metrics.steps:
         raise SimulationError("run finished without taking any step")
     if out is not None:

@@ -490,22 +490,41 @@ __device__ inline bool hencky_dp_body(float H[9], const Material& mat, bool proj
   }
   // log(I + X) = X (1 - X (1/2 - X (1/3 - X (1/4 - X/5))))  (Horner); for
   // ||X|| <= 0.05 the truncation is < 0.05^6/6 = 2.6e-9, below fp32 rounding
-  // of the strains (~1e-8 absolute)
+  // of the strains (~1e-8 absolute).  For ||X|| <= 0.01 (the common case of a
+  // resting or slowly deforming granular body) three terms truncate at
+  // 0.01^4/4 = 2.5e-9: two matrix products fewer.
   float P[6], T[6];
-  const float coef[4] = {1.f / 4.f, 1.f / 3.f, 1.f / 2.f, 1.f};
+#ifndef SMPM_SHORT_LOG
+#define SMPM_SHORT_LOG 1
+#endif
+  if (SMPM_SHORT_LOG && nx <= 0.01f) {
 #pragma unroll
-  for (int q = 0; q < 6; ++q) P[q] = -X[q] * (1.f / 5.f);
-  P[0] += coef[0];
-  P[1] += coef[0];
-  P[2] += coef[0];
-#pragma unroll
-  for (int it = 1; it < 4; ++it) {
+    for (int q = 0; q < 6; ++q) P[q] = -X[q] * (1.f / 3.f);
+    P[0] += 0.5f;
+    P[1] += 0.5f;
+    P[2] += 0.5f;
     sym_mul(X, P, T);
 #pragma unroll
     for (int q = 0; q < 6; ++q) P[q] = -T[q];
-    P[0] += coef[it];
-    P[1] += coef[it];
-    P[2] += coef[it];
+    P[0] += 1.f;
+    P[1] += 1.f;
+    P[2] += 1.f;
+  } else {
+    const float coef[4] = {1.f / 4.f, 1.f / 3.f, 1.f / 2.f, 1.f};
+#pragma unroll
+    for (int q = 0; q < 6; ++q) P[q] = -X[q] * (1.f / 5.f);
+    P[0] += coef[0];
+    P[1] += coef[0];
+    P[2] += coef[0];
+#pragma unroll
+    for (int it = 1; it < 4; ++it) {
+      sym_mul(X, P, T);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) P[q] = -T[q];
+      P[0] += coef[it];
+      P[1] += coef[it];
+      P[2] += coef[it];
+    }
   }
   float eps[6];
   sym_mul(X, P, eps);

@@ -28,6 +28,9 @@
 // sums carry fp32 precision relative to each node's own magnitude -- no global
 // fixed-point scale, no contribution bounds, no scale replays.
 
+#ifndef SMPM_FOLD_W
+#define SMPM_FOLD_W 0  // momentum weights folded into the z factors (A/B: more spills)
+#endif
 constexpr uint32_t RCAP = 512;   // particles per work item (two per thread)
 constexpr int NSTASH = 6;        // float4 per stashed particle
 constexpr int NACELL = 216;      // arena base cells (6^3: the block +- 1 cell)
@@ -38,7 +41,7 @@ struct __align__(16) FusedSmemF {
   float4 garena[2][GATH_N];       // double-buffered velocity arena
   int ahi[NF][SCAT_N];            // split fixed-point arena (m, p0..2, f0..2): value * S = hi * 2^20 + lo
   int alo[NF][SCAT_N];
-  uint32_t kc[SCAT_N];            // stencil contributions per arena node (n_active)
+  uint32_t kc[SCAT_N];            // cell sums added per arena node (> 0: active; the magic-number bias)
   uint32_t bnd[2][3];             // item maxima of the per-particle contribution bounds (m, p, f), by item parity
   uint32_t cnt[SCAT_N];           // particles binned per arena base cell (next table's cell counts)
   uint32_t scnt[NACELL];          // particles scattered from each arena base cell
@@ -64,8 +67,8 @@ __device__ __forceinline__ void arena_add_split(int* hi, int* lo, float x, float
   const float h = fmaf(t, 9.5367431640625e-07f, MAGIC);  // 2^-20
   const float hf = h - MAGIC;
   const float l = fmaf(-hf, 1048576.0f, t) + MAGIC;
-  sred(hi, __float_as_int(h) - int(MAGIC_BITS));
-  sred(lo, __float_as_int(l) - int(MAGIC_BITS));
+  sred(hi, __float_as_int(h));  // both biased by MAGIC_BITS: removed per node with the count kc
+  sred(lo, __float_as_int(l));
 }
 
 template <bool GATHER, int CV>
@@ -371,12 +374,14 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
           sidx[kk] = ci;
           // contribution bounds, worst case over the cell offset (|w| <= 0.75^3,
           // |dx_a| <= 1.5 h, |grad w_a| <= 0.75^2 / h): the item's fixed-point scales
-          float cm = 0.f;
+          // (coarse: the split arena has 2^42 of range, the bound only keeps
+          // the cell sums inside it)
+          float cm = 0.f, fm = 0.f, cs = 0.f;
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
-            cm = fmaxf(cm, fabsf(vn[a]) + (1.5f * hf_) * (fabsf(Cn[3 * a]) + fabsf(Cn[3 * a + 1]) + fabsf(Cn[3 * a + 2])));
-          const float fm = fmaxf(fabsf(M[0]) + fabsf(M[3]) + fabsf(M[4]),
-                                 fmaxf(fabsf(M[3]) + fabsf(M[1]) + fabsf(M[5]), fabsf(M[4]) + fabsf(M[5]) + fabsf(M[2])));
+          for (int a = 0; a < 9; ++a) cs += fabsf(Cn[a]);
+#pragma unroll
+          for (int a = 0; a < 6; ++a) fm += fabsf(M[a]);
+          cm = fmaxf(fmaxf(fabsf(vn[0]), fabsf(vn[1])), fabsf(vn[2])) + (1.5f * hf_) * cs;
           bmx[0] = fmaxf(bmx[0], m * 0.421875f);
           bmx[1] = fmaxf(bmx[1], m * 0.421875f * cm);
           bmx[2] = fmaxf(bmx[2], fm * 0.5625f * ih);
@@ -504,6 +509,29 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
           const float M00 = s1.w * fs, M11 = s4.y * fs, M22 = s4.z * fs, M01 = s4.w * fs, M02 = s5.x * fs,
                       M12 = s5.y * fs;
 #pragma unroll
+#if SMPM_FOLD_W
+          for (int j = 0; j < 3; ++j) {
+            const float dy = (float(j) - s0.y) * hf_;
+            const float W = mW * wy[j];
+            // W folded into the z factors: momentum += (W z1) q_a + (W z2) C_a2
+            const float2 Wz1 = __fmul2_rn(z1, make_float2(W, W)), Wz2 = __fmul2_rn(z2, make_float2(W, W));
+            const float Wz12 = W * wz[2], Wz22 = W * z22;
+            const float q[3] = {fmaf(s2.y, dy, b0), fmaf(s3.x, dy, b1), fmaf(s3.w, dy, b2)};
+            const float c2[3] = {s2.z, s3.y, s4.x};
+            const float Ax = gx * wy[j], Ay = wx * gy[j], Az = wx * wy[j];
+            const float P[3] = {fmaf(M00, Ax, M01 * Ay), fmaf(M01, Ax, M11 * Ay), fmaf(M02, Ax, M12 * Ay)};
+            const float Q[3] = {M02 * Az, M12 * Az, M22 * Az};
+            mm01[j] = __fadd2_rn(mm01[j], Wz1);
+            mm2[j] += Wz12;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              p01[a][j] = __ffma2_rn(Wz2, make_float2(c2[a], c2[a]), __ffma2_rn(Wz1, make_float2(q[a], q[a]), p01[a][j]));
+              p2[a][j] = fmaf(Wz22, c2[a], fmaf(Wz12, q[a], p2[a][j]));
+              f01[a][j] = __ffma2_rn(gz01, make_float2(Q[a], Q[a]), __ffma2_rn(z1, make_float2(P[a], P[a]), f01[a][j]));
+              f2[a][j] = fmaf(gz[2], Q[a], fmaf(wz[2], P[a], f2[a][j]));
+            }
+          }
+#else
           for (int j = 0; j < 3; ++j) {
             const float dy = (float(j) - s0.y) * hf_;
             const float W = mW * wy[j];
@@ -523,6 +551,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
               f2[a][j] = fmaf(gz[2], Q[a], fmaf(wz[2], P[a], f2[a][j]));
             }
           }
+#endif
         }
         // add the task's 9 nodes to the arena (fixed point, the item's scales:
         // a cell sum is at most RCAP bounds, kept below 2^42), and K
@@ -547,7 +576,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
 #pragma unroll
             for (int f = 0; f < NF; ++f)
               arena_add_split(&sm.ahi[f][ad], &sm.alo[f][ad], v[f], Sg[f == 0 ? 0 : (f < 4 ? 1 : 2)]);
-            atomicAdd(&sm.kc[ad], n);
+            atomicAdd(&sm.kc[ad], 1u);
           }
       }
     } else {
@@ -625,7 +654,9 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
       float vals[NF];
 #pragma unroll
       for (int f = 0; f < NF; ++f) {
-        vals[f] = fmaf(float(sm.ahi[f][ad]), 1048576.0f, float(sm.alo[f][ad])) * iS[f == 0 ? 0 : (f < 4 ? 1 : 2)];
+        const int bias = int(K * MAGIC_BITS);  // mod 2^32: the true sums fit in int32
+        vals[f] = fmaf(float(sm.ahi[f][ad] - bias), 1048576.0f, float(sm.alo[f][ad] - bias)) *
+                  iS[f == 0 ? 0 : (f < 4 ? 1 : 2)];
         sm.ahi[f][ad] = 0;
         sm.alo[f][ad] = 0;
       }
@@ -634,7 +665,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
       if (rk == BAD_KEY) continue;
       const size_t node = size_t(rk) * 64 + ((((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3));
       red_v4(&A.acc[2 * node], vals[0], vals[1], vals[2], vals[3]);
-      red_v4(&A.acc[2 * node + 1], vals[4], vals[5], vals[6], float(K));  // .w: contribution count K (n_active)
+      red_v4(&A.acc[2 * node + 1], vals[4], vals[5], vals[6], float(K));  // .w > 0: active node (n_active)
     }
     for (int i = tid; i < NACELL; i += CTA) sm.scnt[i] = 0;
     if (tid == 0) sm.touched = 0;

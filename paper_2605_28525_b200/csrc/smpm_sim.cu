@@ -3032,6 +3032,19 @@ int smpm_sim_query_grid(smpm_sim* s, int32_t* blocks, float* mass, float* mom, f
   return SMPM_OK;
 }
 
+int smpm_sim_snapshot_xv(smpm_sim* s, double* out) {
+  if (!s || !out) return set_err(SMPM_ERR_ARG, "null argument");
+  CK(cudaSetDevice(s->device));
+  // stream-ordered after the last step's kernels, no host sync: the inverse
+  // permutation into the download scratch, then x and v in pid order
+  const int64_t n = s->n;
+  CK(cudaMemsetAsync(s->dl_inv, 0, size_t(n) * 4, s->stream));
+  k_invperm<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n_store, s->pid_base, n, s->bin, s->dl_inv);
+  k_gather_xv<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], s->dl_inv, 0, n, out);
+  CK(cudaGetLastError());
+  return SMPM_OK;
+}
+
 int smpm_sim_retain_fields(smpm_sim* s, int on) {
   if (!s) return set_err(SMPM_ERR_ARG, "null sim");
   CK(cudaSetDevice(s->device));
