@@ -1,6 +1,7 @@
 """A few fused steps of a 16k-particle DP column (with a moving elastic
 block for larger strains) for compute-sanitizer (tools/sanitize.sh).
-usage: python tools/sanitize_run.py narrow|wide fast|det [steps]"""
+Mode from the environment: SMPM_MODE=fast|det, SMPM_ARENA, SMPM_ITEM_LAYOUT
+(see tools/sanitize.sh)."""
 import os
 import sys
 
@@ -8,9 +9,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np  # noqa: E402
 
-layout, mode = sys.argv[1], sys.argv[2]
-steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-os.environ["SMPM_ITEM_LAYOUT"] = layout
+mode = os.environ.get("SMPM_MODE", "fast")
+layout = os.environ.get("SMPM_ITEM_LAYOUT", "auto") + "/" + os.environ.get("SMPM_ARENA", "default")
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 
 from paper_2605_28525_b200 import scenes  # noqa: E402
 from paper_2605_28525_b200.solver import Simulation  # noqa: E402
