@@ -6,35 +6,34 @@
 // Reference: the P2G it replaces is the fused scatter of
 // /root/reference/pkg/src/sparsempm/solver.py:456-575 (per particle, 27 nodes,
 // 7 fields, one atomic per field per node).  Here a work item (up to RCAP = 512
-// particles of one block, slot-major) runs in five phases:
+// particles of one block, slot-major) runs in three phases, three barriers:
 //
-//   A   per particle: G2P from the smem velocity arena, F update, advection,
+//   A   all threads start the next item's velocity-arena prefetch; per
+//       particle: G2P from the smem velocity arena, F update, advection,
 //       Hencky/DP stress of the next step, record store, next-step keys; the
-//       P2G operands (cell offset d, m, v, C, M = V0 tau: 22 floats) go to a
-//       per-particle stash (the particle's own record stage slot), counted by
-//       the arena base cell the particle scatters from.
-//   S1  warp 0 scans the base-cell counts and lists the non-empty cells;
-//       warps 1..6 prefetch the next item's velocity arena.
-//   S2  every particle takes its slot in the cell-sorted order.
-//   S3  a task = (non-empty base cell, x offset oi) loops over the cell's
-//       particles and accumulates its 9 nodes x 7 fields in registers (fp32),
-//       then adds them to the fp32 smem arena: ~1/8 of an atomic per
+//       P2G operands (cell offset d, m, v, C, N = -V0 tau / h: 24 floats, laid
+//       out so every pair the scatter multiplies is an aligned float2) go to a
+//       per-particle stash (the particle's own record stage slot), and the
+//       slot is pushed onto its base cell's list (atomicExch on the list head;
+//       the first particle of a cell appends the cell to the task list).
+//   S   a task = (non-empty base cell, x offset i) walks the cell's list and
+//       accumulates its 9 nodes x 7 fields in registers (fp32, packed FFMA2:
+//       over k = 0,1 per field, over fields at k = 2), then adds them to the
+//       split fixed-point smem arena: ~1/8 of an atomic pair per
 //       particle-node-field instead of one.  Warp 7 inserts the item's touched
 //       blocks into the next step's table meanwhile.
 //   F   flush: bins, cell counts, red.global.add.v4.f32 of the arena nodes;
 //       records of the next item are fetched (cp.async) into the stage.
 //
-// The arena is fp32 (CAS-loop atomics, affordable at 1/8 the count), so grid
-// sums carry fp32 precision relative to each node's own magnitude -- no global
-// fixed-point scale, no contribution bounds, no scale replays.
+// Grid sums carry fp32 precision relative to each node's own magnitude: the
+// arena is int32 hi/lo fixed point (2^42 of range) with per-item scales, no
+// global scale, no scale replays.
 
-#ifndef SMPM_FOLD_W
-#define SMPM_FOLD_W 0  // momentum weights folded into the z factors (A/B: more spills)
-#endif
 constexpr uint32_t RCAP = 512;   // particles per work item (two per thread)
 constexpr int NSTASH = 6;        // float4 per stashed particle
 constexpr int NACELL = 216;      // arena base cells (6^3: the block +- 1 cell)
 constexpr int TASK_WARPS = 7;    // warps running scatter tasks (warp 7 inserts blocks)
+constexpr uint32_t LEND = 0xFFFFu;  // end of a cell list
 
 struct __align__(16) FusedSmemF {
   float4 st[2][NSTASH][CTA];      // per particle slot: record chunks 0..4 (stage), then the P2G stash
@@ -44,10 +43,9 @@ struct __align__(16) FusedSmemF {
   uint32_t kc[SCAT_N];            // cell sums added per arena node (> 0: active; the magic-number bias)
   uint32_t bnd[2][3];             // item maxima of the per-particle contribution bounds (m, p, f), by item parity
   uint32_t cnt[SCAT_N];           // particles binned per arena base cell (next table's cell counts)
-  uint32_t scnt[NACELL];          // particles scattered from each arena base cell
-  uint32_t soff[NACELL];          // their offsets in `order` (start, then end after placement)
-  uint16_t order[2 * CTA];        // stash slots (kk * CTA + tid) sorted by base cell
-  uint16_t tcell[NACELL];         // non-empty base cells (scatter tasks)
+  uint32_t head[NACELL];          // list head per arena base cell (stash slot kk * CTA + tid, LEND: empty)
+  uint16_t nxt[2 * CTA];          // list link per stash slot
+  uint16_t tcell[NACELL];         // non-empty base cells (scatter tasks), in arrival order
   uint32_t ntask;
   uint32_t touched;
   uint32_t rank[27];
@@ -57,17 +55,30 @@ struct __align__(16) FusedSmemF {
   Material mats[8];
 };
 
-// Adds x * S to one arena field as hi * 2^20 + lo (two native int32 reds, no
-// carries: |lo| <= 2^19).  t = x S is an fp32 value below 2^45, so both
-// parts are exact (magic-number rounding: h is t / 2^20 rounded to an
-// integer, |t / 2^20| < 2^25 ... kept below 2^22 by the scale choice; L = t -
-// 2^20 H is exact in an FFMA and rounded to an integer by the second magic).
-__device__ __forceinline__ void arena_add_split(int* hi, int* lo, float x, float S) {
+__device__ __forceinline__ float2 f2b(float a) { return make_float2(a, a); }
+
+// Adds the pair x * S to two arena words as hi * 2^20 + lo (four native int32
+// reds, no carries: |lo| <= 2^19).  t = x S is an fp32 value below 2^45, so
+// both parts are exact (magic-number rounding: h is t / 2^20 rounded to an
+// integer, kept below 2^22 by the scale choice; L = t - 2^20 H is exact in an
+// FFMA and rounded to an integer by the second magic).  Both words are biased
+// by MAGIC_BITS; the flush removes the bias with the count kc.
+__device__ __forceinline__ void arena_add_pair(int* hi0, int* lo0, int* hi1, int* lo1, float2 x, float2 S) {
+  const float2 t = __fmul2_rn(x, S);
+  const float2 h = __ffma2_rn(t, f2b(9.5367431640625e-07f), f2b(MAGIC));  // 2^-20
+  const float2 hf = __fadd2_rn(h, f2b(-MAGIC));
+  const float2 l = __fadd2_rn(__ffma2_rn(hf, f2b(-1048576.0f), t), f2b(MAGIC));
+  sred(hi0, __float_as_int(h.x));
+  sred(hi1, __float_as_int(h.y));
+  sred(lo0, __float_as_int(l.x));
+  sred(lo1, __float_as_int(l.y));
+}
+__device__ __forceinline__ void arena_add_one(int* hi, int* lo, float x, float S) {
   const float t = x * S;
-  const float h = fmaf(t, 9.5367431640625e-07f, MAGIC);  // 2^-20
+  const float h = fmaf(t, 9.5367431640625e-07f, MAGIC);
   const float hf = h - MAGIC;
   const float l = fmaf(-hf, 1048576.0f, t) + MAGIC;
-  sred(hi, __float_as_int(h));  // both biased by MAGIC_BITS: removed per node with the count kc
+  sred(hi, __float_as_int(h));
   sred(lo, __float_as_int(l));
 }
 
@@ -91,8 +102,11 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
       sm.kc[i] = 0;
       sm.cnt[i] = 0;
     }
-    for (int i = tid; i < NACELL; i += CTA) sm.scnt[i] = 0;
-    if (tid == 0) sm.touched = 0;
+    for (int i = tid; i < NACELL; i += CTA) sm.head[i] = LEND;
+    if (tid == 0) {
+      sm.touched = 0;
+      sm.ntask = 0;
+    }
   }
   // sorted positions of the thread's particles of an item: slot-major ranges
   // of RCAP (k_bin's wide placement), positions first + t and first + 256 + t
@@ -109,8 +123,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
     cnt = A.B.block_total[r];
     off = A.B.cell_off[r * 64 + 32] + cnt;  // level table: block start (k_scan2)
   };
-  // ---- prime: metadata of items 0..2, positions of items 0 and 1, records and
-  // velocity arena of item 0
+  // ---- prime: metadata of items 0..2, neighbour ranks of items 0 and 1,
+  // positions of items 0 and 1, records and velocity arena of item 0
   if (tid == 0) fetch_item(A, n_items, 0, sm.info[0], false);
   if (tid == 1) fetch_item(A, n_items, 1, sm.info[1], false);
   if (tid == 2) fetch_item(A, n_items, 2, sm.info[2], false);
@@ -120,6 +134,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
     const ItemInfo& i0 = sm.info[0];
     const ItemInfo& i1 = sm.info[1];
     if (GATHER && tid < 8 && i0.r() != BAD_KEY) sm.info[0].nbr[tid] = A.B.nbr8[size_t(i0.r()) * 8 + tid];
+    if (GATHER && tid >= 8 && tid < 16 && i1.r() != BAD_KEY)
+      sm.info[1].nbr[tid - 8] = A.B.nbr8[size_t(i1.r()) * 8 + tid - 8];
     uint32_t c0 = 0, o0 = 0, c1 = 0, o1 = 0;
     if (i0.r() != BAD_KEY) item_counts(i0.r(), c0, o0);
     if (i1.r() != BAD_KEY) item_counts(i1.r(), c1, o1);
@@ -148,7 +164,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
 
   while (true) {
     cp_async_wait_all();
-    __syncthreads();  // [B1] records and velocity arena of item i landed
+    __syncthreads();  // [B1] records and velocity arena of item i landed; item i-1 flushed
     const ItemInfo& cur = sm.info[c];
     const int c1r = c == 2 ? 0 : c + 1, c2r = c == 0 ? 2 : c - 1;
     const ItemInfo& nxt = sm.info[c1r];
@@ -156,10 +172,11 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
     if (cur.r() == BAD_KEY) break;
     int B0, B1, B2;
     cur.block(B0, B1, B2);
-    if (GATHER && tid < 8 && nxt.r() != BAD_KEY) sm.info[c1r].nbr[tid] = A.B.nbr8[size_t(nxt.r()) * 8 + tid];
+    // velocity arena of item i+1 (its neighbour ranks arrived with item i-1's flush)
+    if (GATHER && nxt.r() != BAD_KEY) prefetch_arena(sm.garena[buf ^ 1], A, nxt, tid, CTA);
+    cp_async_commit();
     uint32_t tmask = 0;
-    uint32_t sidx[2] = {0xFFFFu, 0xFFFFu};  // stash cell of the thread's particles (0xFFFF: none)
-    float bmx[3] = {0.f, 0.f, 0.f};         // contribution bounds of the thread's stashed particles
+    float bmx[3] = {0.f, 0.f, 0.f};  // contribution bounds of the thread's stashed particles
 
     // ================================================================ A
 #pragma unroll 1
@@ -362,16 +379,23 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
           }
         }
         if (ok && !far) {
-          // ---- stash the P2G operands (this slot's record stage is consumed)
+          // ---- stash the P2G operands (this slot's record stage is consumed):
+          // pairs the scatter multiplies sit in aligned float2 halves
+          //   s0 (dx, dy, dz, m)  s1 (v0, v1, C00, C10)  s2 (v2, C20, C01, C11)
+          //   s3 (C02, C12, C21, C22)  s4 (N00, N01, N01, N11)  s5 (N02, N12, N22, -)
+          // with C row-major and N = -M / h (M = V0 tau symmetric: xx yy zz xy xz yz)
           const uint32_t ci = uint32_t((ab[0] * 6 + ab[1]) * 6 + ab[2]);
+          const float nh = -ih;
           sm.st[kk][0][tid] = make_float4(d1[0], d1[1], d1[2], m);
-          sm.st[kk][1][tid] = make_float4(vn[0], vn[1], vn[2], M[0]);
-          sm.st[kk][2][tid] = make_float4(Cn[0], Cn[1], Cn[2], Cn[3]);
-          sm.st[kk][3][tid] = make_float4(Cn[4], Cn[5], Cn[6], Cn[7]);
-          sm.st[kk][4][tid] = make_float4(Cn[8], M[1], M[2], M[3]);
-          sm.st[kk][5][tid] = make_float4(M[4], M[5], 0.f, 0.f);
-          atomicAdd(&sm.scnt[ci], 1u);
-          sidx[kk] = ci;
+          sm.st[kk][1][tid] = make_float4(vn[0], vn[1], Cn[0], Cn[3]);
+          sm.st[kk][2][tid] = make_float4(vn[2], Cn[6], Cn[1], Cn[4]);
+          sm.st[kk][3][tid] = make_float4(Cn[2], Cn[5], Cn[7], Cn[8]);
+          sm.st[kk][4][tid] = make_float4(M[0] * nh, M[3] * nh, M[3] * nh, M[1] * nh);
+          sm.st[kk][5][tid] = make_float4(M[4] * nh, M[5] * nh, M[2] * nh, 0.f);
+          const uint32_t slot = uint32_t(kk * CTA + tid);
+          const uint32_t prev = atomicExch(&sm.head[ci], slot);
+          sm.nxt[slot] = uint16_t(prev);
+          if (prev == LEND) sm.tcell[atomicAdd(&sm.ntask, 1u)] = uint16_t(ci);
           // contribution bounds, worst case over the cell offset (|w| <= 0.75^3,
           // |dx_a| <= 1.5 h, |grad w_a| <= 0.75^2 / h): the item's fixed-point scales
           // (coarse: the split arena has 2^42 of range, the bound only keeps
@@ -409,175 +433,117 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
         if (lane == 0 && b) atomicMax(&sm.bnd[buf][f], b);
       }
     }
-    __syncthreads();  // [B2] stash, base-cell counts, touched blocks of item i
+    __syncthreads();  // [B2] stash, cell lists, touched blocks and bounds of item i
 
-    // ================================================================ S1
-    if (warp == 0) {
-      // exclusive scan of the 216 base-cell counts (7 per lane) and the list
-      // of non-empty cells
-      uint32_t cv[7], loc = 0, ne = 0;
-#pragma unroll
-      for (int q = 0; q < 7; ++q) {
-        const int cc = lane * 7 + q;
-        cv[q] = cc < NACELL ? sm.scnt[cc] : 0u;
-        loc += cv[q];
-        ne += cv[q] ? 1u : 0u;
-      }
-      uint32_t xs = loc, xn_ = ne;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, xs, o), z = __shfl_up_sync(0xffffffffu, xn_, o);
-        if (lane >= o) {
-          xs += y;
-          xn_ += z;
-        }
-      }
-      uint32_t run = xs - loc, tix = xn_ - ne;
-#pragma unroll
-      for (int q = 0; q < 7; ++q) {
-        const int cc = lane * 7 + q;
-        if (cc < NACELL) {
-          sm.soff[cc] = run;
-          run += cv[q];
-          if (cv[q]) sm.tcell[tix++] = uint16_t(cc);
-        }
-      }
-      if (lane == 31) sm.ntask = xn_;
-    } else if (warp <= 6) {
-      if (GATHER && nxt.r() != BAD_KEY) prefetch_arena(sm.garena[buf ^ 1], A, nxt, tid - 32, 6 * 32);
-    }
-    __syncthreads();  // [B3]
-
-    // ================================================================ S2
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk)
-      if (sidx[kk] != 0xFFFFu) sm.order[atomicAdd(&sm.soff[sidx[kk]], 1u)] = uint16_t(kk * CTA + tid);
-    __syncthreads();  // [B4] order complete (soff now holds each cell's end)
-
-    // ================================================================ S3
+    // ================================================================ S
     if (warp < TASK_WARPS) {
       const uint32_t nt = sm.ntask;
+      float Sg[3];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        const float b = __uint_as_float(sm.bnd[buf][f]);
+        Sg[f] = b > 0.f ? 8589934592.0f / b : 1.0f;  // 2^33 / bound = 2^42 / (RCAP bound)
+      }
 #pragma unroll 1
       for (uint32_t t = tid; t < 3 * nt; t += TASK_WARPS * 32) {
         const uint32_t oi = t / nt;
         const uint32_t cc = sm.tcell[t - oi * nt];
-        const uint32_t end = sm.soff[cc], n = sm.scnt[cc];
         const int a0 = int(cc / 36), a1 = int((cc / 6) % 6), a2 = int(cc % 6);
-        // node (oi, j, k) accumulators, packed over k = 0, 1 (.x, .y) + k = 2
+        // x weight of offset oi as a function of dx: t = dx - xc, w = wa + wb t^2, g = wg t
+        const float xc = oi == 0 ? 1.5f : (oi == 1 ? 1.0f : 0.5f);
+        const float wa = oi == 1 ? 0.75f : 0.0f, wb = oi == 1 ? -1.0f : 0.5f, wg = oi == 1 ? -2.0f : 1.0f;
+        const float oih = float(oi) * hf_;
+        // node (oi, j, k) accumulators: k = 0, 1 packed per field; k = 2
+        // packed over fields: (m, p2), (p0, p1), (f0, f1), f2
         const float2 Z2 = make_float2(0.f, 0.f);
-        float2 mm01[3], p01[3][3], f01[3][3];
-        float mm2[3], p2[3][3], f2[3][3];
+        float2 m01[3], p01[3][3], f01[3][3], mp2[3], pp2[3], ff2[3];
+        float f22[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-          mm01[j] = Z2;
-          mm2[j] = 0.f;
+          m01[j] = mp2[j] = pp2[j] = ff2[j] = Z2;
+          f22[j] = 0.f;
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            p01[a][j] = f01[a][j] = Z2;
-            p2[a][j] = f2[a][j] = 0.f;
-          }
+          for (int a = 0; a < 3; ++a) p01[a][j] = f01[a][j] = Z2;
         }
-        const float foi = float(oi);
+        uint32_t sl = sm.head[cc];
 #pragma unroll 1
-        for (uint32_t e = end - n; e < end; ++e) {
-          const uint32_t sl = sm.order[e];
+        while (sl != LEND) {
           const float4* sp = &sm.st[sl >> 8][0][sl & (CTA - 1)];
+          sl = sm.nxt[sl];
           const float4 s0 = sp[0], s1 = sp[CTA], s2 = sp[2 * CTA], s3 = sp[3 * CTA], s4 = sp[4 * CTA],
                        s5 = sp[5 * CTA];
-          // C row-major: s2 = C00 C01 C02 C10, s3 = C11 C12 C20 C21, s4.x = C22
-          // M = V0 tau: s1.w = xx, s4.y = yy, s4.z = zz, s4.w = xy, s5.x = xz, s5.y = yz
-          const float t0 = s0.x - 1.0f;
-          const float wx = oi == 0 ? 0.5f * (1.5f - s0.x) * (1.5f - s0.x)
-                                   : (oi == 1 ? 0.75f - t0 * t0 : 0.5f * (s0.x - 0.5f) * (s0.x - 0.5f));
-          const float gx = oi == 0 ? s0.x - 1.5f : (oi == 1 ? -2.0f * t0 : s0.x - 0.5f);
+          const float tx = s0.x - xc;
+          const float wx = fmaf(wb, tx * tx, wa), gx = wg * tx;
           float wy[3], gy[3], wz[3], gz[3];
           bspline(s0.y, wy, gy);
           bspline(s0.z, wz, gz);
-          // momentum m w (v + C dx) with dx = h (o - d): per node
-          //   z1_k R_a(j) + z2_k T_a(j), z1 = wz, z2 = wz (k - dz) h,
-          //   R_a = W (v_a + C_a0 dx + C_a1 dy), T_a = W C_a2, W = m wx wy_j;
-          // force -(M grad w), grad w = (gx wy wz, wx gy wz, wx wy gz) / h: per node
-          //   wz_k P_a(j) + gz_k Q_a(j), P_a = Mh_a0 gx wy + Mh_a1 wx gy, Q_a = Mh_a2 wx wy
-          const float2 z1 = make_float2(wz[0], wz[1]), gz01 = make_float2(gz[0], gz[1]);
-          const float dz0 = -s0.z * hf_;
-          const float2 z2 = make_float2(wz[0] * dz0, wz[1] * (dz0 + hf_));
-          const float z22 = wz[2] * (dz0 + 2.0f * hf_);
-          const float mW = s0.w * wx;
-          const float dx = (foi - s0.x) * hf_;
-          const float b0 = fmaf(s2.x, dx, s1.x), b1 = fmaf(s2.w, dx, s1.y), b2 = fmaf(s3.z, dx, s1.z);
-          const float fs = -ih;
-          const float M00 = s1.w * fs, M11 = s4.y * fs, M22 = s4.z * fs, M01 = s4.w * fs, M02 = s5.x * fs,
-                      M12 = s5.y * fs;
+          // momentum m w (v + C dx), dx = h (o - d): per node
+          //   wz_k R_a(j) + wz_k tz_k T_a(j), R_a = W (u_a + C_a1 ty_j), T_a = W C_a2,
+          //   u_a = v_a + C_a0 tx, W = m wx wy_j;
+          // force N grad w (N = -M / h, grad in cell units): per node
+          //   wz_k P_a(j) + gz_k Q_a(j), P_a = N_a0 gx wy_j + N_a1 wx gy_j, Q_a = N_a2 wx wy_j
+          const float txh = fmaf(-s0.x, hf_, oih);
+          const float2 u01 = __ffma2_rn(make_float2(s1.z, s1.w), f2b(txh), make_float2(s1.x, s1.y));
+          const float u2 = fmaf(s2.y, txh, s2.x);
+          const float X = s0.w * wx;
+          const float2 MG01 = __fmul2_rn(make_float2(s4.x, s4.y), f2b(gx));
+          const float2 MW01 = __fmul2_rn(make_float2(s4.z, s4.w), f2b(wx));
+          const float2 MQ01 = __fmul2_rn(make_float2(s5.x, s5.y), f2b(wx));
+          const float MG2 = s5.x * gx, MW2 = s5.y * wx, MQ2 = s5.z * wx;
+          const float tz0 = -s0.z * hf_;
+          const float2 z1 = make_float2(wz[0], wz[1]);
+          const float2 z2 = __fmul2_rn(z1, make_float2(tz0, tz0 + hf_));
+          const float z22 = wz[2] * (tz0 + 2.0f * hf_);
+          const float2 gz01 = make_float2(gz[0], gz[1]);
+          const float ty0 = -s0.y * hf_;
 #pragma unroll
-#if SMPM_FOLD_W
           for (int j = 0; j < 3; ++j) {
-            const float dy = (float(j) - s0.y) * hf_;
-            const float W = mW * wy[j];
-            // W folded into the z factors: momentum += (W z1) q_a + (W z2) C_a2
-            const float2 Wz1 = __fmul2_rn(z1, make_float2(W, W)), Wz2 = __fmul2_rn(z2, make_float2(W, W));
-            const float Wz12 = W * wz[2], Wz22 = W * z22;
-            const float q[3] = {fmaf(s2.y, dy, b0), fmaf(s3.x, dy, b1), fmaf(s3.w, dy, b2)};
-            const float c2[3] = {s2.z, s3.y, s4.x};
-            const float Ax = gx * wy[j], Ay = wx * gy[j], Az = wx * wy[j];
-            const float P[3] = {fmaf(M00, Ax, M01 * Ay), fmaf(M01, Ax, M11 * Ay), fmaf(M02, Ax, M12 * Ay)};
-            const float Q[3] = {M02 * Az, M12 * Az, M22 * Az};
-            mm01[j] = __fadd2_rn(mm01[j], Wz1);
-            mm2[j] += Wz12;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              p01[a][j] = __ffma2_rn(Wz2, make_float2(c2[a], c2[a]), __ffma2_rn(Wz1, make_float2(q[a], q[a]), p01[a][j]));
-              p2[a][j] = fmaf(Wz22, c2[a], fmaf(Wz12, q[a], p2[a][j]));
-              f01[a][j] = __ffma2_rn(gz01, make_float2(Q[a], Q[a]), __ffma2_rn(z1, make_float2(P[a], P[a]), f01[a][j]));
-              f2[a][j] = fmaf(gz[2], Q[a], fmaf(wz[2], P[a], f2[a][j]));
-            }
+            const float tyh = ty0 + float(j) * hf_;
+            const float W = X * wy[j];
+            const float2 R01 = __fmul2_rn(__ffma2_rn(make_float2(s2.z, s2.w), f2b(tyh), u01), f2b(W));
+            const float2 WR2 = make_float2(W, W * fmaf(s3.z, tyh, u2));
+            const float2 T01 = __fmul2_rn(make_float2(s3.x, s3.y), f2b(W));
+            const float T2 = W * s3.w;
+            const float2 P01 = __ffma2_rn(MG01, f2b(wy[j]), __fmul2_rn(MW01, f2b(gy[j])));
+            const float P2 = fmaf(MG2, wy[j], MW2 * gy[j]);
+            const float2 Q01 = __fmul2_rn(MQ01, f2b(wy[j]));
+            const float Q2 = MQ2 * wy[j];
+            m01[j] = __ffma2_rn(z1, f2b(W), m01[j]);
+            p01[0][j] = __ffma2_rn(z2, f2b(T01.x), __ffma2_rn(z1, f2b(R01.x), p01[0][j]));
+            p01[1][j] = __ffma2_rn(z2, f2b(T01.y), __ffma2_rn(z1, f2b(R01.y), p01[1][j]));
+            p01[2][j] = __ffma2_rn(z2, f2b(T2), __ffma2_rn(z1, f2b(WR2.y), p01[2][j]));
+            f01[0][j] = __ffma2_rn(gz01, f2b(Q01.x), __ffma2_rn(z1, f2b(P01.x), f01[0][j]));
+            f01[1][j] = __ffma2_rn(gz01, f2b(Q01.y), __ffma2_rn(z1, f2b(P01.y), f01[1][j]));
+            f01[2][j] = __ffma2_rn(gz01, f2b(Q2), __ffma2_rn(z1, f2b(P2), f01[2][j]));
+            mp2[j] = __ffma2_rn(WR2, f2b(wz[2]), mp2[j]);
+            mp2[j].y = fmaf(T2, z22, mp2[j].y);
+            pp2[j] = __ffma2_rn(T01, f2b(z22), __ffma2_rn(R01, f2b(wz[2]), pp2[j]));
+            ff2[j] = __ffma2_rn(Q01, f2b(gz[2]), __ffma2_rn(P01, f2b(wz[2]), ff2[j]));
+            f22[j] = fmaf(Q2, gz[2], fmaf(P2, wz[2], f22[j]));
           }
-#else
-          for (int j = 0; j < 3; ++j) {
-            const float dy = (float(j) - s0.y) * hf_;
-            const float W = mW * wy[j];
-            const float R0 = W * fmaf(s2.y, dy, b0), R1 = W * fmaf(s3.x, dy, b1), R2 = W * fmaf(s3.w, dy, b2);
-            const float T0 = W * s2.z, T1 = W * s3.y, T2 = W * s4.x;
-            const float Ax = gx * wy[j], Ay = wx * gy[j], Az = wx * wy[j];
-            const float P0 = fmaf(M00, Ax, M01 * Ay), P1 = fmaf(M01, Ax, M11 * Ay), P2 = fmaf(M02, Ax, M12 * Ay);
-            const float Q0 = M02 * Az, Q1 = M12 * Az, Q2 = M22 * Az;
-            mm01[j] = __ffma2_rn(z1, make_float2(W, W), mm01[j]);
-            mm2[j] = fmaf(wz[2], W, mm2[j]);
-            const float R[3] = {R0, R1, R2}, T[3] = {T0, T1, T2}, P[3] = {P0, P1, P2}, Q[3] = {Q0, Q1, Q2};
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              p01[a][j] = __ffma2_rn(z2, make_float2(T[a], T[a]), __ffma2_rn(z1, make_float2(R[a], R[a]), p01[a][j]));
-              p2[a][j] = fmaf(z22, T[a], fmaf(wz[2], R[a], p2[a][j]));
-              f01[a][j] = __ffma2_rn(gz01, make_float2(Q[a], Q[a]), __ffma2_rn(z1, make_float2(P[a], P[a]), f01[a][j]));
-              f2[a][j] = fmaf(gz[2], Q[a], fmaf(wz[2], P[a], f2[a][j]));
-            }
-          }
-#endif
         }
         // add the task's 9 nodes to the arena (fixed point, the item's scales:
         // a cell sum is at most RCAP bounds, kept below 2^42), and K
-        float Sg[3];
+        const float2 Smm = f2b(Sg[0]), Spp = f2b(Sg[1]), Sff = f2b(Sg[2]), Smp = make_float2(Sg[0], Sg[1]);
 #pragma unroll
-        for (int f = 0; f < 3; ++f) {
-          const float b = __uint_as_float(sm.bnd[buf][f]);
-          Sg[f] = b > 0.f ? 8589934592.0f / b : 1.0f;  // 2^33 / bound = 2^42 / (RCAP bound)
-        }
+        for (int j = 0; j < 3; ++j) {
+          const int d0 = aaddr(a0 + int(oi), a1 + j, a2), d1 = d0 + 1, d2 = d0 + 2;
+          arena_add_pair(&sm.ahi[0][d0], &sm.alo[0][d0], &sm.ahi[0][d1], &sm.alo[0][d1], m01[j], Smm);
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const int ad = aaddr(a0 + int(oi), a1 + j, a2 + k);
-            const float v[NF] = {k == 0 ? mm01[j].x : (k == 1 ? mm01[j].y : mm2[j]),
-                                 k == 0 ? p01[0][j].x : (k == 1 ? p01[0][j].y : p2[0][j]),
-                                 k == 0 ? p01[1][j].x : (k == 1 ? p01[1][j].y : p2[1][j]),
-                                 k == 0 ? p01[2][j].x : (k == 1 ? p01[2][j].y : p2[2][j]),
-                                 k == 0 ? f01[0][j].x : (k == 1 ? f01[0][j].y : f2[0][j]),
-                                 k == 0 ? f01[1][j].x : (k == 1 ? f01[1][j].y : f2[1][j]),
-                                 k == 0 ? f01[2][j].x : (k == 1 ? f01[2][j].y : f2[2][j])};
-#pragma unroll
-            for (int f = 0; f < NF; ++f)
-              arena_add_split(&sm.ahi[f][ad], &sm.alo[f][ad], v[f], Sg[f == 0 ? 0 : (f < 4 ? 1 : 2)]);
-            atomicAdd(&sm.kc[ad], 1u);
+          for (int a = 0; a < 3; ++a) {
+            arena_add_pair(&sm.ahi[1 + a][d0], &sm.alo[1 + a][d0], &sm.ahi[1 + a][d1], &sm.alo[1 + a][d1], p01[a][j],
+                           Spp);
+            arena_add_pair(&sm.ahi[4 + a][d0], &sm.alo[4 + a][d0], &sm.ahi[4 + a][d1], &sm.alo[4 + a][d1], f01[a][j],
+                           Sff);
           }
+          arena_add_pair(&sm.ahi[0][d2], &sm.alo[0][d2], &sm.ahi[3][d2], &sm.alo[3][d2], mp2[j], Smp);
+          arena_add_pair(&sm.ahi[1][d2], &sm.alo[1][d2], &sm.ahi[2][d2], &sm.alo[2][d2], pp2[j], Spp);
+          arena_add_pair(&sm.ahi[4][d2], &sm.alo[4][d2], &sm.ahi[5][d2], &sm.alo[5][d2], ff2[j], Sff);
+          arena_add_one(&sm.ahi[6][d2], &sm.alo[6][d2], f22[j], Sg[2]);
+          atomicAdd(&sm.kc[d0], 1u);
+          atomicAdd(&sm.kc[d1], 1u);
+          atomicAdd(&sm.kc[d2], 1u);
+        }
       }
     } else {
       // warp 7: insert the item's touched blocks into the next step's table
@@ -596,7 +562,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
         sm.rank[lane] = rk;
       }
     }
-    __syncthreads();  // [B5] arena and ranks of item i complete; the stash is free
+    __syncthreads();  // [B3] arena and ranks of item i complete; the stash is free
 
     // ================================================================ F
     // records of item i+1 into the stage (overlaps the flush)
@@ -612,6 +578,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
     }
     if (tid == 0) fetch_item(A, n_items, kf, sm.info[c], true);  // item i+3 -> this item's ring slot
     cp_async_commit();
+    // neighbour ranks of item i+2 (its velocity arena is prefetched at item i+1's start)
+    if (GATHER && tid < 8 && nn.r() != BAD_KEY) sm.info[c2r].nbr[tid] = A.B.nbr8[size_t(nn.r()) * 8 + tid];
     uint32_t cnt2 = 0, off2 = 0;  // item i+2's range (consumed after the flush)
     if (nn.r() != BAD_KEY) item_counts(nn.r(), cnt2, off2);
     // bins of item i (positions from ring slot c)
@@ -638,6 +606,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
         const uint32_t lc = (((i + 3) & 3) << 4) | (((j + 3) & 3) << 2) | ((k + 3) & 3);
         if (rq2 != BAD_KEY) atomicAdd(&A.S.cell_count[rq2 * 64 + lc], cc);
       }
+      sm.head[nd] = LEND;
     }
     float iS[3];
 #pragma unroll
@@ -667,8 +636,10 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
       red_v4(&A.acc[2 * node], vals[0], vals[1], vals[2], vals[3]);
       red_v4(&A.acc[2 * node + 1], vals[4], vals[5], vals[6], float(K));  // .w > 0: active node (n_active)
     }
-    for (int i = tid; i < NACELL; i += CTA) sm.scnt[i] = 0;
-    if (tid == 0) sm.touched = 0;
+    if (tid == 0) {
+      sm.touched = 0;
+      sm.ntask = 0;
+    }
     // item i+2's sorted positions (ring slot of item i-1; loads issued before
     // the flush) and source indices
     slots(nn, cnt2, off2, c2r);
@@ -683,5 +654,5 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
   }
   vmax2_local = warp_max(vmax2_local);
   if (lane == 0 && vmax2_local) atomicMax(&A.stS->vmax2_bits, vmax2_local);
-  if (blockIdx.x == 0 && tid < 3) A.stS->scale_inv[tid] = 0.f;  // fp32 arena: no fixed-point scales
+  if (blockIdx.x == 0 && tid < 3) A.stS->scale_inv[tid] = 0.f;  // fp32-grade arena: no global fixed-point scales
 }
