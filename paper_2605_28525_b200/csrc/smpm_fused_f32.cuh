@@ -50,12 +50,17 @@ struct __align__(16) FusedSmemF {
   uint32_t touched;
   uint32_t rank[27];
   uint32_t posr[3][2][CTA];       // sorted positions of the thread's particles (ring: items i, i+1, i+2)
+  uint32_t icnt[3][2];            // (particle count, first sorted position) of the ring's blocks
   uint32_t binr[2][CTA];          // bins of the item awaiting its ranks
   ItemInfo info[3];
   Material mats[8];
 };
 
 __device__ __forceinline__ float2 f2b(float a) { return make_float2(a, a); }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
 
 // Adds the pair x * S to two arena words as hi * 2^20 + lo (four native int32
 // reds, no carries: |lo| <= 2^19).  t = x S is an fp32 value below 2^45, so
@@ -110,18 +115,17 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
   }
   // sorted positions of the thread's particles of an item: slot-major ranges
   // of RCAP (k_bin's wide placement), positions first + t and first + 256 + t
-  auto slots = [&](const ItemInfo& inf, uint32_t cnt, uint32_t off, int ring) {
+  // (count, start): the block's particle count and first sorted position (the
+  // level table's block start, k_scan2), from icnt[ring]
+  auto slots = [&](const ItemInfo& inf, int ring) {
+    const uint32_t cnt = sm.icnt[ring][0], start = sm.icnt[ring][1];
     const uint32_t first = inf.g() * RCAP;
     const uint32_t n = inf.r() != BAD_KEY && cnt > first ? min(cnt - first, RCAP) : 0u;
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk) {
       const uint32_t j = CTA * kk + tid;
-      sm.posr[ring][kk][tid] = j < n ? off - cnt + first + j : NOPOS;
+      sm.posr[ring][kk][tid] = j < n ? start + first + j : NOPOS;
     }
-  };
-  auto item_counts = [&](uint32_t r, uint32_t& cnt, uint32_t& off) {
-    cnt = A.B.block_total[r];
-    off = A.B.cell_off[r * 64 + 32] + cnt;  // level table: block start (k_scan2)
   };
   // ---- prime: metadata of items 0..2, neighbour ranks of items 0 and 1,
   // positions of items 0 and 1, records and velocity arena of item 0
@@ -136,11 +140,17 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
     if (GATHER && tid < 8 && i0.r() != BAD_KEY) sm.info[0].nbr[tid] = A.B.nbr8[size_t(i0.r()) * 8 + tid];
     if (GATHER && tid >= 8 && tid < 16 && i1.r() != BAD_KEY)
       sm.info[1].nbr[tid - 8] = A.B.nbr8[size_t(i1.r()) * 8 + tid - 8];
-    uint32_t c0 = 0, o0 = 0, c1 = 0, o1 = 0;
-    if (i0.r() != BAD_KEY) item_counts(i0.r(), c0, o0);
-    if (i1.r() != BAD_KEY) item_counts(i1.r(), c1, o1);
-    slots(i0, c0, o0, 0);
-    slots(i1, c1, o1, 1);
+    if (tid >= 16 && tid < 18) {
+      const ItemInfo& ii = sm.info[tid - 16];
+      if (ii.r() != BAD_KEY) {
+        sm.icnt[tid - 16][0] = A.B.block_total[ii.r()];
+        sm.icnt[tid - 16][1] = A.B.cell_off[size_t(ii.r()) * 64 + 32];
+      }
+    }
+  }
+  __syncthreads();
+  {
+    slots(sm.info[0], 0);
     if (GATHER) {
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
@@ -152,9 +162,6 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
         }
       }
     }
-    const uint32_t pa = sm.posr[1][0][tid], pb = sm.posr[1][1][tid];
-    if (pa != NOPOS) src1a = A.perm[pa];
-    if (pb != NOPOS) src1b = A.perm[pb];
   }
   __syncthreads();
   if (GATHER && sm.info[0].r() != BAD_KEY) prefetch_arena(sm.garena[0], A, sm.info[0], tid, CTA);
@@ -172,9 +179,17 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
     if (cur.r() == BAD_KEY) break;
     int B0, B1, B2;
     cur.block(B0, B1, B2);
-    // velocity arena of item i+1 (its neighbour ranks arrived with item i-1's flush)
+    // velocity arena of item i+1 (its neighbour ranks arrived with item i-1's
+    // flush), sorted positions and source indices of its particles (consumed
+    // by this item's flush)
     if (GATHER && nxt.r() != BAD_KEY) prefetch_arena(sm.garena[buf ^ 1], A, nxt, tid, CTA);
     cp_async_commit();
+    slots(nxt, c1r);
+    {
+      const uint32_t pa = sm.posr[c1r][0][tid], pb = sm.posr[c1r][1][tid];
+      src1a = pa != NOPOS ? A.perm[pa] : 0u;
+      src1b = pb != NOPOS ? A.perm[pb] : 0u;
+    }
     uint32_t tmask = 0;
     float bmx[3] = {0.f, 0.f, 0.f};  // contribution bounds of the thread's stashed particles
 
@@ -577,11 +592,14 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
       }
     }
     if (tid == 0) fetch_item(A, n_items, kf, sm.info[c], true);  // item i+3 -> this item's ring slot
+    // neighbour ranks and particle range of item i+2 (used from item i+1's start)
+    if (nn.r() != BAD_KEY) {
+      if (GATHER && tid >= 32 && tid < 34)
+        cp_async16(&sm.info[c2r].nbr[4 * (tid - 32)], A.B.nbr8 + size_t(nn.r()) * 8 + 4 * (tid - 32));
+      if (tid == 34) cp_async4(&sm.icnt[c2r][0], A.B.block_total + nn.r());
+      if (tid == 35) cp_async4(&sm.icnt[c2r][1], A.B.cell_off + size_t(nn.r()) * 64 + 32);
+    }
     cp_async_commit();
-    // neighbour ranks of item i+2 (its velocity arena is prefetched at item i+1's start)
-    if (GATHER && tid < 8 && nn.r() != BAD_KEY) sm.info[c2r].nbr[tid] = A.B.nbr8[size_t(nn.r()) * 8 + tid];
-    uint32_t cnt2 = 0, off2 = 0;  // item i+2's range (consumed after the flush)
-    if (nn.r() != BAD_KEY) item_counts(nn.r(), cnt2, off2);
     // bins of item i (positions from ring slot c)
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk) {
@@ -639,14 +657,6 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
     if (tid == 0) {
       sm.touched = 0;
       sm.ntask = 0;
-    }
-    // item i+2's sorted positions (ring slot of item i-1; loads issued before
-    // the flush) and source indices
-    slots(nn, cnt2, off2, c2r);
-    {
-      const uint32_t pa = sm.posr[c2r][0][tid], pb = sm.posr[c2r][1][tid];
-      src1a = pa != NOPOS ? A.perm[pa] : 0u;
-      src1b = pb != NOPOS ? A.perm[pb] : 0u;
     }
     ++kf;
     buf ^= 1;
