@@ -463,7 +463,13 @@ __device__ inline int hencky_dp_mid(float H[9], const float X[6], const Material
 // of eps, F' = U exp(e') V^T = exp(eps' - eps) F.
 // MID: strains beyond the series range take hencky_dp_mid before the Jacobi
 // path (chosen per kernel variant, see hencky_dp below).
-template <bool MID>
+// MODE 0: series, Jacobi beyond; 1: series, moderate-strain path beyond (Jacobi
+// past that); 2: as 1, but a warp with any lane beyond the series range sends
+// all its lanes down the moderate-strain path (one path per warp instead of
+// both: the late, disordered regime mixes the two in most warps).  MODE 2
+// makes a particle's path depend on its warp neighbours, so the deterministic
+// mode (layout-independent bits) uses 1.
+template <int MODE>
 __device__ inline bool hencky_dp_body(float H[9], const Material& mat, bool project, float tau[6], float& J) {
   const float trH = H[0] + H[4] + H[8];
   const float m2 = (H[0] * H[4] - H[1] * H[3]) + (H[0] * H[8] - H[2] * H[6]) + (H[4] * H[8] - H[5] * H[7]);
@@ -481,13 +487,14 @@ __device__ inline bool hencky_dp_body(float H[9], const Material& mat, bool proj
   X[5] = (H[5] + H[7]) + (H[3] * H[6] + H[4] * H[7] + H[5] * H[8]);
   const float nx = fmaxf(fabsf(X[0]) + fabsf(X[3]) + fabsf(X[4]),
                          fmaxf(fabsf(X[3]) + fabsf(X[1]) + fabsf(X[5]), fabsf(X[4]) + fabsf(X[5]) + fabsf(X[2])));
-  if (!(nx <= 0.05f)) {
-    if (MID) {
-      const int mid = hencky_dp_mid(H, X, mat, project, tau, J);
-      if (mid != 0) return mid > 0;
-    }
-    return hencky_dp_eig(H, mat, project, tau, J);
+  const bool big = !(nx <= 0.05f);
+  bool use_mid = MODE != 0 && big;
+  if (MODE == 2) use_mid = __any_sync(__activemask(), big);
+  if (use_mid) {
+    const int mid = hencky_dp_mid(H, X, mat, project, tau, J);
+    if (mid != 0) return mid > 0;
   }
+  if (big) return hencky_dp_eig(H, mat, project, tau, J);
   // log(I + X) = X (1 - X (1/2 - X (1/3 - X (1/4 - X/5))))  (Horner); for
   // ||X|| <= 0.05 the truncation is < 0.05^6/6 = 2.6e-9, below fp32 rounding
   // of the strains (~1e-8 absolute).  For ||X|| <= 0.01 (the common case of a
@@ -735,7 +742,7 @@ __device__ inline void err_report(unsigned long long* err, uint32_t code, uint64
 
 
 // CV = 0: series + Jacobi, inlined (ordered regime); 1: series + moderate-
-// strain path + Jacobi, inlined; 2: the same compiled once, out of line, so
+// strain path + Jacobi, inlined, path voted per warp (MODE 2 above); 2: the same compiled once, out of line, so
 // every deterministic kernel variant (both work-item layouts) runs the same
 // machine code and bitwise results do not depend on the layout choice
 // (inlined copies may contract multiply-adds differently).
@@ -748,7 +755,7 @@ struct HenckyIO {
   int ok;
 };
 static __device__ __noinline__ HenckyIO hencky_dp_shared(HenckyIO io, const Material& mat, bool project) {
-  io.ok = hencky_dp_body<true>(io.H, mat, project, io.tau, io.J) ? 1 : 0;
+  io.ok = hencky_dp_body<1>(io.H, mat, project, io.tau, io.J) ? 1 : 0;
   return io;
 }
 template <int CV = 0>
@@ -765,7 +772,7 @@ __device__ __forceinline__ bool hencky_dp(float H[9], const Material& mat, bool 
     J = io.J;
     return io.ok != 0;
   }
-  return hencky_dp_body<CV == 1>(H, mat, project, tau, J);
+  return hencky_dp_body<CV == 1 ? 2 : 0>(H, mat, project, tau, J);
 }
 
 }  // namespace smpm

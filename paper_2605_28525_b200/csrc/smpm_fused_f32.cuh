@@ -29,6 +29,9 @@
 // arena is int32 hi/lo fixed point (2^42 of range) with per-item scales, no
 // global scale, no scale replays.
 
+#ifndef SMPM_ABL
+#define SMPM_ABL 0  // timing ablations (results wrong): 1 no scatter tasks, 2 no stress, 4 no flush, 8 no gather
+#endif
 constexpr uint32_t RCAP = 512;   // particles per work item (two per thread)
 constexpr int NSTASH = 6;        // float4 per stashed particle
 constexpr int NACELL = 216;      // arena base cells (6^3: the block +- 1 cell)
@@ -47,7 +50,6 @@ struct __align__(16) FusedSmemF {
   uint16_t nxt[2 * CTA];          // list link per stash slot
   uint16_t tcell[NACELL];         // non-empty base cells (scatter tasks), in arrival order
   uint32_t ntask;
-  uint32_t touched;
   uint32_t rank[27];
   uint32_t posr[3][2][CTA];       // sorted positions of the thread's particles (ring: items i, i+1, i+2)
   uint32_t icnt[3][2];            // (particle count, first sorted position) of the ring's blocks
@@ -77,6 +79,15 @@ __device__ __forceinline__ void arena_add_pair(int* hi0, int* lo0, int* hi1, int
   sred(hi1, __float_as_int(h.y));
   sred(lo0, __float_as_int(l.x));
   sred(lo1, __float_as_int(l.y));
+}
+// Power-of-two item scale for contribution bound b (bits of a non-negative
+// float): S = 2^(32-e) for b in [2^e, 2^(e+1)), so a cell sum of <= RCAP = 2^9
+// bounds times S stays below 2^42; iS = 1/S exactly.  b = 0: S = 1.
+__device__ __forceinline__ void item_scale(uint32_t bbits, float& S, float& iS) {
+  const int e = bbits ? int((bbits >> 23) & 0xFFu) - 127 : 32;
+  const int s = max(-100, min(100, 32 - e));
+  S = __uint_as_float(uint32_t(127 + s) << 23);
+  iS = __uint_as_float(uint32_t(127 - s) << 23);
 }
 __device__ __forceinline__ void arena_add_one(int* hi, int* lo, float x, float S) {
   const float t = x * S;
@@ -109,7 +120,6 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
     }
     for (int i = tid; i < NACELL; i += CTA) sm.head[i] = LEND;
     if (tid == 0) {
-      sm.touched = 0;
       sm.ntask = 0;
     }
   }
@@ -190,7 +200,6 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
       src1a = pa != NOPOS ? A.perm[pa] : 0u;
       src1b = pb != NOPOS ? A.perm[pb] : 0u;
     }
-    uint32_t tmask = 0;
     float bmx[3] = {0.f, 0.f, 0.f};  // contribution bounds of the thread's stashed particles
 
     // ================================================================ A
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
         const uint32_t pm = __float_as_uint(c4.y);
         const uint32_t pidv = pm & PID_MASK;
         const int mt = int(pm >> 29);
-        if (GATHER) {
+        if (GATHER && !(SMPM_ABL & 8)) {
           // ---- G2P (solver.py:628-732), as k_g2p2g
           int lb[3];
           float d[3], w[3][3], g[3][3];
@@ -322,6 +331,9 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
           xn[0] = __dadd_rn(xn[0], __dmul_rn(dt, double(vn[0])));
           xn[1] = __dadd_rn(xn[1], __dmul_rn(dt, double(vn[1])));
           xn[2] = __dadd_rn(xn[2], __dmul_rn(dt, double(vn[2])));
+        } else if (SMPM_ABL & 8) {
+          vn[0] = vn[1] = vn[2] = 0.f;
+          for (int q = 0; q < 9; ++q) Cn[q] = 0.f;
         } else {
           vn[0] = c4.z;
           vn[1] = c4.w;
@@ -339,7 +351,9 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
         // ---- stress of the next step (materials.py:169-238)
         float tau[6], J;
         const Material& mat = sm.mats[mt];
-        if (!hencky_dp<CV>(F, mat, A.project != 0, tau, J)) {
+        if (SMPM_ABL & 2) {
+          tau[0] = F[0] * mat.mu; tau[1] = F[4] * mat.mu; tau[2] = F[8] * mat.mu; tau[3] = tau[4] = tau[5] = 0.f;
+        } else if (!hencky_dp<CV>(F, mat, A.project != 0, tau, J)) {
           err_report(A.err, ERR_DEGENERATE_F, pidv);
           ok = false;
           tau[0] = tau[1] = tau[2] = tau[3] = tau[4] = tau[5] = 0.f;
@@ -424,7 +438,6 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
           bmx[0] = fmaxf(bmx[0], m * 0.421875f);
           bmx[1] = fmaxf(bmx[1], m * 0.421875f * cm);
           bmx[2] = fmaxf(bmx[2], fm * 0.5625f * ih);
-          tmask |= touched27(axis_blocks(ab[0]), axis_blocks(ab[1]), axis_blocks(ab[2]));
           if (mig < 0) {
             atomicAdd(&sm.cnt[aaddr(ab[0], ab[1], ab[2])], 1u);
             binv = BIN_ARENA | uint32_t((ab[0] << 6) | (ab[1] << 3) | ab[2]);
@@ -440,11 +453,9 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
       sm.binr[kk][tid] = valid ? binv : BIN_SKIP;
     }
     {
-      const uint32_t tm = __reduce_or_sync(0xffffffffu, tmask);
-      if (lane == 0 && tm) atomicOr(&sm.touched, tm);
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
-        const uint32_t b = warp_max(__float_as_uint(bmx[f]));
+        const uint32_t b = __reduce_max_sync(0xffffffffu, __float_as_uint(bmx[f]));
         if (lane == 0 && b) atomicMax(&sm.bnd[buf][f], b);
       }
     }
@@ -452,13 +463,10 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
 
     // ================================================================ S
     if (warp < TASK_WARPS) {
-      const uint32_t nt = sm.ntask;
-      float Sg[3];
+      const uint32_t nt = (SMPM_ABL & 1) ? 0u : sm.ntask;
+      float Sg[3], iSg;
 #pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        const float b = __uint_as_float(sm.bnd[buf][f]);
-        Sg[f] = b > 0.f ? 8589934592.0f / b : 1.0f;  // 2^33 / bound = 2^42 / (RCAP bound)
-      }
+      for (int f = 0; f < 3; ++f) item_scale(sm.bnd[buf][f], Sg[f], iSg);
 #pragma unroll 1
       for (uint32_t t = tid; t < 3 * nt; t += TASK_WARPS * 32) {
         const uint32_t oi = t / nt;
@@ -561,8 +569,15 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
         }
       }
     } else {
-      // warp 7: insert the item's touched blocks into the next step's table
-      const uint32_t tm = sm.touched;
+      // warp 7: the blocks the item's stencils touch (from its non-empty base
+      // cells), inserted into the next step's table
+      const uint32_t nt = sm.ntask;
+      uint32_t tm = 0;
+      for (uint32_t e = lane; e < nt; e += 32) {
+        const uint32_t cc = sm.tcell[e];
+        tm |= touched27(axis_blocks(int(cc / 36)), axis_blocks(int((cc / 6) % 6)), axis_blocks(int(cc % 6)));
+      }
+      tm = __reduce_or_sync(0xffffffffu, tm);
       if (lane < 27) {
         uint32_t rk = BAD_KEY;
         if ((tm >> lane) & 1u) {
@@ -629,15 +644,15 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
     float iS[3];
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
-      const float b = __uint_as_float(sm.bnd[buf][f]);
-      iS[f] = b > 0.f ? b * (1.0f / 8589934592.0f) : 1.0f;
+      float S_;
+      item_scale(sm.bnd[buf][f], S_, iS[f]);
     }
     if (tid < 3) sm.bnd[buf ^ 1][tid] = 0;  // the next item's (item i-1 is done with them)
     for (int nd = tid; nd < 512; nd += CTA) {
       const int i = nd >> 6, j = (nd >> 3) & 7, k = nd & 7;
       const int ad = aaddr(i, j, k);
       const uint32_t K = sm.kc[ad];
-      if (!K) continue;
+      if (!K || (SMPM_ABL & 4)) continue;
       float vals[NF];
 #pragma unroll
       for (int f = 0; f < NF; ++f) {
@@ -654,15 +669,12 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
       red_v4(&A.acc[2 * node], vals[0], vals[1], vals[2], vals[3]);
       red_v4(&A.acc[2 * node + 1], vals[4], vals[5], vals[6], float(K));  // .w > 0: active node (n_active)
     }
-    if (tid == 0) {
-      sm.touched = 0;
-      sm.ntask = 0;
-    }
+    if (tid == 0) sm.ntask = 0;
     ++kf;
     buf ^= 1;
     c = c1r;
   }
-  vmax2_local = warp_max(vmax2_local);
+  vmax2_local = __reduce_max_sync(0xffffffffu, vmax2_local);
   if (lane == 0 && vmax2_local) atomicMax(&A.stS->vmax2_bits, vmax2_local);
   if (blockIdx.x == 0 && tid < 3) A.stS->scale_inv[tid] = 0.f;  // fp32-grade arena: no global fixed-point scales
 }
