@@ -196,6 +196,14 @@ int smpm_sim_get_particles(smpm_sim* s, double* x, double* v, double* C, double*
 int smpm_sim_step(smpm_sim* s, double dt);
 /* Waits for the last step and returns its stats (status != 0 on error). */
 int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out);
+/* n steps (dt <= 0: the CFL bound each step) with one host synchronisation
+ * per batch of up to 1024 steps: the reference's loop of Simulation.step
+ * calls (solver.py:1001-1093; bench.py:216-226).  The between-step checks
+ * (dt bound, errors, grid capacity) run on the device; a failing step halts
+ * its batch and is handled as after smpm_sim_step + smpm_sim_sync.  out[i]
+ * (may be NULL) receives step i's stats, *n_done the steps completed; returns
+ * the first error. */
+int smpm_sim_run(smpm_sim* s, int64_t n, double dt, smpm_step_stats* out, int64_t* n_done);
 /* Active blocks (int32 (n,3), rank order) and nodal fields after the
  * step's P2G: mass, momentum, force (f32, gravity included). Host pointers,
  * sized by smpm_sim_sync's n_blocks. */

@@ -103,6 +103,7 @@ _SIGS = {
     "smpm_sim_get_particles": (ctypes.c_int, [P, P, P, P, P, P, P]),
     "smpm_sim_step": (ctypes.c_int, [P, D]),
     "smpm_sim_sync": (ctypes.c_int, [P, P]),
+    "smpm_sim_run": (ctypes.c_int, [P, I64, D, P, P]),
     "smpm_sim_query_grid": (ctypes.c_int, [P, P, P, P, P]),
     "smpm_sim_num_particles": (I64, [P]),
     "smpm_sim_vmax": (D, [P]),

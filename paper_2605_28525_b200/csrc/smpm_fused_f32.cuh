@@ -102,6 +102,7 @@ template <bool GATHER, int CV>
 __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
   FusedSmemF& sm = *reinterpret_cast<FusedSmemF*>(smraw);
+  if (*A.B.halt) return;  // a batched step that must not run (smpm_sim_run)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < A.n_mat && i < 8; i += CTA) sm.mats[i] = A.mats[i];
   const uint32_t n_items = A.stB->n_items;

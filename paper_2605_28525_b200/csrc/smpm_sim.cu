@@ -72,7 +72,8 @@ constexpr uint32_t MAGIC_BITS = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float MAGIC = 12582912.0f;
 constexpr uint32_t BAD_KEY = 0xFFFFFFFFu;  // bin of a hole (departed particle) or an invalid one
 constexpr uint32_t OVF_KEY = 0xFFFFFFFEu;  // live particle whose block did not fit (replayed after growth)
-constexpr uint32_t MIG_KEY = 0xFFFFFFFDu;  // left this rank's slab: live until the exchange hands it over
+constexpr uint32_t MIG_KEY = 0xFFFFFFFDu;
+constexpr uint32_t HALT_ERR = 1, HALT_OVERFLOW = 2, HALT_DT = 3;  // why a batched step did not run  // left this rank's slab: live until the exchange hands it over
 // Gather arena: float4 velocity per node, nodes 4B .. 4B+5 per axis, address
 // (k ^ 4*(j&1)) + 8 j + 48 i in float4 units: each quarter-warp (2x4 cells)
 // reads 8 distinct 16-byte bank groups, so the 27 LDS.128 per particle are
@@ -103,6 +104,7 @@ struct TableDev {
   uint4* items;          // [cap_items] (rank, group, block key lo, hi)
   uint32_t* tile_sums;   // [3*max_tiles]
   uint32_t* done;        // last-CTA counter
+  uint32_t* halt;        // batched steps (smpm_sim_run): nonzero once a step must not run (shared by both tables)
 };
 
 // Device-side per-table statistics (the step whose particles are binned in
@@ -133,6 +135,7 @@ struct StepParams {
   int bx0, bx1;  // owned block-x range (n_active / n_owned count owned blocks only)
   int wide;      // work-item layout (see k_g2p2g): 0 cell slots, 1 block ranges of `cap`
   uint32_t cap;  // particles per block-range item (WIDE_CAP, or RCAP for the fp32-arena kernel)
+  int batch;     // smpm_sim_run: dt and the halt conditions are decided on the device
 };
 
 // ------------------------------------------------------------------ scan
@@ -182,6 +185,29 @@ __device__ inline uint32_t cta_excl_scan(uint32_t v, uint32_t* sh /*[8]*/, uint3
 __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
                                                unsigned long long* err, StepParams sp, uint32_t* nstore) {
   __shared__ bool last;
+  double dt_dev = sp.dt_req;
+  if (sp.batch) {
+    // batched steps: the checks smpm_sim_step/smpm_sim_sync make on the host
+    // between steps, decided identically by every CTA from the previous
+    // step's outputs; a failing check halts this and every later step of the
+    // batch (the host then handles it as after a single step)
+    if (*S.halt) return;
+    uint32_t code = 0;
+    if (*err != ERR_CLEAR) {
+      code = HALT_ERR;
+    } else if (*S.hv.overflow || *S.hv.counter > S.hv.cap_blocks) {
+      code = HALT_OVERFLOW;
+    } else {  // CFL bound and dt validation (solver.py:984-987, 1021-1030)
+      const double vmax = sqrt(double(__uint_as_float(stS->vmax2_bits)));
+      const double bound = sp.cfl * sp.h / (sp.wave_speed + vmax);
+      dt_dev = sp.dt_req > 0 ? sp.dt_req : bound;
+      if (dt_dev > bound * (1.0 + 1e-9)) code = HALT_DT;
+    }
+    if (code) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *S.halt = code;
+      return;
+    }
+  }
   const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
   const int ntiles = (nb + TB - 1) / TB;
   const int lane = threadIdx.x & 31;
@@ -237,8 +263,9 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
     st->n_owned = carry[3];
     st->n_items_alt = carry[2];
     st->overflow = *S.hv.overflow | (*S.hv.counter > S.hv.cap_blocks ? 1u : 0u);
-    // dt is validated on the host against the CFL bound (solver.py:1021-1030)
-    st->dt = sp.dt_req;
+    // dt is validated against the CFL bound on the host (single steps) or
+    // above (batched steps) (solver.py:1021-1030)
+    st->dt = dt_dev;
     st->mass_sum = 0.0;
     st->mom_sum[0] = st->mom_sum[1] = st->mom_sum[2] = 0.0;
     // snapshot + reset of the other table: it receives the next P2G
@@ -261,13 +288,19 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
 // the start of each level and of the tail (levels >= 16, placed by a cursor
 // in word 49); cell_count becomes the per-cell cursor.
 constexpr int WL = 16;
+constexpr int SCAN2_SLICES = 8;  // CTAs per tile: each re-scans the tile and fills 32 of its blocks
 __global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide) {
+  if (*S.halt) return;
   __shared__ uint32_t sh[8];
   __shared__ uint32_t boff[TB], ioff[TB];
   const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
   const int ntiles = (nb + TB - 1) / TB;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // (tile, slice) work units: the per-block level tables and items are
+  // latency-bound (dependent loads per block), so a tile's 256 blocks are
+  // spread over SCAN2_SLICES CTAs (4 blocks per warp) instead of one
+  for (int unit = blockIdx.x; unit < ntiles * SCAN2_SLICES; unit += gridDim.x) {
+    const int tile = unit / SCAN2_SLICES, slice = unit % SCAN2_SLICES;
     uint32_t r = tile * TB + threadIdx.x;
     uint32_t tot = r < nb ? S.block_total[r] : 0, it = r < nb ? S.block_items[r] : 0, t1, t2;
     uint32_t e1 = cta_excl_scan(tot, sh, t1);
@@ -275,7 +308,7 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide) {
     boff[threadIdx.x] = e1 + S.tile_sums[4 * tile];
     ioff[threadIdx.x] = e2 + S.tile_sums[4 * tile + 1];
     __syncthreads();
-    for (int b = w; b < TB; b += 8) {
+    for (int b = slice * (TB / SCAN2_SLICES) + w; b < (slice + 1) * (TB / SCAN2_SLICES); b += 8) {
       uint32_t rr = tile * TB + b;
       if (rr >= nb) break;
       uint32_t c0 = S.cell_count[size_t(rr) * 64 + lane], c1 = S.cell_count[size_t(rr) * 64 + 32 + lane];
@@ -331,10 +364,12 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide) {
 // Wide layout: the particle's level s comes from the per-cell cursor, its
 // position from the block's level table (see k_scan2).
 __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm,
-                      int wide) {
+                      int wide, const uint32_t* __restrict__ n_dev) {
   // Storage order is the previous step's sorted order, so equal bins come in
   // runs: one atomic per run of a warp (head lane), ranks within the run from
   // the ballot of run heads.
+  if (*S.halt) return;
+  if (n_dev) n = *n_dev;  // batched steps: positions the previous fused kernel wrote
   const int lane = threadIdx.x & 31;
   const int64_t w_first = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t w_step = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -383,6 +418,7 @@ __global__ void __launch_bounds__(256, DET ? 2 : SMPM_GRID_MINB) k_grid(TableDev
                                                  float4* __restrict__ acc, float4* __restrict__ gv, GridParams gp,
                                                  int record, int bx0, int bx1, unsigned long long* acc_fx,
                                                  float4* __restrict__ gforce) {
+  if (*S.halt) return;
   __shared__ Boundary sbc[8];
   if (threadIdx.x < gp.n_bc && threadIdx.x < 8) sbc[threadIdx.x] = gp.bc[threadIdx.x];
   __syncthreads();
@@ -493,6 +529,7 @@ __global__ void __launch_bounds__(256, DET ? 2 : SMPM_GRID_MINB) k_grid(TableDev
 // box are appended by the fused kernel after them.  The table is empty when
 // this runs, so each key is inserted once and takes its index as rank.
 __global__ void k_dense_insert(TableDev T, int b0, int b1, int b2, int s0, int s1, int s2) {
+  if (*T.halt) return;
   const uint32_t nd = uint32_t(s0) * uint32_t(s1) * uint32_t(s2);
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
     const int i = int(r / uint32_t(s1 * s2)), j = int((r / uint32_t(s2)) % uint32_t(s1)), k = int(r % uint32_t(s2));
@@ -1836,6 +1873,32 @@ __global__ void k_apply_global(const double* rows, int world, DevStats* stNew, f
 // =================================================================== host
 using namespace smpm;
 
+// Per-step record of a batched run (smpm_sim_run): what smpm_sim_sync reads
+// from the two DevStats after a single step.
+struct StepRec {
+  double dt, mass_sum, mom_sum[3];
+  unsigned long long n_active;
+  uint32_t n_owned, n_blocks, n_binned, vmax2_bits;
+};
+constexpr int RUN_RING = 1024;  // steps per batch
+
+__global__ void k_step_record(const uint32_t* halt, uint32_t* count, StepRec* ring, const DevStats* st,
+                              const DevStats* nx) {
+  if (*halt || threadIdx.x) return;
+  const uint32_t i = count[0];
+  StepRec r;
+  r.dt = st->dt;
+  r.mass_sum = st->mass_sum;
+  for (int a = 0; a < 3; ++a) r.mom_sum[a] = st->mom_sum[a];
+  r.n_active = st->n_active;
+  r.n_owned = st->n_owned;
+  r.n_blocks = st->n_blocks;
+  r.n_binned = st->n_binned;
+  r.vmax2_bits = nx->vmax2_bits;
+  ring[i] = r;
+  count[0] = i + 1;
+}
+
 struct smpm_sim {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -1908,6 +1971,13 @@ struct smpm_sim {
   // fast (non-deterministic) mode runs k_g2p2g_f32: block ranges of RCAP
   // particles (the wide placement), fp32 arena, no fixed-point scales
   bool f32 = false;
+  // batched steps (smpm_sim_run): halt word, per-step records (device ring +
+  // pinned copy)
+  bool batching = false;
+  uint32_t* dhalt = nullptr;   // [4]: halt code, records written
+  StepRec* dring = nullptr;    // [RUN_RING]
+  StepRec* hring = nullptr;    // pinned [RUN_RING]
+  uint32_t* hhalt = nullptr;   // pinned [4]
   // download scratch (inverse permutation, two staging chunks), kept once made
   uint32_t* dl_inv = nullptr;
   double* dl_dst[2] = {nullptr, nullptr};
@@ -2051,6 +2121,7 @@ int alloc_grid(smpm_sim* s) {
     DA(T.hv.counter, 4);
     T.hv.overflow = T.hv.counter + 1;
     T.done = T.hv.counter + 2;
+    T.halt = s->dhalt;
     DA(T.hv.active_keys, cb);
     DA(T.hv.slot_of_rank, cb);
     T.hv.mask = uint32_t(s->n_slots - 1);
@@ -2129,6 +2200,7 @@ StepParams step_params(smpm_sim* s, double dt) {
   sp.bx1 = s->bx1;
   sp.wide = s->nkk == 3;
   sp.cap = s->f32 ? RCAP : WIDE_CAP;
+  sp.batch = s->batching ? 1 : 0;
   return sp;
 }
 
@@ -2144,11 +2216,12 @@ int scan_and_bin(smpm_sim* s, int Sx, double dt) {
   StepParams sp = step_params(s, dt);
   s->nkk_scan = s->nkk;  // the items just built are laid out for this kernel variant
   CK(cudaMemsetAsync(s->tab[Sx].tile_sums, 0, 16 * size_t(s->max_tiles), s->stream));
-  int grid = std::max(1, std::min<int>(s->max_tiles, 148 * 8));
+  int grid = std::max(1, std::min<int>(s->max_tiles * SCAN2_SLICES, 148 * 8));
   k_scan1<<<148 * 4, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp,
                                        s->dnstore);
   k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx], sp.wide);
-  k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm, sp.wide);
+  k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm, sp.wide,
+                                       s->batching ? &s->dstats[1 - Sx].n_binned : nullptr);
   CK(cudaGetLastError());
   return SMPM_OK;
 }
@@ -2685,6 +2758,13 @@ int sim_create_body(const smpm_sim_config* cfg, smpm_sim* s) {
                                         : next_pow2(std::max<uint64_t>(4096, uint64_t(s->cap_p) / 96));
   s->cap_b = uint32_t(std::min<uint64_t>(cb, 1ull << 25));
   s->cap_items = uint32_t(std::min<uint64_t>(uint64_t(s->cap_p) / ISLOTS + s->cap_b + 1024, 0xFFFFFFF0ull));
+  rc = dalloc(s, &s->dhalt, 4);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(s->dhalt, 0, 16, s->stream));
+  rc = dalloc(s, &s->dring, RUN_RING);
+  if (rc) return rc;
+  CK(cudaMallocHost(&s->hring, RUN_RING * sizeof(StepRec)));
+  CK(cudaMallocHost(&s->hhalt, 16));
   rc = alloc_grid(s);
   if (rc) return rc;
   rc = dalloc(s, &s->dstats, 2);
@@ -2751,6 +2831,8 @@ int smpm_sim_destroy(smpm_sim* s) {
   if (s->hxcount) cudaFreeHost(s->hxcount);
   if (s->hnstore) cudaFreeHost(s->hnstore);
   if (s->hgbound) cudaFreeHost(s->hgbound);
+  if (s->hring) cudaFreeHost(s->hring);
+  if (s->hhalt) cudaFreeHost(s->hhalt);
   for (int b = 0; b < 2; ++b)  // the pinned buffers are process-wide
     if (s->pin_ev[b]) cudaEventDestroy(s->pin_ev[b]);
   for (int i = 0; i < 5; ++i)
@@ -2976,6 +3058,142 @@ int smpm_sim_sync(smpm_sim* s, smpm_step_stats* out) {
     s->nstore_pending = false;
   }
   if (out) *out = s->last;
+  return SMPM_OK;
+}
+
+// n steps with one host synchronisation per batch of up to RUN_RING steps
+// (the reference's loop of Simulation.step calls, solver.py:1001-1093, without
+// the per-step host round trip).  The CFL bound and dt validation, the error
+// word and the table-capacity checks that smpm_sim_step/smpm_sim_sync make on
+// the host between steps are made on the device by k_scan1 (halt word); a
+// step that fails one halts the rest of its batch, and the host then handles
+// it exactly as after a single step (error, or grid growth + P2G replay, and
+// the remaining steps).  Each step writes its StepStats record into a device
+// ring copied back once per batch.  Modes that need host decisions between
+// steps (deterministic / fixed-point scales, slab exchange) take the
+// single-step path.
+int smpm_sim_run(smpm_sim* s, int64_t n, double dt, smpm_step_stats* out, int64_t* n_done) {
+  if (!s) return set_err(SMPM_ERR_ARG, "null sim");
+  if (n_done) *n_done = 0;
+  if (n < 0) return set_err(SMPM_ERR_ARG, "negative step count");
+  if (s->n < 1) return set_err(SMPM_ERR_CONFIG, "no particles");
+  CK(cudaSetDevice(s->device));
+  int64_t done = 0;
+  while (done < n) {
+    const bool batchable = s->f32 && !s->acc_fx && !s->ext_bounds && !s->mig_count && !s->nstore_pending &&
+                           !s->gbound_pending && !s->dense;
+    if (!batchable) {
+      int rc = smpm_sim_step(s, dt);
+      if (rc) return rc;
+      rc = smpm_sim_sync(s, out ? out + done : nullptr);
+      if (rc) return rc;
+      ++done;
+      if (n_done) *n_done = done;
+      continue;
+    }
+    if (s->in_flight) {
+      int rc = smpm_sim_sync(s, nullptr);
+      if (rc) return rc;
+    }
+    if (s->pending_err) {
+      s->last.status = s->pending_err;
+      s->last.err_particle = s->pending_particle;
+      return s->pending_err;
+    }
+    if (s->need_prologue) {
+      int rc = run_prologue(s, s->prologue_project ? 1 : 0);
+      if (rc) {
+        s->last.status = rc;
+        s->last.err_particle = s->pending_particle;
+        return rc;
+      }
+      s->prologue_project = false;
+    }
+    const int64_t m = std::min<int64_t>(n - done, RUN_RING);
+    const int S0 = s->S, cur0 = s->cur;
+    CK(cudaMemsetAsync(s->dhalt, 0, 16, s->stream));
+    CK(cudaEventRecord(s->ev[0], s->stream));
+    CK(cudaEventRecord(s->ev[1], s->stream));
+    CK(cudaEventRecord(s->ev[2], s->stream));
+    s->batching = true;
+    const GridParams gp = grid_params(s);
+    auto kg = k_grid<false>;
+    int rc = SMPM_OK;
+    for (int64_t i = 0; i < m && rc == SMPM_OK; ++i) {
+      const int Sx = s->S;
+      rc = scan_and_bin(s, Sx, dt > 0 ? dt : -1.0);
+      if (rc) break;
+      kg<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
+                                         s->gv, gp, s->record, s->bx0, s->bx1, nullptr, s->gforce);
+      rc = launch_fused(s, true, 1);
+      if (rc) break;
+      k_step_record<<<1, 32, 0, s->stream>>>(s->dhalt, s->dhalt + 1, s->dring, s->dstats + Sx, s->dstats + s->S);
+      if (cudaGetLastError() != cudaSuccess) rc = set_err(SMPM_ERR_CUDA, "batched step launch failed");
+    }
+    s->batching = false;
+    CK(cudaEventRecord(s->ev[3], s->stream));
+    CK(cudaMemcpyAsync(s->hhalt, s->dhalt, 16, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(s->hring, s->dring, size_t(m) * sizeof(StepRec), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    if (rc) return rc;
+    const uint32_t code = s->hhalt[0];
+    const int64_t k = std::min<int64_t>(s->hhalt[1], m);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->ev[0], s->ev[3]);
+    // the halted steps changed nothing: the state is the one after step k
+    s->S = S0 ^ int(k & 1);
+    s->cur = cur0 ^ int(k & 1);
+    for (int64_t i = 0; i + 1 < k; ++i) {
+      const StepRec& R = s->hring[i];
+      smpm_step_stats r{};
+      r.dt = R.dt;
+      r.n_active = int64_t(R.n_active);
+      r.n_blocks = int64_t(R.n_owned);
+      r.mass_sum = R.mass_sum;
+      for (int a = 0; a < 3; ++a) r.mom_sum[a] = R.mom_sum[a];
+      s->vmax = std::sqrt(double(__uint_as_float_host(R.vmax2_bits)));
+      r.vmax = s->vmax;
+      r.ms_fused = r.ms_total = ms / float(k);
+      s->n_store = R.n_binned;
+      s->step_count += 1;
+      s->t += R.dt;
+      r.step = s->step_count;
+      r.t = s->t;
+      r.status = SMPM_OK;
+      s->last = r;
+      if (out) out[done + i] = r;
+    }
+    if (k > 0) {
+      // the last completed step goes through smpm_sim_sync: stats, the
+      // last-step grid view, and the checks of its outputs (error word, table
+      // capacity) exactly as for a single step
+      CK(cudaMemcpyAsync(s->hstats, s->dstats, 2 * sizeof(DevStats), cudaMemcpyDeviceToHost, s->stream));
+      CK(cudaMemcpyAsync(s->herr, s->derr, 8, cudaMemcpyDeviceToHost, s->stream));
+      CK(cudaMemcpyAsync(s->hcount, s->tab[s->S].hv.counter, 8, cudaMemcpyDeviceToHost, s->stream));
+      s->in_flight = true;
+      smpm_step_stats r{};
+      rc = smpm_sim_sync(s, &r);
+      if (rc) return rc;
+      r.ms_map = r.ms_grid = 0.f;
+      r.ms_fused = r.ms_total = ms / float(k);
+      s->last = r;
+      if (out) out[done + k - 1] = r;
+    }
+    done += k;
+    if (n_done) *n_done = done;
+    if (k < m) {
+      if (code == HALT_DT) {
+        const double bound = s->cfl * s->h / (s->wave_speed + s->vmax);
+        s->last.status = SMPM_ERR_DT_BOUND;
+        s->last.dt = dt;
+        s->last.vmax = bound;
+        return set_err(SMPM_ERR_DT_BOUND, "timestep exceeds the stability bound");
+      }
+      if (code != HALT_ERR && code != HALT_OVERFLOW) return set_err(SMPM_ERR_CUDA, "batched step halted without a cause");
+      // HALT_ERR / HALT_OVERFLOW: smpm_sim_sync recorded the pending error or
+      // the grid growth + replay; the next batch raises or replays
+    }
+  }
   return SMPM_OK;
 }
 

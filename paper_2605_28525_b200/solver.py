@@ -654,6 +654,60 @@ class Simulation:
             raise KeyRangeError("particle stencil block outside packable coordinate range")
         _lib.check(rc, "step")
 
+    def _stats(self, st, step, t):
+        times = {p: 0.0 for p in PHASES}
+        times["map_build"] = st.ms_map * 1e-3
+        times["grid_update"] = st.ms_grid * 1e-3
+        times["g2p"] = st.ms_fused * 1e-3
+        times["metrics"] = 0.0
+        return StepStats(step=step, t=t, dt=st.dt, n_active=int(st.n_active),
+                         n_allocated=int(st.n_blocks) * 64, times=times,
+                         mass_sum=float(st.mass_sum) if self.record_conservation else None,
+                         mom_sum=np.array(st.mom_sum[:]) if self.record_conservation else None)
+
+    def run(self, n_steps, dt=None):
+        """Advance ``n_steps`` explicit steps; returns their StepStats.
+
+        Same steps as ``n_steps`` calls of :meth:`step` (the reference's
+        loop, S/bench.py:216-226) without a host round trip per step: the
+        CFL bound, dt validation, error and grid-capacity checks run on the
+        device and the stats come back once per batch of up to 1024 steps
+        (``smpm_sim_run``).  An error is raised after the steps before it
+        completed (``step_count`` and ``last_stats`` include them)."""
+        import ctypes
+
+        n_steps = int(n_steps)
+        if n_steps < 0:
+            raise ConfigError(f"n_steps must be >= 0, got {n_steps}")
+        self._sync_host_edits()
+        cfg = self.config
+        if dt is None:
+            dt = cfg.dt
+        if dt is not None:
+            dt = float(dt)
+            if not dt > 0.0:
+                raise SimulationError(f"timestep must be positive, got {dt}")
+        if n_steps == 0:
+            return []
+        lib = _lib.load()
+        arr = (_lib.StepStatsC * n_steps)()
+        done = ctypes.c_int64(0)
+        rc = lib.smpm_sim_run(self._h, n_steps, -1.0 if dt is None else dt, arr, ctypes.byref(done))
+        out = []
+        for i in range(int(done.value)):
+            self.t += arr[i].dt
+            self.step_count += 1
+            out.append(self._stats(arr[i], self.step_count, self.t))
+        if out:
+            self.last_stats = out[-1]
+            self._fresh = False
+            self._fp = None
+            if self._mirror:
+                self._refresh_host()
+        if rc:
+            self._raise_status(rc, dt)
+        return out
+
     def step(self, dt=None):
         """Advance one explicit step; returns its StepStats (solver.py:1001-1093)."""
         import ctypes
@@ -675,15 +729,7 @@ class Simulation:
         _lib.check(lib.smpm_sim_sync(self._h, ctypes.byref(st)), "sync")
         self.t += st.dt
         self.step_count += 1
-        times = {p: 0.0 for p in PHASES}
-        times["map_build"] = st.ms_map * 1e-3
-        times["grid_update"] = st.ms_grid * 1e-3
-        times["g2p"] = st.ms_fused * 1e-3
-        times["metrics"] = 0.0
-        stats = StepStats(step=self.step_count, t=self.t, dt=st.dt, n_active=int(st.n_active),
-                          n_allocated=int(st.n_blocks) * 64, times=times,
-                          mass_sum=float(st.mass_sum) if self.record_conservation else None,
-                          mom_sum=np.array(st.mom_sum[:]) if self.record_conservation else None)
+        stats = self._stats(st, self.step_count, self.t)
         self.last_stats = stats
         self._fresh = False
         self._fp = None
