@@ -38,9 +38,8 @@ def line_of(pat):
     return next(i for i, l in enumerate(src, 1) if pat in l)
 
 
-b = [line_of("// [B1]"), line_of("// [B2]"), line_of("// [B3]"), line_of("// [B4]"), line_of("// [B5]")]
-regions = [("prime", 1, b[0]), ("A", b[0] + 1, b[1]), ("S1", b[1] + 1, b[2]), ("S2", b[2] + 1, b[3]),
-           ("S3", b[3] + 1, b[4]), ("F", b[4] + 1, len(src))]
+b = [line_of("// [B1]"), line_of("// [B2]"), line_of("// [B3]")]
+regions = [("prime", 1, b[0]), ("A", b[0] + 1, b[1]), ("S", b[1] + 1, b[2]), ("F", b[2] + 1, len(src))]
 acc = collections.defaultdict(lambda: [0, 0])
 region = "pre"
 ts = sum(x[2] for x in rws)
