@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
   for (int i = tid; i < A.n_mat && i < 8; i += CTA) sm.mats[i] = A.mats[i];
   const uint32_t n_items = A.stB->n_items;
   const double dt = GATHER ? A.stB->dt : 0.0;
-  const float ih = float(A.inv_h);
-  const float hf_ = float(A.h);
+  const float ih = A.ihf;
+  const float hf_ = A.hf;
   uint32_t vmax2_local = 0;
   {
     int* zh = &sm.ahi[0][0];
@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
         const uint32_t cc = sm.tcell[t - oi * nt];
         const int a0 = int(cc / 36), a1 = int((cc / 6) % 6), a2 = int(cc % 6);
         // x weight of offset oi as a function of dx: t = dx - xc, w = wa + wb t^2, g = wg t
-        const float xc = oi == 0 ? 1.5f : (oi == 1 ? 1.0f : 0.5f);
-        const float wa = oi == 1 ? 0.75f : 0.0f, wb = oi == 1 ? -1.0f : 0.5f, wg = oi == 1 ? -2.0f : 1.0f;
+        const float4 xw = A.xw[oi];
+        const float xc = xw.x, wa = xw.y, wb = xw.z, wg = xw.w;
         const float oih = float(oi) * hf_;
         // node (oi, j, k) accumulators: k = 0, 1 packed per field; k = 2
         // packed over fields: (m, p2), (p0, p1), (f0, f1), f2

@@ -607,6 +607,8 @@ struct FusedArgs {
   const Material* mats;
   int n_mat;
   double h, inv_h;
+  float hf, ihf;              // fp32 h and 1/h (kernel-parameter operands, no per-use conversion)
+  float4 xw[3];               // per x offset i: (xc, wa, wb, wg) of w = wa + wb (d - xc)^2, g = wg (d - xc)
   const DevStats* stB;
   DevStats* stS;
   const uint32_t* scale_src;  // contribution bounds (m, p, f) the fixed-point scales derive from
@@ -2167,6 +2169,11 @@ FusedArgs fused_args(smpm_sim* s, int B, int dstbuf, int project) {
   A.n_mat = s->n_mat;
   A.h = s->h;
   A.inv_h = s->inv_h;
+  A.hf = float(s->h);
+  A.ihf = float(s->inv_h);
+  A.xw[0] = make_float4(1.5f, 0.0f, 0.5f, 1.0f);
+  A.xw[1] = make_float4(1.0f, 0.75f, -1.0f, -2.0f);
+  A.xw[2] = make_float4(0.5f, 0.0f, 0.5f, 1.0f);
   A.stB = s->dstats + B;
   A.stS = s->dstats + (1 - B);
   A.err = s->derr;
