@@ -500,11 +500,18 @@ __device__ inline bool hencky_dp_body(float H[9], const Material& mat, bool proj
   // of the strains (~1e-8 absolute).  For ||X|| <= 0.01 (the common case of a
   // resting or slowly deforming granular body) three terms truncate at
   // 0.01^4/4 = 2.5e-9: two matrix products fewer.
+  // Two terms for ||X|| <= 1e-3 (truncation X^3/3 <= 3.3e-10).  The term
+  // count is voted per warp in MODE 2 (one path per warp).
   float P[6], T[6];
-#ifndef SMPM_SHORT_LOG
-#define SMPM_SHORT_LOG 1
-#endif
-  if (SMPM_SHORT_LOG && nx <= 0.01f) {
+  uint32_t ltier = nx <= 1e-3f ? 0u : (nx <= 0.01f ? 1u : 2u);
+  if (MODE == 2) ltier = __reduce_max_sync(__activemask(), ltier);
+  if (ltier == 0) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) P[q] = -0.5f * X[q];
+    P[0] += 1.f;
+    P[1] += 1.f;
+    P[2] += 1.f;
+  } else if (ltier == 1) {
 #pragma unroll
     for (int q = 0; q < 6; ++q) P[q] = -X[q] * (1.f / 3.f);
     P[0] += 0.5f;
@@ -566,28 +573,37 @@ __device__ inline bool hencky_dp_body(float H[9], const Material& mat, bool proj
     }
   }
   if (changed && project) {
-    // H' = H + E (I + H), E = exp(D) - I = D (1 + D/2 (1 + D/3 (1 + D/4))), D = eps' - eps
+    // H' = H + E (I + H), E = exp(D) - I = D (1 + D/2 (1 + D/3 (1 + D/4))), D = eps' - eps;
+    // two terms for ||D|| <= 1e-3 (truncation D^3/6 <= 1.7e-10), three for
+    // ||D|| <= 1e-2 (D^4/24 <= 4.2e-10), voted per warp in MODE 2
     float D[6], E[6], Q[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      D[q] = e2[q] - eps[q];
-      Q[q] = D[q] * 0.25f;
+    for (int q = 0; q < 6; ++q) D[q] = e2[q] - eps[q];
+    const float dn = fmaxf(fabsf(D[0]) + fabsf(D[3]) + fabsf(D[4]),
+                           fmaxf(fabsf(D[3]) + fabsf(D[1]) + fabsf(D[5]), fabsf(D[4]) + fabsf(D[5]) + fabsf(D[2])));
+    uint32_t et = dn <= 1e-3f ? 0u : (dn <= 1e-2f ? 1u : 2u);
+    if (MODE == 2) et = __reduce_max_sync(__activemask(), et);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) Q[q] = D[q] * (et == 2 ? 0.25f : (et == 1 ? (1.f / 3.f) : 0.5f));
+    Q[0] += 1.f;
+    Q[1] += 1.f;
+    Q[2] += 1.f;
+    if (et == 2) {
+      sym_mul(D, Q, T);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) Q[q] = T[q] * (1.f / 3.f);
+      Q[0] += 1.f;
+      Q[1] += 1.f;
+      Q[2] += 1.f;
     }
-    Q[0] += 1.f;
-    Q[1] += 1.f;
-    Q[2] += 1.f;
-    sym_mul(D, Q, T);
+    if (et >= 1) {
+      sym_mul(D, Q, T);
 #pragma unroll
-    for (int q = 0; q < 6; ++q) Q[q] = T[q] * (1.f / 3.f);
-    Q[0] += 1.f;
-    Q[1] += 1.f;
-    Q[2] += 1.f;
-    sym_mul(D, Q, T);
-#pragma unroll
-    for (int q = 0; q < 6; ++q) Q[q] = T[q] * 0.5f;
-    Q[0] += 1.f;
-    Q[1] += 1.f;
-    Q[2] += 1.f;
+      for (int q = 0; q < 6; ++q) Q[q] = T[q] * 0.5f;
+      Q[0] += 1.f;
+      Q[1] += 1.f;
+      Q[2] += 1.f;
+    }
     sym_mul(D, Q, E);
     // full 3x3 of E (symmetric)
     const float Ef[9] = {E[0], E[3], E[4], E[3], E[1], E[5], E[4], E[5], E[2]};
