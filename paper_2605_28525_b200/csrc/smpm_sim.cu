@@ -1412,6 +1412,7 @@ __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g(FusedArgs A) {
 }
 
 #include "smpm_fused_f32.cuh"
+#include "smpm_fused_ws.cuh"
 
 // ------------------------------------------------------- state transfer
 // Upload: reference layout f64 -> 128-byte records (x f64, rest f32).
@@ -1947,6 +1948,10 @@ struct smpm_sim {
   int pending_err = 0;
   int64_t pending_particle = 0;
   int persist_blocks = 0;
+  // k_g2p2g_f32 as the warp-specialised k_g2p2g_ws (one 512-thread CTA per SM),
+  // chosen when the scene fills the SMs (SMPM_FUSED=ws|cta pins it)
+  int ws_blocks = 0;
+  int ws_mode = -1;  // -1 auto, 0 off, 1 on
   cudaEvent_t ev[5] = {};
   smpm_step_stats last{};
   double vmax = 0;        // max |v| of the current particles (CFL bound input)
@@ -2153,6 +2158,7 @@ int alloc_grid(smpm_sim* s) {
 
 size_t smem_bytes() { return sizeof(FusedSmem); }
 size_t smem_bytes_f32() { return sizeof(FusedSmemF); }
+size_t smem_bytes_ws() { return sizeof(FusedSmemWS); }
 
 FusedArgs fused_args(smpm_sim* s, int B, int dstbuf, int project) {
   FusedArgs A;
@@ -2240,7 +2246,13 @@ template <bool GATHER>
 void launch_g2p2g(smpm_sim* s, const FusedArgs& A, size_t smem) {
   const bool wide = s->nkk_scan == 3;
   if (s->f32) {
-    k_g2p2g_f32<GATHER, 1><<<s->persist_blocks, CTA, smem_bytes_f32(), s->stream>>>(A);
+    // auto: the warp-specialised kernel once there are several items per SM
+    // (its per-item latency is the same, its throughput higher)
+    const bool ws = s->ws_mode > 0 || (s->ws_mode < 0 && s->n_store >= int64_t(RCAP) * 4 * s->ws_blocks);
+    if (ws)
+      k_g2p2g_ws<GATHER, 1><<<s->ws_blocks, WS_CTA, smem_bytes_ws(), s->stream>>>(A);
+    else
+      k_g2p2g_f32<GATHER, 1><<<s->persist_blocks, CTA, smem_bytes_f32(), s->stream>>>(A);
     return;
   }
   if (s->acc_fx) {
@@ -2815,11 +2827,19 @@ int sim_create_body(const smpm_sim_config* cfg, smpm_sim* s) {
     CK(cudaFuncSetAttribute(k_g2p2g_f32<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
     CK(cudaFuncSetAttribute(k_g2p2g_f32<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g_f32<true, 1>, CTA, smem_bytes_f32()));
+    const int sw = int(smem_bytes_ws());
+    CK(cudaFuncSetAttribute(k_g2p2g_ws<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sw));
+    CK(cudaFuncSetAttribute(k_g2p2g_ws<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sw));
+    int occ_ws = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ws, k_g2p2g_ws<true, 1>, WS_CTA, smem_bytes_ws()));
+    s->ws_blocks = std::max(1, occ_ws);
+    if (const char* fz = std::getenv("SMPM_FUSED")) s->ws_mode = !std::strcmp(fz, "ws") ? 1 : (!std::strcmp(fz, "cta") ? 0 : -1);
   } else {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<true, 2, 0>, CTA, smem_bytes()));
   }
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
   s->persist_blocks = std::max(1, occ) * sms;
+  s->ws_blocks *= sms;
   for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&s->ev[i]));
   return SMPM_OK;
 }
