@@ -263,6 +263,10 @@ def ours(args):
         run_leg = {"ms_per_step": ms_run / args.steps, "value": n * args.steps / (ms_run * 1e-3),
                    "scope": "Simulation.run(K): same steps, one host sync per batch (smpm_sim_run)"}
     # ---- roofline of the dominant kernel (fused g2p->stress->p2g), this rank
+    dbg0 = (ctypes.c_int64 * 24)()
+    _lib.check(_lib.load().smpm_sim_debug_stats(inner._h, dbg0), "debug stats")
+    fused_name = {0: "k_g2p2g_f32", 1: "k_g2p2g_ws", 2: "k_g2p2g (int32)", 3: "k_g2p2g (int64 det)"}.get(
+        int(dbg0[23]), "k_g2p2g")
     peak, peak_kind = measured_peaks()
     ph = _phase_means(hist)
     n_alloc_local = float(np.mean(nalloc)) if world == 1 else float(np.mean(nalloc)) / world
@@ -300,7 +304,7 @@ def ours(args):
         lms = s0.elapsed_time(s1)
         lph = _phase_means(lh)
         lbytes = 204.0 * n_local + 40.0 * float(np.mean(lalloc))
-        dbg = (ctypes.c_int64 * 23)()
+        dbg = (ctypes.c_int64 * 24)()
         _lib.check(_lib.load().smpm_sim_debug_stats(inner._h, dbg), "debug stats")
         late = {"after_steps": args.late_steps, "sim_time_s": round(inner.t, 4), "steps": args.steps,
                 "ms_per_step": lms / args.steps, "value": n * args.steps / (lms * 1e-3),
@@ -394,7 +398,7 @@ def ours(args):
         "parallelism": f"slab{world}" if world > 1 else "single",
         "mean_allocated_nodes": float(np.mean(nalloc)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_g2p2g (G2P+F+return map+next P2G)",
+                     "traffic": traffic, "kernel": f"{fused_name} (G2P+F+return map+next P2G)",
                      "peak_kind": peak_kind, "kernel_ms": ph["fused"], "atomics": atomics,
                      "step_frac": step_bytes / world / (ms / args.steps * 1e-3) / 1e9 / peak},
         "phases_ms": {"map_build(scan+bin)": ph["map"], "grid_update": ph["grid"], "fused": ph["fused"]},

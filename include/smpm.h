@@ -254,7 +254,9 @@ int smpm_sim_p2g_bounds(smpm_sim* s, int set, float* bounds);
  * n_owned) x 2, then S, n_store, need_prologue, migrants_sent, and the bin
  * census of the stored particles (holes, in-flight migrants, overflowed,
  * unresolved, binned), then the work-item layout of the last scan and of the
- * next step (0 narrow, 1 wide): 23 int64. */
+ * next step (0 narrow, 1 wide), then the fused kernel of the last launch
+ * (0 k_g2p2g_f32, 1 k_g2p2g_ws, 2 k_g2p2g int32 fixed point, 3 k_g2p2g
+ * int64 deterministic): 24 int64. */
 int smpm_sim_debug_stats(smpm_sim* s, int64_t* out);
 /* Bytes per block record of smpm_sim_exchange_pack (2064 fp32, 4112 deterministic). */
 int64_t smpm_sim_exchange_record_bytes(const smpm_sim* s);

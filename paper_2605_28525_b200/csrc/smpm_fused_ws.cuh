@@ -26,6 +26,15 @@
 constexpr int WS_CTA = 512;  // threads per CTA: 256 consumer (S) + 256 producer (A)
 constexpr int WA = 256;      // threads per role
 constexpr int WB_FULL = 1, WB_EMPTY = 3, WB_A = 5, WB_S = 6;
+#ifndef SMPM_WS_PERM
+#define SMPM_WS_PERM 0  // 1: unconditional perm loads of the next item's sources (A/B)
+#endif
+#ifndef SMPM_WS_RA
+#define SMPM_WS_RA 0  // setmaxnreg of the producer warps (0: the launch's 128)
+#endif
+#ifndef SMPM_WS_RS
+#define SMPM_WS_RS 0  // setmaxnreg of the consumer warps (RA + RS <= 256)
+#endif
 
 struct __align__(16) FusedSmemWS {
   float4 stage[2][GCH][WA];          // records of the A thread's two particles (G2P chunks)
@@ -146,11 +155,18 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
     // particles (their records are fetched as this item's are consumed)
     if (GATHER && nxt.r() != BAD_KEY) prefetch_arena(sm.garena[b ^ 1], A, nxt, t, WA);
     slots(nxt, pn, int((k + 1) & 3));
+    // (unconditional loads: nothing waits for them before the first prefetch)
     uint32_t src1[2];
+    bool has1[2];
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk) {
       const uint32_t p = sm.posr[pn][kk][t];
-      src1[kk] = p != NOPOS ? A.perm[p] : NOPOS;
+      has1[kk] = p != NOPOS;
+#if SMPM_WS_PERM
+      src1[kk] = A.perm[has1[kk] ? p : 0u];
+#else
+      src1[kk] = has1[kk] ? A.perm[p] : 0u;
+#endif
     }
     float bmx[3] = {0.f, 0.f, 0.f};
 
@@ -391,7 +407,7 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
       }
       sm.binr[b][kk][t] = valid ? binv : BIN_SKIP;
       // this slot's stage is consumed (or was empty): the record of item k+1
-      if (GATHER && src1[kk] != NOPOS) {
+      if (GATHER && has1[kk]) {
         const float4* g = A.src.rec + size_t(src1[kk]) * 8;
 #pragma unroll
         for (int q = 0; q < GCH; ++q) cp_async16(&sm.stage[kk][q][t], &g[q]);
@@ -611,9 +627,12 @@ __global__ void __launch_bounds__(WS_CTA, 1) k_g2p2g_ws(FusedArgs A) {
     if (tid < 2) sm.ntask[tid] = 0;
   }
   __syncthreads();
-  if (tid >= WA)
+  if (tid >= WA) {
+    if (SMPM_WS_RA) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(SMPM_WS_RA));
     ws_produce<GATHER, CV>(A, sm, tid - WA, A.stB->n_items);
-  else
+  } else {
+    if (SMPM_WS_RS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SMPM_WS_RS));
     ws_consume(A, sm, tid);
+  }
   if (blockIdx.x == 0 && tid < 3) A.stS->scale_inv[tid] = 0.f;  // fp32-grade arena: no global fixed-point scales
 }

@@ -1952,6 +1952,7 @@ struct smpm_sim {
   // chosen when the scene fills the SMs (SMPM_FUSED=ws|cta pins it)
   int ws_blocks = 0;
   int ws_mode = -1;  // -1 auto, 0 off, 1 on
+  int last_kernel = -1;  // 0 f32, 1 ws, 2 int32 fixed point, 3 int64 deterministic
   cudaEvent_t ev[5] = {};
   smpm_step_stats last{};
   double vmax = 0;        // max |v| of the current particles (CFL bound input)
@@ -2253,8 +2254,10 @@ void launch_g2p2g(smpm_sim* s, const FusedArgs& A, size_t smem) {
       k_g2p2g_ws<GATHER, 1><<<s->ws_blocks, WS_CTA, smem_bytes_ws(), s->stream>>>(A);
     else
       k_g2p2g_f32<GATHER, 1><<<s->persist_blocks, CTA, smem_bytes_f32(), s->stream>>>(A);
+    s->last_kernel = ws ? 1 : 0;
     return;
   }
+  s->last_kernel = s->acc_fx ? 3 : 2;
   if (s->acc_fx) {
     if (wide)
       k_g2p2g<GATHER, 3, 2><<<s->persist_blocks, CTA, smem, s->stream>>>(A);
@@ -2821,7 +2824,7 @@ int sim_create_body(const smpm_sim_config* cfg, smpm_sim* s) {
     CK(cudaFuncSetAttribute(k_g2p2g<true, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
     CK(cudaFuncSetAttribute(k_g2p2g<false, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
   }
-  int occ = 0, sms = 0;
+  int occ = 0, sms = 0, ws_cap = 0;
   if (s->f32) {
     const int sb = int(smem_bytes_f32());
     CK(cudaFuncSetAttribute(k_g2p2g_f32<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
@@ -2834,12 +2837,15 @@ int sim_create_body(const smpm_sim_config* cfg, smpm_sim* s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ws, k_g2p2g_ws<true, 1>, WS_CTA, smem_bytes_ws()));
     s->ws_blocks = std::max(1, occ_ws);
     if (const char* fz = std::getenv("SMPM_FUSED")) s->ws_mode = !std::strcmp(fz, "ws") ? 1 : (!std::strcmp(fz, "cta") ? 0 : -1);
+    ws_cap = 0;
+    if (const char* wb = std::getenv("SMPM_WS_BLOCKS")) ws_cap = std::atoi(wb);  // sanitizer runs: many items per CTA
   } else {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<true, 2, 0>, CTA, smem_bytes()));
   }
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
   s->persist_blocks = std::max(1, occ) * sms;
   s->ws_blocks *= sms;
+  if (ws_cap > 0) s->ws_blocks = std::min(s->ws_blocks, ws_cap);
   for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&s->ev[i]));
   return SMPM_OK;
 }
@@ -3429,6 +3435,7 @@ int smpm_sim_debug_stats(smpm_sim* s, int64_t* out) {
   for (int k = 0; k < 5; ++k) out[16 + k] = c[k];
   out[21] = s->nkk_scan == 3 ? 1 : 0;  // work-item layout of the last scan (1 wide)
   out[22] = s->nkk == 3 ? 1 : 0;       // layout chosen for the next step
+  out[23] = s->last_kernel;            // fused kernel of the last launch
   return SMPM_OK;
 }
 

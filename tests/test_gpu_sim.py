@@ -164,7 +164,7 @@ def test_item_layouts_are_bitwise_identical_in_deterministic_mode(monkeypatch, m
 def _layout(sim):
     import ctypes
     from paper_2605_28525_b200 import _lib
-    out = (ctypes.c_int64 * 23)()
+    out = (ctypes.c_int64 * 24)()
     _lib.check(_lib.load().smpm_sim_debug_stats(sim._h, out), "debug stats")
     return int(out[21])
 

@@ -18,7 +18,7 @@ hist = []
 def item_stats(tag):
     import ctypes
     from paper_2605_28525_b200 import _lib
-    out = (ctypes.c_int64 * 23)()
+    out = (ctypes.c_int64 * 24)()
     _lib.check(_lib.load().smpm_sim_debug_stats(sim._h, out), "debug stats")
     o = list(out)
     print(f"{tag}: blocks {o[0]} items {o[2]} ({o[2] / max(o[0], 1):.2f}/block) binned {o[1]} | bins: bad {o[16]} "
