@@ -332,6 +332,73 @@ __device__ __forceinline__ void sym_mul(const float a[6], const float b[6], floa
   c[5] = a[3] * b[4] + a[1] * b[5] + a[5] * b[2];
 }
 
+#ifndef SMPM_PADE
+#define SMPM_PADE 1  // moderate-strain log by Pade approximants (0: the atanh series)
+#endif
+// inverse of a symmetric 3x3 (xx, yy, zz, xy, xz, yz)
+__device__ __forceinline__ void sym_inv(const float d[6], float o[6]) {
+  const float c00 = d[1] * d[2] - d[5] * d[5], c11 = d[0] * d[2] - d[4] * d[4], c22 = d[0] * d[1] - d[3] * d[3];
+  const float c01 = d[4] * d[5] - d[3] * d[2], c02 = d[3] * d[5] - d[4] * d[1], c12 = d[3] * d[4] - d[0] * d[5];
+  const float id = 1.0f / (d[0] * c00 + d[3] * c01 + d[4] * c02);
+  o[0] = c00 * id;
+  o[1] = c11 * id;
+  o[2] = c22 * id;
+  o[3] = c01 * id;
+  o[4] = c02 * id;
+  o[5] = c12 * id;
+}
+// eps = atanh(Z) = Z R(W), W = Z^2, with R(w) = atanh(sqrt w)/sqrt w replaced
+// by its [n/n] Pade approximant P_n(W) Q_n(W)^-1.  On the spectrum (w <= 0.36,
+// |z| <= 0.6: the caller's bound) the truncation of eps is <= 4e-9 for
+// n = 2, 3, 4 up to w = 0.09, 0.23, 0.36 (tools/pade_atanh.py); Q_n's
+// eigenvalues stay >= 0.47.  All factors are polynomials of Z, so they commute
+// and every product is symmetric.  The order is chosen from the Frobenius
+// norm (>= spectral radius), per warp when VOTE.
+template <int N>
+__device__ __forceinline__ void atanh_pade_n(const float Z[6], const float W[6], float eps[6]) {
+  constexpr float P[3][5] = {{1.f, -7.f / 9.f, 64.f / 945.f, 0.f, 0.f},
+                             {1.f, -50.f / 39.f, 283.f / 715.f, -256.f / 15015.f, 0.f},
+                             {1.f, -91.f / 51.f, 83.f / 85.f, -1289.f / 7735.f, 16384.f / 3828825.f}};
+  constexpr float Q[3][5] = {{1.f, -10.f / 9.f, 5.f / 21.f, 0.f, 0.f},
+                             {1.f, -21.f / 13.f, 105.f / 143.f, -35.f / 429.f, 0.f},
+                             {1.f, -36.f / 17.f, 126.f / 85.f, -84.f / 221.f, 63.f / 2431.f}};
+  float Pn[6], Qn[6], Wk[6], Tm[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const float dg = q < 3 ? 1.f : 0.f;
+    Pn[q] = fmaf(P[N - 2][1], W[q], dg);
+    Qn[q] = fmaf(Q[N - 2][1], W[q], dg);
+    Wk[q] = W[q];
+  }
+#pragma unroll
+  for (int j = 2; j <= N; ++j) {
+    sym_mul(Wk, W, Tm);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      Wk[q] = Tm[q];
+      Pn[q] = fmaf(P[N - 2][j], Tm[q], Pn[q]);
+      Qn[q] = fmaf(Q[N - 2][j], Tm[q], Qn[q]);
+    }
+  }
+  float Qi[6];
+  sym_inv(Qn, Qi);
+  sym_mul(Z, Pn, Tm);
+  sym_mul(Tm, Qi, eps);
+}
+template <bool VOTE>
+__device__ __forceinline__ void atanh_pade(const float Z[6], float r2, float eps[6]) {
+  float W[6];
+  sym_mul(Z, Z, W);
+  uint32_t ord = r2 <= 0.09f ? 2u : (r2 <= 0.23f ? 3u : 4u);
+  if (VOTE) ord = __reduce_max_sync(__activemask(), ord);
+  if (ord == 2)
+    atanh_pade_n<2>(Z, W, eps);
+  else if (ord == 3)
+    atanh_pade_n<3>(Z, W, eps);
+  else
+    atanh_pade_n<4>(Z, W, eps);
+}
+
 // Same model for moderate elastic strain (spectral radius of
 // Z = (B - I)(B + I)^-1 up to 0.6, i.e. principal stretches^2 in [0.25, 4]),
 // still without an eigen-decomposition.  eps = 1/2 log B = atanh(Z) =
@@ -341,6 +408,7 @@ __device__ __forceinline__ void sym_mul(const float a[6], const float b[6], floa
 // Frobenius norm (>= spectral radius) so the truncation stays below 1e-8;
 // the loop index is warp-uniform while any lane is still summing.  Returns 0
 // when Z is too large (caller takes the Jacobi path), -1 on a degenerate F.
+template <bool VOTE>
 __device__ inline int hencky_dp_mid(float H[9], const float X[6], const Material& mat, bool project, float tau[6],
                                     float& J) {
   // M = B + I = 2I + X, Z = X M^-1 (X and M^-1 commute)
@@ -355,8 +423,11 @@ __device__ inline int hencky_dp_mid(float H[9], const float X[6], const Material
   sym_mul(X, Mi, Z);
   const float r2 = Z[0] * Z[0] + Z[1] * Z[1] + Z[2] * Z[2] + 2.f * (Z[3] * Z[3] + Z[4] * Z[4] + Z[5] * Z[5]);
   if (!(r2 <= 0.36f)) return 0;
-  // eps = Z + Z^3/3 + Z^5/5 + ...; truncation after Z^(2K+1) <= r^(2K+3)/((2K+3)(1-r^2))
   float W[6], T[6], eps[6];
+#if SMPM_PADE
+  atanh_pade<VOTE>(Z, r2, eps);
+#else
+  // eps = Z + Z^3/3 + Z^5/5 + ...; truncation after Z^(2K+1) <= r^(2K+3)/((2K+3)(1-r^2))
   sym_mul(Z, Z, W);
 #pragma unroll
   for (int q = 0; q < 6; ++q) {
@@ -378,6 +449,7 @@ __device__ inline int hencky_dp_mid(float H[9], const float X[6], const Material
     }
     bound *= r2;
   }
+#endif
   float e2[6];
 #pragma unroll
   for (int q = 0; q < 6; ++q) e2[q] = eps[q];
@@ -491,7 +563,7 @@ __device__ inline bool hencky_dp_body(float H[9], const Material& mat, bool proj
   bool use_mid = MODE != 0 && big;
   if (MODE == 2) use_mid = __any_sync(__activemask(), big);
   if (use_mid) {
-    const int mid = hencky_dp_mid(H, X, mat, project, tau, J);
+    const int mid = hencky_dp_mid<MODE == 2>(H, X, mat, project, tau, J);
     if (mid != 0) return mid > 0;
   }
   if (big) return hencky_dp_eig(H, mat, project, tau, J);

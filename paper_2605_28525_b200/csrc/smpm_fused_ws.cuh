@@ -14,9 +14,15 @@
 //     are prefetched (cp.async) into the thread's own stage slots as soon as
 //     item i's are consumed, the velocity arena of item i+1 at item i's start.
 //   warps 0..7 (S, consumer): bar.sync(FULL[b]); scatter tasks (cell, x
-//     offset) of warps 0..6 into the split fixed-point arena while warp 7
-//     inserts the touched blocks; flush, bins and cell counts; buffer b is
-//     handed back with bar.arrive(EMPTY[b]).
+//     offset) on all 256 lanes into the split fixed-point arena (one round up
+//     to 85 non-empty cells: the flowing regime's halo cells), the first warp
+//     done with its tasks inserts the touched blocks; flush, bins and cell
+//     counts; buffer b is handed back with bar.arrive(EMPTY[b]).
+//
+// Tried and dropped (A/B on C4, tools/gpu_ab_ws.sh): next-step keys, lists
+// and counts on the consumer (fp64 position in a 7-chunk stash): +0.5 ms
+// early, +0.5 ms late -- the consumer's pre-pass sits on its critical path;
+// setmaxnreg 144/112 and 136/120 splits: within noise.
 //
 // A works on item i+1 while S scatters item i, so neither waits for the other
 // at a CTA-wide barrier; the only intra-role barrier is the A-side one that
@@ -26,6 +32,10 @@
 constexpr int WS_CTA = 512;  // threads per CTA: 256 consumer (S) + 256 producer (A)
 constexpr int WA = 256;      // threads per role
 constexpr int WB_FULL = 1, WB_EMPTY = 3, WB_A = 5, WB_S = 6;
+#ifndef SMPM_WS_TW
+#define SMPM_WS_TW 8  // consumer warps running scatter tasks (7: warp 7 only inserts)
+#endif
+constexpr int WS_TW = SMPM_WS_TW;
 #ifndef SMPM_WS_PERM
 #define SMPM_WS_PERM 0  // 1: unconditional perm loads of the next item's sources (A/B)
 #endif
@@ -48,6 +58,7 @@ struct __align__(16) FusedSmemWS {
   uint16_t nxt[2][2 * WA];           // list links
   uint16_t tcell[2][NACELL];         // non-empty base cells
   uint32_t ntask[2];
+  uint32_t iclaim;                   // insert duty of the current item taken (WS_TW = 8)
   uint32_t bnd[2][3];                // item maxima of the contribution bounds (m, p, f)
   int blk[2][4];                     // block coordinates of the buffer's item; [3] != 0: no item (end)
   uint32_t rank[27];                 // next-table ranks of the item's touched blocks (S only)
@@ -438,9 +449,9 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
     float Sg[3], iS[3];
 #pragma unroll
     for (int f = 0; f < 3; ++f) item_scale(sm.bnd[b][f], Sg[f], iS[f]);
-    if (warp < TASK_WARPS) {
+    if (warp < WS_TW) {
 #pragma unroll 1
-      for (uint32_t tk = t; tk < 3 * nt; tk += TASK_WARPS * 32) {
+      for (uint32_t tk = t; tk < 3 * nt; tk += WS_TW * 32) {
         const uint32_t oi = tk / nt;
         const uint32_t cc = sm.tcell[b][tk - oi * nt];
         const int a0 = int(cc / 36), a1 = int((cc / 6) % 6), a2 = int(cc % 6);
@@ -460,7 +471,7 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
         uint32_t sl = sm.head[b][cc];
 #pragma unroll 1
         while (sl != LEND) {
-          const float4* sp = &sm.stash[b][sl >> 8][0][sl & (WA - 1)];
+          const float4* sp = &sm.stash[b][sl >> 8][0][sl & (WA - 1)];  // chunks 0..5
           sl = sm.nxt[b][sl];
           const float4 s0 = sp[0], s1 = sp[WA], s2 = sp[2 * WA], s3 = sp[3 * WA], s4 = sp[4 * WA], s5 = sp[5 * WA];
           const float tx = s0.x - xc;
@@ -529,9 +540,15 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
           atomicAdd(&sm.kc[d2], 1u);
         }
       }
-    } else {
-      // warp 7: the blocks the item's stencils touch, inserted into the next
-      // step's table
+    }
+    bool ins = warp >= WS_TW;  // WS_TW = 7: warp 7 inserts; 8: the first warp done with its tasks
+    if (WS_TW == 8) {
+      uint32_t cl = 0;
+      if (lane == 0) cl = atomicExch(&sm.iclaim, 1u);
+      ins = __shfl_sync(0xffffffffu, cl, 0) == 0u;
+    }
+    if (ins) {
+      // the blocks the item's stencils touch, inserted into the next step's table
       uint32_t tm = 0;
       for (uint32_t e = lane; e < nt; e += 32) {
         const uint32_t cc = sm.tcell[b][e];
@@ -580,6 +597,7 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
       sm.head[b][nd] = LEND;
     }
     if (t == 0) sm.ntask[b] = 0;
+    if (t == 1) sm.iclaim = 0;
     if (t < 3) sm.bnd[b][t] = 0;
     for (int nd = t; nd < 512; nd += WA) {
       const int i = nd >> 6, j = (nd >> 3) & 7, kz = nd & 7;
@@ -625,6 +643,7 @@ __global__ void __launch_bounds__(WS_CTA, 1) k_g2p2g_ws(FusedArgs A) {
     for (int i = tid; i < 2 * NACELL; i += WS_CTA) (&sm.head[0][0])[i] = LEND;
     if (tid < 6) (&sm.bnd[0][0])[tid] = 0;
     if (tid < 2) sm.ntask[tid] = 0;
+    if (tid == 2) sm.iclaim = 0;
   }
   __syncthreads();
   if (tid >= WA) {
