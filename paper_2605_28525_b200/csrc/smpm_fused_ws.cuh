@@ -36,9 +36,6 @@ constexpr int WB_FULL = 1, WB_EMPTY = 3, WB_A = 5, WB_S = 6;
 #define SMPM_WS_TW 8  // consumer warps running scatter tasks (7: warp 7 only inserts)
 #endif
 constexpr int WS_TW = SMPM_WS_TW;
-#ifndef SMPM_WS_PERM
-#define SMPM_WS_PERM 0  // 1: unconditional perm loads of the next item's sources (A/B)
-#endif
 #ifndef SMPM_WS_RA
 #define SMPM_WS_RA 0  // setmaxnreg of the producer warps (0: the launch's 128)
 #endif
@@ -97,6 +94,24 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
       sm.posr[pr][kk][t] = j < n ? start + first + j : NOPOS;
     }
   };
+  // this thread's velocity-arena node (t < 216): neighbour slot, arena
+  // address and node within the neighbour block, fixed for the launch
+  int pa_slot = 0, pa_dst = 0, pa_loc = 0;
+  if (t < 216) {
+    const int i = t / 36, j = (t / 6) % 6, k = t % 6;
+    pa_slot = ((i >> 2) << 2) | ((j >> 2) << 1) | (k >> 2);
+    pa_dst = gaddr(i, j, k);
+    pa_loc = ((i & 3) << 4) | ((j & 3) << 2) | (k & 3);
+  }
+  auto prefetch_ga = [&](float4* ga, const ItemInfo& inf) {
+    if (t < 216) {
+      const uint32_t gr = inf.nbr[pa_slot];
+      if (gr < A.B.hv.cap_blocks)
+        cp_async16(ga + pa_dst, &A.gv[size_t(gr) * 64 + pa_loc]);
+      else
+        ga[pa_dst] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
   // ---- prime: metadata of items 0..2, neighbour ranks and ranges of items
   // 0 and 1, records and velocity arena of item 0
   if (t < 3) fetch_item(A, n_items, t, sm.info[t], false);
@@ -126,7 +141,7 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
         for (int q = 0; q < GCH; ++q) cp_async16(&sm.stage[kk][q][t], &g[q]);
       }
     }
-    if (sm.info[0].r() != BAD_KEY) prefetch_arena(sm.garena[0], A, sm.info[0], t, WA);
+    if (sm.info[0].r() != BAD_KEY) prefetch_ga(sm.garena[0], sm.info[0]);
   }
   cp_async_commit();
 
@@ -164,21 +179,12 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
     }
     // velocity arena of item k+1; sorted positions and source indices of its
     // particles (their records are fetched as this item's are consumed)
-    if (GATHER && nxt.r() != BAD_KEY) prefetch_arena(sm.garena[b ^ 1], A, nxt, t, WA);
+    if (GATHER && nxt.r() != BAD_KEY) prefetch_ga(sm.garena[b ^ 1], nxt);
     slots(nxt, pn, int((k + 1) & 3));
-    // (unconditional loads: nothing waits for them before the first prefetch)
-    uint32_t src1[2];
-    bool has1[2];
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-      const uint32_t p = sm.posr[pn][kk][t];
-      has1[kk] = p != NOPOS;
-#if SMPM_WS_PERM
-      src1[kk] = A.perm[has1[kk] ? p : 0u];
-#else
-      src1[kk] = has1[kk] ? A.perm[p] : 0u;
-#endif
-    }
+    // (two scalars, not a kk-indexed array: the kk loop is not unrolled and an
+    // indexed array would live in local memory)
+    const uint32_t pn0 = sm.posr[pn][0][t], pn1 = sm.posr[pn][1][t];
+    const uint32_t srcA = pn0 != NOPOS ? A.perm[pn0] : 0u, srcB = pn1 != NOPOS ? A.perm[pn1] : 0u;
     float bmx[3] = {0.f, 0.f, 0.f};
 
 #pragma unroll 1
@@ -418,8 +424,8 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
       }
       sm.binr[b][kk][t] = valid ? binv : BIN_SKIP;
       // this slot's stage is consumed (or was empty): the record of item k+1
-      if (GATHER && has1[kk]) {
-        const float4* g = A.src.rec + size_t(src1[kk]) * 8;
+      if (GATHER && (kk ? pn1 : pn0) != NOPOS) {
+        const float4* g = A.src.rec + size_t(kk ? srcB : srcA) * 8;
 #pragma unroll
         for (int q = 0; q < GCH; ++q) cp_async16(&sm.stage[kk][q][t], &g[q]);
       }
