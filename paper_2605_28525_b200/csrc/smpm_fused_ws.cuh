@@ -61,6 +61,7 @@ struct __align__(16) FusedSmemWS {
   uint32_t rank[27];                 // next-table ranks of the item's touched blocks (S only)
   uint32_t posr[3][2][WA];           // sorted positions of the A thread's particles, ring by item % 3
   uint32_t binr[2][2][WA];           // bins awaiting the item's ranks
+  uint32_t srcr[2][WA];              // storage indices of the next item's particles
   uint32_t icnt[4][2];               // (particle count, first sorted position), ring by item % 4
   ItemInfo info[4];                  // item metadata ring (A only)
   Material mats[8];
@@ -161,6 +162,18 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
     const ItemInfo& nxt = sm.info[(k + 1) & 3];
     int B0, B1, B2;
     cur.block(B0, B1, B2);
+    // sorted positions of item k+1's particles; their source indices land in
+    // smem by cp.async, committed as the oldest group of the item (a register
+    // load would be waited for at the head of the non-unrolled kk loop)
+    slots(nxt, pn, int((k + 1) & 3));
+    if (GATHER) {
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint32_t p = sm.posr[pn][kk][t];
+        if (p != NOPOS) cp_async4(&sm.srcr[kk][t], A.perm + p);
+      }
+      cp_async_commit();
+    }
     if (t == 0) {
       sm.blk[b][0] = B0;
       sm.blk[b][1] = B1;
@@ -177,20 +190,27 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
         if (t == 35) cp_async4(&sm.icnt[(k + 2) & 3][1], A.B.cell_off + size_t(nn.r()) * 64 + 32);
       }
     }
-    // velocity arena of item k+1; sorted positions and source indices of its
-    // particles (their records are fetched as this item's are consumed)
+    // velocity arena of item k+1 (its records are fetched as this item's are consumed)
     if (GATHER && nxt.r() != BAD_KEY) prefetch_ga(sm.garena[b ^ 1], nxt);
-    slots(nxt, pn, int((k + 1) & 3));
-    // (two scalars, not a kk-indexed array: the kk loop is not unrolled and an
-    // indexed array would live in local memory)
-    const uint32_t pn0 = sm.posr[pn][0][t], pn1 = sm.posr[pn][1][t];
-    const uint32_t srcA = pn0 != NOPOS ? A.perm[pn0] : 0u, srcB = pn1 != NOPOS ? A.perm[pn1] : 0u;
+    cp_async_commit();
+    // record of item k+1 into stage slot kk (called once the slot's record of
+    // item k has been consumed, or at once for an empty slot)
+    auto prefetch_rec = [&](int kk) {
+      if (GATHER && sm.posr[pn][kk][t] != NOPOS) {
+        if (kk == 0) asm volatile("cp.async.wait_group 1;" ::: "memory");  // the source indices (oldest group)
+        const float4* g = A.src.rec + size_t(sm.srcr[kk][t]) * 8;
+#pragma unroll
+        for (int q = 0; q < GCH; ++q) cp_async16(&sm.stage[kk][q][t], &g[q]);
+        cp_async_commit();
+      }
+    };
     float bmx[3] = {0.f, 0.f, 0.f};
 
 #pragma unroll 1
     for (int kk = 0; kk < 2; ++kk) {
       const uint32_t pos = sm.posr[pc][kk][t];
       const bool valid = pos != NOPOS;
+      if (!valid) prefetch_rec(kk);
       float4 c0, c1, c2, c3, c4, c5, c6, c7;
       if (valid) {
         if (GATHER) {
@@ -312,6 +332,7 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
                   F[3 * i + j] + (A9[3 * i + j] + (A9[3 * i] * F[j] + A9[3 * i + 1] * F[3 + j] + A9[3 * i + 2] * F[6 + j]));
 #pragma unroll
           for (int q = 0; q < 9; ++q) F[q] = Fn[q];
+          prefetch_rec(kk);  // x, m, V0, H and pid|mat of the stage slot are consumed
           xn[0] = __dadd_rn(xn[0], __dmul_rn(dt, double(vn[0])));
           xn[1] = __dadd_rn(xn[1], __dmul_rn(dt, double(vn[1])));
           xn[2] = __dadd_rn(xn[2], __dmul_rn(dt, double(vn[2])));
@@ -424,11 +445,6 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
       }
       sm.binr[b][kk][t] = valid ? binv : BIN_SKIP;
       // this slot's stage is consumed (or was empty): the record of item k+1
-      if (GATHER && (kk ? pn1 : pn0) != NOPOS) {
-        const float4* g = A.src.rec + size_t(kk ? srcB : srcA) * 8;
-#pragma unroll
-        for (int q = 0; q < GCH; ++q) cp_async16(&sm.stage[kk][q][t], &g[q]);
-      }
     }
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
