@@ -29,6 +29,12 @@
 // publishes the landed velocity arena.  Named barriers: FULL[b] = 1 + b,
 // EMPTY[b] = 3 + b (512 threads: 256 arrive, 256 sync), A-side 5 (256).
 
+#ifndef SMPM_WS_STATS
+#define SMPM_WS_STATS 0
+#endif
+#if SMPM_WS_STATS
+__device__ uint32_t ws_stat_nt[128], ws_stat_lm[64], ws_stat_lmax_item;
+#endif
 constexpr int WS_CTA = 512;  // threads per CTA: 256 consumer (S) + 256 producer (A)
 constexpr int WA = 256;      // threads per role
 constexpr int WB_FULL = 1, WB_EMPTY = 3, WB_A = 5, WB_S = 6;
@@ -468,6 +474,27 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
     if (sm.blk[b][3]) break;
     const int B0 = sm.blk[b][0], B1 = sm.blk[b][1], B2 = sm.blk[b][2];
     const uint32_t nt = sm.ntask[b];
+#if SMPM_WS_STATS
+    // diagnostics (timing builds only): per item, the task count and the
+    // longest cell list, histogrammed by CTA 0 and printed at the end
+    if (blockIdx.x == 0) {
+      uint32_t lmax = 0;
+      for (uint32_t e = t; e < nt; e += WA) {
+        uint32_t n = 0;
+        for (uint32_t sl = sm.head[b][sm.tcell[b][e]]; sl != LEND; sl = sm.nxt[b][sl]) ++n;
+        lmax = max(lmax, n);
+      }
+      lmax = __reduce_max_sync(0xffffffffu, lmax);
+      if (lane == 0) atomicMax(&ws_stat_lmax_item, lmax);
+      nbar_sync(WB_S, WA);
+      if (t == 0) {
+        atomicAdd(&ws_stat_nt[min(nt, 127u)], 1u);
+        atomicAdd(&ws_stat_lm[min(ws_stat_lmax_item, 63u)], 1u);
+        ws_stat_lmax_item = 0;
+      }
+      nbar_sync(WB_S, WA);
+    }
+#endif
     float Sg[3], iS[3];
 #pragma unroll
     for (int f = 0; f < 3; ++f) item_scale(sm.bnd[b][f], Sg[f], iS[f]);
@@ -676,4 +703,15 @@ __global__ void __launch_bounds__(WS_CTA, 1) k_g2p2g_ws(FusedArgs A) {
     ws_consume(A, sm, tid);
   }
   if (blockIdx.x == 0 && tid < 3) A.stS->scale_inv[tid] = 0.f;  // fp32-grade arena: no global fixed-point scales
+#if SMPM_WS_STATS
+  if (blockIdx.x == 0 && tid == 0) {
+    printf("WSSTATS nt");
+    for (int i = 0; i < 128; ++i) printf(" %u", ws_stat_nt[i]);
+    printf("\nWSSTATS lmax");
+    for (int i = 0; i < 64; ++i) printf(" %u", ws_stat_lm[i]);
+    printf("\n");
+    for (int i = 0; i < 128; ++i) ws_stat_nt[i] = 0;
+    for (int i = 0; i < 64; ++i) ws_stat_lm[i] = 0;
+  }
+#endif
 }
