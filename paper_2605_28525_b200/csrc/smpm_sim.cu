@@ -363,6 +363,9 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide) {
 // starts at the scanned cell offset and ends at offset + count).
 // Wide layout: the particle's level s comes from the per-cell cursor, its
 // position from the block's level table (see k_scan2).
+#ifndef SMPM_KB_U
+#define SMPM_KB_U 4  // 32-particle tiles per warp and pass in k_bin
+#endif
 __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm,
                       int wide, const uint32_t* __restrict__ n_dev) {
   // Storage order is the previous step's sorted order, so equal bins come in
@@ -371,7 +374,7 @@ __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, u
   // time, each phase (bin loads, cursor atomics, level-table lookups) issued
   // for all of them before the next: KB_U independent dependency chains (a
   // single chain per warp left the kernel latency-bound at 1.6 TB/s).
-  constexpr int KB_U = 4;
+  constexpr int KB_U = SMPM_KB_U;
   if (*S.halt) return;
   if (n_dev) n = *n_dev;  // batched steps: positions the previous fused kernel wrote
   const int lane = threadIdx.x & 31;
