@@ -288,8 +288,8 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
 // the start of each level and of the tail (levels >= 16, placed by a cursor
 // in word 49); cell_count becomes the per-cell cursor.
 constexpr int WL = 16;
-constexpr int SCAN2_SLICES = 8;  // CTAs per tile: each re-scans the tile and fills 32 of its blocks
-__global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide) {
+constexpr int SCAN2_SLICES = 8;  // CTAs per tile: each re-scans the tile and fills 32 of its blocks (32 for a single-tile grid)
+__global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide, int slices) {
   if (*S.halt) return;
   __shared__ uint32_t sh[8];
   __shared__ uint32_t boff[TB], ioff[TB];
@@ -299,8 +299,8 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide) {
   // (tile, slice) work units: the per-block level tables and items are
   // latency-bound (dependent loads per block), so a tile's 256 blocks are
   // spread over SCAN2_SLICES CTAs (4 blocks per warp) instead of one
-  for (int unit = blockIdx.x; unit < ntiles * SCAN2_SLICES; unit += gridDim.x) {
-    const int tile = unit / SCAN2_SLICES, slice = unit % SCAN2_SLICES;
+  for (int unit = blockIdx.x; unit < ntiles * slices; unit += gridDim.x) {
+    const int tile = unit / slices, slice = unit % slices;
     uint32_t r = tile * TB + threadIdx.x;
     uint32_t tot = r < nb ? S.block_total[r] : 0, it = r < nb ? S.block_items[r] : 0, t1, t2;
     uint32_t e1 = cta_excl_scan(tot, sh, t1);
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide) {
     boff[threadIdx.x] = e1 + S.tile_sums[4 * tile];
     ioff[threadIdx.x] = e2 + S.tile_sums[4 * tile + 1];
     __syncthreads();
-    for (int b = slice * (TB / SCAN2_SLICES) + w; b < (slice + 1) * (TB / SCAN2_SLICES); b += 8) {
+    for (int b = slice * (TB / slices) + w; b < (slice + 1) * (TB / slices); b += 8) {
       uint32_t rr = tile * TB + b;
       if (rr >= nb) break;
       uint32_t c0 = S.cell_count[size_t(rr) * 64 + lane], c1 = S.cell_count[size_t(rr) * 64 + 32 + lane];
@@ -2250,15 +2250,29 @@ int dense_insert(smpm_sim* s, int t) {
   return SMPM_OK;
 }
 
+// CTAs for a kernel that handles per_cta blocks per CTA: from twice the last
+// synced block count (the whole capacity before the first sync), at most maxg
+uint64_t nb_estimate(const smpm_sim* s) {
+  return s->last_nb ? std::min<uint64_t>(uint64_t(s->last_nb) * 2 + 64, s->cap_b) : s->cap_b;
+}
+int small_grid(const smpm_sim* s, int per_cta, int maxg) {
+  const uint64_t nb = nb_estimate(s);
+  return int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(maxg), (nb + per_cta - 1) / per_cta)));
+}
+
 int scan_and_bin(smpm_sim* s, int Sx, double dt) {
   StepParams sp = step_params(s, dt);
   s->nkk_scan = s->nkk;  // the items just built are laid out for this kernel variant
   CK(cudaMemsetAsync(s->tab[Sx].tile_sums, 0, 16 * size_t(s->max_tiles), s->stream));
-  int grid = std::max(1, std::min<int>(s->max_tiles * SCAN2_SLICES, 148 * 8));
-  k_scan1<<<148 * 4, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp,
+  // grids sized from the last synced block / particle counts (2x margin; the
+  // kernels stride over any excess): a small scene launches tens of CTAs,
+  // not a thousand mostly idle ones
+  const int slices = nb_estimate(s) <= uint64_t(16 * TB) ? 32 : SCAN2_SLICES;
+  int grid = std::max(1, std::min<int>(s->max_tiles * slices, 148 * 8));
+  k_scan1<<<small_grid(s, 8, 148 * 4), 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp,
                                        s->dnstore);
-  k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx], sp.wide);
-  k_bin<<<148 * 8, 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm, sp.wide,
+  k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx], sp.wide, slices);
+  k_bin<<<std::max(1, std::min<int>(148 * 8, int((int64_t(s->n_store) * 2 + 1023) / 1024))), 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm, sp.wide,
                                        s->batching ? &s->dstats[1 - Sx].n_binned : nullptr);
   CK(cudaGetLastError());
   return SMPM_OK;
@@ -3030,7 +3044,7 @@ int smpm_sim_step(smpm_sim* s, double dt) {
   CK(cudaEventRecord(s->ev[1], s->stream));
   GridParams gp = grid_params(s);
   auto kg = s->acc_fx ? k_grid<true> : k_grid<false>;
-  kg<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
+  kg<<<small_grid(s, 16, 148 * 8), 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
                                          s->gv, gp, s->record, s->bx0, s->bx1, s->acc_fx, s->gforce);
   CK(cudaGetLastError());
   rc = dense_insert(s, 1 - Sx);
@@ -3180,7 +3194,7 @@ int smpm_sim_run(smpm_sim* s, int64_t n, double dt, smpm_step_stats* out, int64_
       const int Sx = s->S;
       rc = scan_and_bin(s, Sx, dt > 0 ? dt : -1.0);
       if (rc) break;
-      kg<<<148 * 8, 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
+      kg<<<small_grid(s, 16, 148 * 8), 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
                                          s->gv, gp, s->record, s->bx0, s->bx1, nullptr, s->gforce);
       rc = launch_fused(s, true, 1);
       if (rc) break;
