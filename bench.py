@@ -414,7 +414,7 @@ def ours(args):
                  "download_s": round(t_end - t_st, 4)}
     stats_bytes = args.steps * (2 * 128 + 24)
     h2d = n * 128  # host-packed 128-B particle records (smpm_sim_set_particles, include/smpm.h)
-    d2h = n * 48   # x, v (fp64) of every particle
+    d2h = n * 36   # x (fp64) and v (fp32, as stored; widened on the host) of every particle
     e2e_value = n * args.steps / e2e_s
     sim2 = None
     # ---- cold e2e: the same public-API sequence in a fresh process (cold

@@ -1510,6 +1510,7 @@ __global__ void k_gather_local(Particles P, const uint32_t* __restrict__ idx, in
     v[3 * i + 2] = c5.x;
   }
 }
+template <bool VF32>  // v as fp32 (the host download widens it) or fp64 (smpm_sim_snapshot_xv)
 __global__ void k_gather_xv(Particles P, const uint32_t* __restrict__ inv, int64_t lo, int64_t c,
                             double* __restrict__ out) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < c; i += int64_t(gridDim.x) * blockDim.x) {
@@ -1518,9 +1519,16 @@ __global__ void k_gather_xv(Particles P, const uint32_t* __restrict__ inv, int64
     out[3 * i] = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
     out[3 * i + 1] = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
     out[3 * i + 2] = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
-    out[3 * c + 3 * i] = c4.z;
-    out[3 * c + 3 * i + 1] = c4.w;
-    out[3 * c + 3 * i + 2] = c5.x;
+    if (VF32) {  // v as stored (fp32, 12 B instead of 24 on the PCIe link)
+      float* vo = reinterpret_cast<float*>(out + 3 * c);
+      vo[3 * i] = c4.z;
+      vo[3 * i + 1] = c4.w;
+      vo[3 * i + 2] = c5.x;
+    } else {
+      out[3 * c + 3 * i] = c4.z;
+      out[3 * c + 3 * i + 1] = c4.w;
+      out[3 * c + 3 * i + 2] = c5.x;
+    }
   }
 }
 
@@ -2655,9 +2663,9 @@ int download_xv_host(smpm_sim* s, double* x, double* v) {
   auto issue = [&](int64_t k) -> int {
     const int b = int(k & 1);
     const int64_t lo = k * CH, c = std::min(CH, n - lo);
-    k_gather_xv<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], inv, lo, c, dst[b]);
+    k_gather_xv<true><<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], inv, lo, c, dst[b]);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(s->pin[b], dst[b], size_t(c) * 48, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(s->pin[b], dst[b], size_t(c) * 36, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaEventRecord(s->pin_ev[b], s->stream));
     return SMPM_OK;
   };
@@ -2674,9 +2682,11 @@ int download_xv_host(smpm_sim* s, double* x, double* v) {
     CK(cudaEventSynchronize(s->pin_ev[b]));
     const auto t1 = clk::now();
     const double* src = reinterpret_cast<const double*>(s->pin[b]);
+    const float* srcv = reinterpret_cast<const float*>(src + 3 * c);
     parallel_range(s->host_threads, c, [&](int64_t a, int64_t e) {
       if (x) std::memcpy(x + 3 * (lo + a), src + 3 * a, size_t(e - a) * 24);
-      if (v) std::memcpy(v + 3 * (lo + a), src + 3 * c + 3 * a, size_t(e - a) * 24);
+      if (v)
+        for (int64_t q = 3 * a; q < 3 * e; ++q) v[3 * lo + q] = double(srcv[q]);
     });
     t_wait += std::chrono::duration<double>(t1 - t0).count();
     t_copy += std::chrono::duration<double>(clk::now() - t1).count();
@@ -3329,7 +3339,7 @@ int smpm_sim_snapshot_xv(smpm_sim* s, double* out) {
   const int64_t n = s->n;
   CK(cudaMemsetAsync(s->dl_inv, 0, size_t(n) * 4, s->stream));
   k_invperm<<<148 * 8, 256, 0, s->stream>>>(s->state[s->cur], s->n_store, s->pid_base, n, s->bin, s->dl_inv);
-  k_gather_xv<<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], s->dl_inv, 0, n, out);
+  k_gather_xv<false><<<148 * 4, 256, 0, s->stream>>>(s->state[s->cur], s->dl_inv, 0, n, out);
   CK(cudaGetLastError());
   return SMPM_OK;
 }
