@@ -34,10 +34,19 @@
 #endif
 #if SMPM_WS_STATS
 __device__ uint32_t ws_stat_nt[128], ws_stat_lm[64], ws_stat_lmax_item;
+// clock64 phase sums of CTA 0: producer (warp 8 lane 0) wait-empty, wait-data,
+// work; consumer (per warp, lane 0) wait-full, tasks, wait-consumers, flush
+__device__ unsigned long long ws_clk_a[3], ws_clk_s[8][4];
+#define WS_CLK(v) long long v = clock64()
+#else
+#define WS_CLK(v)
 #endif
 constexpr int WS_CTA = 512;  // threads per CTA: 256 consumer (S) + 256 producer (A)
 constexpr int WA = 256;      // threads per role
 constexpr int WB_FULL = 1, WB_EMPTY = 3, WB_A = 5, WB_S = 6;
+#ifndef SMPM_WS_SHIGH
+#define SMPM_WS_SHIGH 0  // 1: consumer on warps 8..15 (A/B: same early, +0.2 ms late)
+#endif
 #ifndef SMPM_WS_TW
 #define SMPM_WS_TW 8  // consumer warps running scatter tasks (7: warp 7 only inserts)
 #endif
@@ -155,9 +164,12 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
   for (uint32_t k = 0;; ++k) {
     const int b = int(k & 1u);
     const int pc = int(k % 3u), pn = int((k + 1) % 3u);
+    WS_CLK(ta0);
     if (k >= 2) nbar_sync(WB_EMPTY + b, WS_CTA);  // S is done with item k - 2 (buffer b, posr ring slot pn)
+    WS_CLK(ta1);
     cp_async_wait_all();
     nbar_sync(WB_A, WA);  // records, velocity arena and metadata of item k landed; item k-1 fully read
+    WS_CLK(ta2);
     const ItemInfo& cur = sm.info[k & 3];
     if (cur.r() == BAD_KEY) {
       if (t == 0) sm.blk[b][3] = 1;
@@ -458,6 +470,14 @@ __device__ __forceinline__ void ws_produce(const FusedArgs& A, FusedSmemWS& sm, 
       if (lane == 0 && bb) atomicMax(&sm.bnd[b][f], bb);
     }
     cp_async_commit();
+#if SMPM_WS_STATS
+    if (blockIdx.x == 0 && t == 0) {
+      const long long ta3 = clock64();
+      ws_clk_a[0] += ta1 - ta0;
+      ws_clk_a[1] += ta2 - ta1;
+      ws_clk_a[2] += ta3 - ta2;
+    }
+#endif
     nbar_arrive(WB_FULL + b, WS_CTA);  // buffer b (stash, lists, counts, bins, bounds) holds item k
   }
   vmax2_local = __reduce_max_sync(0xffffffffu, vmax2_local);
@@ -470,11 +490,13 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
   const float hf_ = A.hf;
   for (uint32_t k = 0;; ++k) {
     const int b = int(k & 1u);
+    WS_CLK(ts0);
     nbar_sync(WB_FULL + b, WS_CTA);
+    WS_CLK(ts1);
     if (sm.blk[b][3]) break;
     const int B0 = sm.blk[b][0], B1 = sm.blk[b][1], B2 = sm.blk[b][2];
     const uint32_t nt = sm.ntask[b];
-#if SMPM_WS_STATS
+#if SMPM_WS_STATS >= 2
     // diagnostics (timing builds only): per item, the task count and the
     // longest cell list, histogrammed by CTA 0 and printed at the end
     if (blockIdx.x == 0) {
@@ -590,6 +612,7 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
         }
       }
     }
+    WS_CLK(ts2);
     bool ins = warp >= WS_TW;  // WS_TW = 7: warp 7 inserts; 8: the first warp done with its tasks
     if (WS_TW == 8) {
       uint32_t cl = 0;
@@ -617,7 +640,9 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
         sm.rank[lane] = rk;
       }
     }
+    WS_CLK(ts3);
     nbar_sync(WB_S, WA);  // arena and ranks of item k complete
+    WS_CLK(ts4);
     // bins of item k
     const int pc = int(k % 3u);
 #pragma unroll
@@ -669,6 +694,15 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
       red_v4(&A.acc[2 * node], vals[0], vals[1], vals[2], vals[3]);
       red_v4(&A.acc[2 * node + 1], vals[4], vals[5], vals[6], float(K));  // .w > 0: active node (n_active)
     }
+#if SMPM_WS_STATS
+    if (blockIdx.x == 0 && lane == 0) {
+      const long long ts5 = clock64();
+      ws_clk_s[warp][0] += ts1 - ts0;  // wait for a full buffer
+      ws_clk_s[warp][1] += ts2 - ts1 + ts3 - ts2;  // tasks (+ inserts)
+      ws_clk_s[warp][2] += ts4 - ts3;  // wait for the other consumers
+      ws_clk_s[warp][3] += ts5 - ts4;  // bins, counts, flush
+    }
+#endif
     nbar_arrive(WB_EMPTY + b, WS_CTA);  // buffer b is free for item k+2
   }
 }
@@ -695,12 +729,16 @@ __global__ void __launch_bounds__(WS_CTA, 1) k_g2p2g_ws(FusedArgs A) {
     if (tid == 2) sm.iclaim = 0;
   }
   __syncthreads();
-  if (tid >= WA) {
+  // the issue arbiter favours high warp ids: the producer takes warps 8..15
+  // (the consumer there measured the same early and 0.2 ms slower late)
+  const bool producer = SMPM_WS_SHIGH ? tid < WA : tid >= WA;
+  const int rt = tid & (WA - 1);
+  if (producer) {
     if (SMPM_WS_RA) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(SMPM_WS_RA));
-    ws_produce<GATHER, CV>(A, sm, tid - WA, A.stB->n_items);
+    ws_produce<GATHER, CV>(A, sm, rt, A.stB->n_items);
   } else {
     if (SMPM_WS_RS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SMPM_WS_RS));
-    ws_consume(A, sm, tid);
+    ws_consume(A, sm, rt);
   }
   if (blockIdx.x == 0 && tid < 3) A.stS->scale_inv[tid] = 0.f;  // fp32-grade arena: no global fixed-point scales
 #if SMPM_WS_STATS
@@ -710,6 +748,13 @@ __global__ void __launch_bounds__(WS_CTA, 1) k_g2p2g_ws(FusedArgs A) {
     printf("\nWSSTATS lmax");
     for (int i = 0; i < 64; ++i) printf(" %u", ws_stat_lm[i]);
     printf("\n");
+    printf("WSCLK A wait_empty %llu wait_data %llu work %llu\n", ws_clk_a[0], ws_clk_a[1], ws_clk_a[2]);
+    for (int w = 0; w < 8; ++w)
+      printf("WSCLK S%d wait_full %llu tasks %llu wait_s %llu flush %llu\n", w, ws_clk_s[w][0], ws_clk_s[w][1],
+             ws_clk_s[w][2], ws_clk_s[w][3]);
+    for (int i = 0; i < 3; ++i) ws_clk_a[i] = 0;
+    for (int w = 0; w < 8; ++w)
+      for (int i = 0; i < 4; ++i) ws_clk_s[w][i] = 0;
     for (int i = 0; i < 128; ++i) ws_stat_nt[i] = 0;
     for (int i = 0; i < 64; ++i) ws_stat_lm[i] = 0;
   }
