@@ -79,6 +79,13 @@ __device__ inline uint32_t hash_insert(const HashView& h, uint64_t key, bool* fr
   uint32_t s = uint32_t(mix64(key)) & h.mask;
   for (uint32_t it = 0; it <= h.mask; ++it) {
     uint64_t stored = ld_volatile_u64(&h.keys[s]);
+    // the slot's rank in the same round trip: a key inserted earlier (the
+    // common case: a block is touched by up to 27 items) returns at once
+    const uint32_t rv = ld_volatile_u32(&h.vals[s]);
+    if (stored == key && rv != EMPTY_VAL) {
+      if (fresh) *fresh = false;
+      return rv;
+    }
     if (stored == EMPTY_KEY) {
       unsigned long long prev = atomicCAS((unsigned long long*)&h.keys[s], (unsigned long long)EMPTY_KEY,
                                           (unsigned long long)key);
