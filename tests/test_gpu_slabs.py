@@ -71,9 +71,15 @@ def _worker(rank, world, port, dts, outdir, det=False, threshold=0.10):
     dist.destroy_process_group()
 
 
-def test_two_slabs_match_single_gpu(tmp_path):
+@pytest.mark.parametrize("kernel", ["auto", "ws"])
+def test_two_slabs_match_single_gpu(tmp_path, monkeypatch, kernel):
+    """kernel "ws": the warp-specialised fused kernel,
+    which this scene is too small to get by default, with its slab-migration
+    path (departing particles copied out by the producer warps)."""
     import torch.multiprocessing as mp
 
+    if kernel != "auto":
+        monkeypatch.setenv("SMPM_FUSED", kernel)  # inherited by the spawned ranks
     ps, cfg, mats, bc = _scene()
     dts, x1, v1 = _dt_sequence(ps, cfg, mats, bc)
     with socket.socket() as s:
