@@ -421,8 +421,10 @@ def ours(args):
     # cudaMalloc of the device state, no buffer cache, fresh pinned buffers)
     e2e_cold = None
     if not distributed and not args.no_cold:
-        _lib.check(_lib.load().smpm_release_cached_memory(), "release cache")
-        torch.cuda.empty_cache()
+        # the parent keeps its device memory while the child runs (the GPU has
+        # room for both): freeing it first would make the child's allocations
+        # wait for the driver to scrub memory another process just released,
+        # which a cold start on an idle GPU does not pay
         r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--e2e-cold-child", "--config", args.config,
                             "--scale", str(args.scale), "--steps", str(args.steps)] +
                            (["--deterministic"] if args.deterministic else []),
