@@ -100,6 +100,8 @@ __device__ __forceinline__ void arena_add_one(int* hi, int* lo, float x, float S
 
 template <bool GATHER, int CV>
 __global__ void __launch_bounds__(CTA, SMPM_MINB) k_g2p2g_f32(FusedArgs A) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smraw[];
   FusedSmemF& sm = *reinterpret_cast<FusedSmemF*>(smraw);
   if (*A.B.halt) return;  // a batched step that must not run (smpm_sim_run)

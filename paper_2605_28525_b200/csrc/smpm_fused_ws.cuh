@@ -709,6 +709,8 @@ __device__ __forceinline__ void ws_consume(const FusedArgs& A, FusedSmemWS& sm, 
 
 template <bool GATHER, int CV>
 __global__ void __launch_bounds__(WS_CTA, 1) k_g2p2g_ws(FusedArgs A) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smraw[];
   FusedSmemWS& sm = *reinterpret_cast<FusedSmemWS*>(smraw);
   if (*A.B.halt) return;  // a batched step that must not run (smpm_sim_run)

@@ -139,6 +139,13 @@ struct StepParams {
 };
 
 // ------------------------------------------------------------------ scan
+// Programmatic dependent launch (batched steps, smpm_sim_run): every kernel of
+// the step chain waits for its predecessor's completion before touching its
+// outputs (a no-op when launched without the attribute) and lets its
+// successor's CTAs be scheduled as soon as all of its own have started.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 constexpr int TB = 256;  // blocks per tile
 
 __device__ inline uint32_t warp_sum(uint32_t v) {
@@ -184,6 +191,8 @@ __device__ inline uint32_t cta_excl_scan(uint32_t v, uint32_t* sh /*[8]*/, uint3
 // scans tile sums and finalises the step scalars.
 __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats* stS, DevStats* stT,
                                                unsigned long long* err, StepParams sp, uint32_t* nstore) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ bool last;
   double dt_dev = sp.dt_req;
   if (sp.batch) {
@@ -290,6 +299,8 @@ __global__ void __launch_bounds__(256) k_scan1(TableDev S, TableDev T, DevStats*
 constexpr int WL = 16;
 constexpr int SCAN2_SLICES = 8;  // CTAs per tile: each re-scans the tile and fills 32 of its blocks (32 for a single-tile grid)
 __global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide, int slices) {
+  pdl_wait();
+  pdl_trigger();
   if (*S.halt) return;
   __shared__ uint32_t sh[8];
   __shared__ uint32_t boff[TB], ioff[TB];
@@ -368,6 +379,8 @@ __global__ void __launch_bounds__(256) k_scan2(TableDev S, int wide, int slices)
 #endif
 __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, uint32_t* __restrict__ perm,
                       int wide, const uint32_t* __restrict__ n_dev) {
+  pdl_wait();
+  pdl_trigger();
   // Storage order is the previous step's sorted order, so equal bins come in
   // runs: one atomic per run of a warp (head lane), ranks within the run from
   // the ballot of run heads.  A warp takes KB_U tiles of 32 particles at a
@@ -377,6 +390,11 @@ __global__ void k_bin(const uint32_t* __restrict__ bin, int64_t n, TableDev S, u
   constexpr int KB_U = SMPM_KB_U;
   if (*S.halt) return;
   if (n_dev) n = *n_dev;  // batched steps: positions the previous fused kernel wrote
+  {  // k_scan2 is done with this table's tile sums: zero them for its next scan
+    const uint32_t nb = min(*S.hv.counter, S.hv.cap_blocks);
+    const uint32_t nz = 4u * ((nb + TB - 1) / TB);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += gridDim.x * blockDim.x) S.tile_sums[i] = 0;
+  }
   const int lane = threadIdx.x & 31;
   const int64_t w_first = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t w_step = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -442,6 +460,8 @@ __global__ void __launch_bounds__(256, DET ? 2 : SMPM_GRID_MINB) k_grid(TableDev
                                                  float4* __restrict__ acc, float4* __restrict__ gv, GridParams gp,
                                                  int record, int bx0, int bx1, unsigned long long* acc_fx,
                                                  float4* __restrict__ gforce) {
+  pdl_wait();
+  pdl_trigger();
   if (*S.halt) return;
   __shared__ Boundary sbc[8];
   if (threadIdx.x < gp.n_bc && threadIdx.x < 8) sbc[threadIdx.x] = gp.bc[threadIdx.x];
@@ -1919,6 +1939,8 @@ constexpr int RUN_RING = 1024;  // steps per batch
 
 __global__ void k_step_record(const uint32_t* halt, uint32_t* count, StepRec* ring, const DevStats* st,
                               const DevStats* nx) {
+  pdl_wait();
+  pdl_trigger();
   if (*halt || threadIdx.x) return;
   const uint32_t i = count[0];
   StepRec r;
@@ -1984,6 +2006,7 @@ struct smpm_sim {
   // chosen when the scene fills the SMs (SMPM_FUSED=ws|cta pins it)
   int ws_blocks = 0;
   int ws_mode = -1;  // -1 auto, 0 off, 1 on
+  bool pdl = true;   // programmatic dependent launch in batched steps (SMPM_PDL=0: off)
   int last_kernel = -1;  // 0 f32, 1 ws, 2 int32 fixed point, 3 int64 deterministic
   cudaEvent_t ev[5] = {};
   smpm_step_stats last{};
@@ -2173,6 +2196,7 @@ int alloc_grid(smpm_sim* s) {
     DA(T.nbr8, size_t(cb) * 8);
     DA(T.items, s->cap_items);
     DA(T.tile_sums, 4 * size_t(s->max_tiles));
+    CK(cudaMemsetAsync(T.tile_sums, 0, 16 * size_t(s->max_tiles), s->stream));  // k_bin re-zeroes after each use
     CK(cudaMemsetAsync(T.hv.keys, 0xFF, s->n_slots * 8, s->stream));
     CK(cudaMemsetAsync(T.hv.vals, 0xFF, s->n_slots * 4, s->stream));
     CK(cudaMemsetAsync(T.hv.counter, 0, 16, s->stream));
@@ -2268,21 +2292,52 @@ int small_grid(const smpm_sim* s, int per_cta, int maxg) {
   return int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(maxg), (nb + per_cta - 1) / per_cta)));
 }
 
+// Launch on the sim's stream; during batched steps with programmatic stream
+// serialisation (the kernels pdl_wait() before reading their predecessors'
+// outputs), so a kernel's CTAs are scheduled while its predecessor drains.
+// Only for scenes below the warp-specialised kernel's size, where the step is
+// a chain of latency-bound kernels (C1: 78 -> 70 us per step); on C4 it
+// measured 0.05 ms slower.
+bool use_pdl(const smpm_sim* s) {
+  return s->batching && s->pdl && s->n_store < int64_t(RCAP) * 4 * s->ws_blocks;
+}
+template <typename... Params, typename... Args>
+cudaError_t launch_k(const smpm_sim* s, void (*k)(Params...), dim3 g, dim3 b, size_t smem, Args... args) {
+  if (!use_pdl(s)) {
+    k<<<g, b, smem, s->stream>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, Params(args)...);
+}
+
 int scan_and_bin(smpm_sim* s, int Sx, double dt) {
   StepParams sp = step_params(s, dt);
   s->nkk_scan = s->nkk;  // the items just built are laid out for this kernel variant
-  CK(cudaMemsetAsync(s->tab[Sx].tile_sums, 0, 16 * size_t(s->max_tiles), s->stream));
+  // tile sums start at zero: from their allocation and from k_bin after each
+  // use (the memset stays for single steps: a batch then needs no non-kernel
+  // node between its steps, so every kernel launches programmatically)
+  if (!use_pdl(s)) CK(cudaMemsetAsync(s->tab[Sx].tile_sums, 0, 16 * size_t(s->max_tiles), s->stream));
   // grids sized from the last synced block / particle counts (2x margin; the
   // kernels stride over any excess): a small scene launches tens of CTAs,
   // not a thousand mostly idle ones
   const int slices = nb_estimate(s) <= uint64_t(16 * TB) ? 32 : SCAN2_SLICES;
   int grid = std::max(1, std::min<int>(s->max_tiles * slices, 148 * 8));
-  k_scan1<<<small_grid(s, 8, 148 * 4), 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->derr, sp,
-                                       s->dnstore);
-  k_scan2<<<grid, 256, 0, s->stream>>>(s->tab[Sx], sp.wide, slices);
-  k_bin<<<std::max(1, std::min<int>(148 * 8, int((int64_t(s->n_store) * 2 + 1023) / 1024))), 256, 0, s->stream>>>(s->bin, s->n_store, s->tab[Sx], s->perm, sp.wide,
-                                       s->batching ? &s->dstats[1 - Sx].n_binned : nullptr);
-  CK(cudaGetLastError());
+  CK(launch_k(s, k_scan1, dim3(small_grid(s, 8, 148 * 4)), dim3(256), 0, s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx,
+              s->dstats + (1 - Sx), s->derr, sp, s->dnstore));
+  CK(launch_k(s, k_scan2, dim3(grid), dim3(256), 0, s->tab[Sx], int(sp.wide), slices));
+  CK(launch_k(s, k_bin, dim3(std::max(1, std::min<int>(148 * 8, int((int64_t(s->n_store) * 2 + 1023) / 1024)))),
+              dim3(256), 0, static_cast<const uint32_t*>(s->bin), int64_t(s->n_store), s->tab[Sx], s->perm,
+              int(sp.wide), static_cast<const uint32_t*>(s->batching ? &s->dstats[1 - Sx].n_binned : nullptr)));
   return SMPM_OK;
 }
 
@@ -2297,9 +2352,9 @@ void launch_g2p2g(smpm_sim* s, const FusedArgs& A, size_t smem) {
     // (its per-item latency is the same, its throughput higher)
     const bool ws = s->ws_mode > 0 || (s->ws_mode < 0 && s->n_store >= int64_t(RCAP) * 4 * s->ws_blocks);
     if (ws)
-      k_g2p2g_ws<GATHER, 1><<<s->ws_blocks, WS_CTA, smem_bytes_ws(), s->stream>>>(A);
+      launch_k(s, k_g2p2g_ws<GATHER, 1>, dim3(s->ws_blocks), dim3(WS_CTA), smem_bytes_ws(), A);
     else
-      k_g2p2g_f32<GATHER, 1><<<s->persist_blocks, CTA, smem_bytes_f32(), s->stream>>>(A);
+      launch_k(s, k_g2p2g_f32<GATHER, 1>, dim3(s->persist_blocks), dim3(CTA), smem_bytes_f32(), A);
     s->last_kernel = ws ? 1 : 0;
     return;
   }
@@ -2885,6 +2940,7 @@ int sim_create_body(const smpm_sim_config* cfg, smpm_sim* s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ws, k_g2p2g_ws<true, 1>, WS_CTA, smem_bytes_ws()));
     s->ws_blocks = std::max(1, occ_ws);
     if (const char* fz = std::getenv("SMPM_FUSED")) s->ws_mode = !std::strcmp(fz, "ws") ? 1 : (!std::strcmp(fz, "cta") ? 0 : -1);
+    if (const char* pd = std::getenv("SMPM_PDL")) s->pdl = std::strcmp(pd, "0") != 0;
     ws_cap = 0;
     if (const char* wb = std::getenv("SMPM_WS_BLOCKS")) ws_cap = std::atoi(wb);  // sanitizer runs: many items per CTA
   } else {
@@ -3204,12 +3260,18 @@ int smpm_sim_run(smpm_sim* s, int64_t n, double dt, smpm_step_stats* out, int64_
       const int Sx = s->S;
       rc = scan_and_bin(s, Sx, dt > 0 ? dt : -1.0);
       if (rc) break;
-      kg<<<small_grid(s, 16, 148 * 8), 256, 0, s->stream>>>(s->tab[Sx], s->tab[1 - Sx], s->dstats + Sx, s->dstats + (1 - Sx), s->acc,
-                                         s->gv, gp, s->record, s->bx0, s->bx1, nullptr, s->gforce);
+      if (launch_k(s, kg, dim3(small_grid(s, 16, 148 * 8)), dim3(256), 0, s->tab[Sx], s->tab[1 - Sx],
+                   s->dstats + Sx, s->dstats + (1 - Sx), s->acc, s->gv, gp, int(s->record), s->bx0, s->bx1,
+                   static_cast<unsigned long long*>(nullptr), s->gforce) != cudaSuccess) {
+        rc = set_err(SMPM_ERR_CUDA, "batched step launch failed");
+        break;
+      }
       rc = launch_fused(s, true, 1);
       if (rc) break;
-      k_step_record<<<1, 32, 0, s->stream>>>(s->dhalt, s->dhalt + 1, s->dring, s->dstats + Sx, s->dstats + s->S);
-      if (cudaGetLastError() != cudaSuccess) rc = set_err(SMPM_ERR_CUDA, "batched step launch failed");
+      if (launch_k(s, k_step_record, dim3(1), dim3(32), 0, static_cast<const uint32_t*>(s->dhalt), s->dhalt + 1,
+                   s->dring, static_cast<const DevStats*>(s->dstats + Sx),
+                   static_cast<const DevStats*>(s->dstats + s->S)) != cudaSuccess)
+        rc = set_err(SMPM_ERR_CUDA, "batched step launch failed");
     }
     s->batching = false;
     CK(cudaEventRecord(s->ev[3], s->stream));
