@@ -27,7 +27,8 @@
 // A works on item i+1 while S scatters item i, so neither waits for the other
 // at a CTA-wide barrier; the only intra-role barrier is the A-side one that
 // publishes the landed velocity arena.  Named barriers: FULL[b] = 1 + b,
-// EMPTY[b] = 3 + b (512 threads: 256 arrive, 256 sync), A-side 5 (256).
+// EMPTY[b] = 3 + b (512 threads: 256 arrive, 256 sync), producer-only 5 and
+// consumer-only 6 (256 each); barrier 0 (__syncthreads) only before the split.
 
 #ifndef SMPM_WS_STATS
 #define SMPM_WS_STATS 0
