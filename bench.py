@@ -85,6 +85,9 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.nvml = self._nvml_handle()
+            nv, h = self.nvml
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self._sample()  # one sample at the start even of a sub-millisecond region
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
             return self
@@ -100,16 +103,18 @@ class ClockSampler:
             self.proc = None
         return self
 
-    def _poll(self):
+    def _sample(self):
         nv, h = self.nvml
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((float(sm), float(self.max_mhz), int(rs)))
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _poll(self):
         while not self.stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((float(sm), float(mx), int(rs)))
-            except Exception:  # noqa: BLE001
-                pass
+            self._sample()
             self.stop.wait(0.005)
 
     def _read(self):
@@ -120,6 +125,7 @@ class ClockSampler:
         self.stop.set()
         if self.nvml:
             self.t.join(timeout=2)
+            self._sample()  # and one at the end
         if self.proc:
             self.proc.terminate()
             try:
