@@ -244,8 +244,9 @@ class DistributedSimulation:
         # capacity: local particles + arrivals (slabs rebalance slowly)
         cap_mig = int(migrant_capacity or max(4096, n // 8))
         self._cap_mig = cap_mig
+        self._cap_store = n + 4 * cap_mig  # particle storage slots (live + holes + arrivals)
         self.sim = Simulation(particles, config, materials, boundaries, record_conservation=record_conservation,
-                              block_capacity=block_capacity, particle_capacity=n + 4 * cap_mig,
+                              block_capacity=block_capacity, particle_capacity=self._cap_store,
                               slab=(int(bounds[0]), int(bounds[1]), int(pid_base), cap_mig),
                               host_sync="on_access")  # the local set changes size with migration
         self._h = self.sim._h
@@ -472,17 +473,23 @@ class DistributedSimulation:
         lo = int(bx.min()) if bx.size else 0
         hist = np.bincount(bx - lo, minlength=1) if bx.size else np.zeros(0, np.int64)
         objs = [None] * self.tr.world
-        dist.all_gather_object(objs, (lo, hist, tuple(self.bounds)), group=self.tr.group)
+        stored = int(self.lib.smpm_sim_num_stored(self._h))
+        dist.all_gather_object(objs, (lo, hist, tuple(self.bounds), self._cap_mig, self._cap_store, stored),
+                               group=self.tr.group)
         g_lo = min(o[0] for o in objs if o[1].size)
         g_hi = max(o[0] + o[1].size for o in objs if o[1].size)
         total = np.zeros(g_hi - g_lo, dtype=np.int64)
-        for o_lo, o_hist, _ in objs:
+        for o_lo, o_hist, *_ in objs:
             if o_hist.size:
                 total[o_lo - g_lo:o_lo - g_lo + o_hist.size] += o_hist
         cum = np.cumsum(total)
         old = [o[2] for o in objs]
         world = self.tr.world
         cuts = []
+        def left_of(f):  # particles in blocks < f
+            f = np.asarray(f)
+            return cum[np.clip(f - g_lo - 1, 0, cum.size - 1)] * (f > g_lo)
+
         for r in range(1, world):
             target = r * cum[-1] / world
             # face f: blocks < f go left; choose the f whose left count is nearest the target
@@ -493,8 +500,21 @@ class DistributedSimulation:
             if faces.size == 0:
                 cuts.append(int(old[r][0]))
                 continue
-            left = cum[np.clip(faces - g_lo - 1, 0, cum.size - 1)] * (faces > g_lo)
-            cuts.append(int(faces[np.argmin(np.abs(left - target))]))
+            left = left_of(faces)
+            # a face moves only as far as the sender's migrant buffer and the
+            # receiver's particle storage allow in one step (half of each, so
+            # the particles that drift across meanwhile still fit); a large
+            # imbalance is then levelled over several steps
+            moved = left - left_of(old[r][0])
+            send_cap = np.where(moved > 0, objs[r][3], objs[r - 1][3])  # moved > 0: rank r -> r - 1
+            recv = np.where(moved > 0, r - 1, r)
+            room = np.array([objs[q][4] - objs[q][5] for q in recv], dtype=float)
+            ok = (np.abs(moved) <= 0.5 * send_cap) & (np.abs(moved) <= 0.5 * room)
+            if not ok.any():
+                cuts.append(int(old[r][0]))
+                continue
+            cand = faces[ok]
+            cuts.append(int(cand[np.argmin(np.abs(left[ok] - target))]))
         new = [(INT32_MIN if r == 0 else cuts[r - 1], INT32_MAX if r == world - 1 else cuts[r]) for r in range(world)]
         if new == [tuple(b) for b in old]:
             return

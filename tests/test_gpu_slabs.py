@@ -153,3 +153,54 @@ def test_drifting_slabs_rebalance(tmp_path):
     v[d["pid"]] = d["v"]
     assert np.abs(x - x1).max() < 1e-6 * np.abs(x1).max()
     assert np.abs(v - v1).max() < 1e-4 * np.abs(v1).max()
+
+
+def _landslide_worker(rank, world, port, outdir, cap):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_28525_b200 import scenes
+    from paper_2605_28525_b200.slabs import DistributedSimulation
+
+    slab = scenes.landslide_slabs(world, fraction=0.02)[rank]
+    sc = scenes.landslide(fraction=0.02, columns=(slab[2], slab[3]))
+    per_col = sc.particles.n // max(1, slab[3] - slab[2])
+    sim = DistributedSimulation(sc.particles, sc.config, sc.materials, sc.boundaries, (slab[0], slab[1]),
+                                pid_base=slab[2] * per_col, migrant_capacity=cap)
+    counts = [sc.particles.n]
+    for _ in range(6):
+        sim.step()
+        counts.append(int(sim.local_counts[rank]))
+    if rank == 0:
+        np.savez(os.path.join(outdir, "ls.npz"), rebalances=sim.rebalances, counts=np.array(counts),
+                 n=sum(int(c) for c in sim.local_counts))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cap", [None, 2_000_000], ids=["default_buffers", "large_buffers"])
+def test_imbalanced_landslide_slabs_rebalance_within_capacity(tmp_path, cap):
+    """The bench's slab setup on a small release (bench.py --gpus N --scale
+    0.02: 17 lattice columns on rank 0, 3 on rank 1; one block of x holds
+    ~0.8M particles).  A face moves only as far as the sender's migrant buffer
+    and the receiver's storage allow: with the default buffers (n / 8) no move
+    fits and the run continues unbalanced (it used to overflow the migrant
+    buffer: a capacity error); with buffers for a block the faces move."""
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_landslide_worker, args=(2, port, str(tmp_path), cap), nprocs=2, join=True)
+    d = np.load(tmp_path / "ls.npz")
+    assert int(d["n"]) == 2_020_000  # nobody lost
+    c = d["counts"]
+    if cap is None:
+        assert int(d["rebalances"]) == 0
+    else:
+        assert int(d["rebalances"]) >= 1
+        assert c[-1] < c[0]  # rank 0 handed particles over
