@@ -502,14 +502,14 @@ class DistributedSimulation:
                 continue
             left = left_of(faces)
             # a face moves only as far as the sender's migrant buffer and the
-            # receiver's particle storage allow in one step (half of each, so
+            # receiver's particle storage allow in one step (80 % of each, so
             # the particles that drift across meanwhile still fit); a large
             # imbalance is then levelled over several steps
             moved = left - left_of(old[r][0])
             send_cap = np.where(moved > 0, objs[r][3], objs[r - 1][3])  # moved > 0: rank r -> r - 1
             recv = np.where(moved > 0, r - 1, r)
             room = np.array([objs[q][4] - objs[q][5] for q in recv], dtype=float)
-            ok = (np.abs(moved) <= 0.5 * send_cap) & (np.abs(moved) <= 0.5 * room)
+            ok = (np.abs(moved) <= 0.8 * send_cap) & (np.abs(moved) <= 0.8 * room)
             if not ok.any():
                 cuts.append(int(old[r][0]))
                 continue

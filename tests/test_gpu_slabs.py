@@ -186,9 +186,9 @@ def _landslide_worker(rank, world, port, outdir, cap):
 def test_imbalanced_landslide_slabs_rebalance_within_capacity(tmp_path, cap):
     """The bench's slab setup on a small release (bench.py --gpus N --scale
     0.02: 17 lattice columns on rank 0, 3 on rank 1; one block of x holds
-    ~0.8M particles).  A face moves only as far as the sender's migrant buffer
-    and the receiver's storage allow: with the default buffers (n / 8) no move
-    fits and the run continues unbalanced (it used to overflow the migrant
+    ~0.8M particles).  A face moves only as far as 80 % of the sender's
+    migrant buffer and of the receiver's free storage allow: with the default
+    buffers (n / 8) no move fits and the run continues unbalanced (it used to overflow the migrant
     buffer: a capacity error); with buffers for a block the faces move."""
     import torch.multiprocessing as mp
 
